@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 packet-filter hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config data|grid|function|adversarial|oracle]
+    python bench.py --impl reference ...     # the CPU arm (oracle C port, all host cores)
+
+One step = one pass of the hot path over one batch: every packet of this
+rank's share of the workload classified (first-match index + verdict +
+comparison counters) against the whole ruleset (data-parallel / grid /
+adversarial / oracle configs) or against this rank's rule shard followed by
+the per-packet MIN all-reduce (function-parallel).  Inputs are resident in
+HBM when the timed region starts; L2 (126 MB) is flushed between timed steps
+by writing a 256 MiB buffer.  Each step is timed with CUDA events on the
+launching stream; steps are bracketed by a barrier + synchronize; the job
+time is the MAX over ranks.  Rank 0 prints ONE JSON line.
+
+The default config is BASELINE.json configs[1] (data-parallel, 10K rules,
+64Mi packets sharded over the GPUs: total work fixed -> "strong" scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+K_OPS = 10  # int32 ops per rule test: 5 fields x (compare + combine), SURVEY.md 8(d)
+INT32_LANES_PER_SM_CLK = 128  # 4 SMSP x 32 lanes, issue bound across ALU + FMA pipes
+PKT_BYTES, OUT_BYTES = 16, 4  # algorithmic HBM bytes per packet: uint4 in, uint32 index out
+
+
+def load_peaks() -> dict:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int) -> None:
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.thread is not None:
+                self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_arm(w, sample: int, threads: int = 0) -> dict:
+    """The reference path on the host cores: the oracle's C restatement of
+    scan_range (data-parallel over packets, all host threads) on the first
+    ``sample`` packets of the same workload."""
+    import numpy as np
+    from oracle import oracle
+    if w.name == "adversarial":
+        rules = oracle.adversarial_rules(w.rules)
+        pk = oracle.adversarial_traffic(w.packets)
+        pk = {k: v[:sample] for k, v in pk.items()}
+    else:
+        rules = oracle.gen_ruleset(w.rules, 1)
+        pk = oracle.gen_traffic_uniform(sample, 2)
+    nthreads = threads or oracle.max_threads()
+    t0 = time.perf_counter()
+    if w.model == "function":
+        first, comps, total, _ = oracle.engine_run(rules, pk, "data", 1, nthreads)
+    else:
+        first = oracle.scan_range(rules, pk, 0, w.rules, nthreads)
+        comps = oracle.sequential_comparisons(first, w.rules)
+    dt = time.perf_counter() - t0
+    return {"value": sample / dt / 1e6, "unit": "Mpps", "cores": nthreads, "kind": "port",
+            "sample": f"{sample} packets of the {w.name} workload x {w.rules} rules "
+                      f"(oracle/fw_oracle.c orc_scan_range, pthreads over packets)",
+            "seconds": dt, "comparisons": int(np.asarray(comps).sum())}
+
+
+def run_reference(args, w, world, rank) -> None:
+    if rank != 0:
+        return
+    sample = args.cpu_sample or {"oracle": 100_000, "data": 400_000, "grid": 400_000,
+                                 "function": 200_000, "adversarial": 20_000}[w.name]
+    sample = min(sample, w.packets)
+    runs = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_arm(w, sample)
+        if i >= args.warmup:
+            runs.append(r)
+    val = statistics.median(r["value"] for r in runs)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Mpps", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(r["seconds"] for r in runs) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (reference generators: rules seed 1, packets seed 2)",
+        "config": {"workload": w.description, "rules": w.rules, "packets": sample,
+                   "parallelism": "cpu threads"},
+        "cpu_baseline": {k: runs[0][k] for k in ("kind", "cores", "sample")} | {"value": val, "unit": "Mpps"},
+        "e2e": {"value": val, "unit": "Mpps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "Mpackets/sec vs rule count at 1/2/4/8 B200; % of HBM/INT32 roofline"
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="data", choices=("data", "grid", "function", "adversarial", "oracle"))
+    ap.add_argument("--packets", type=int, default=0, help="override the workload's packet count")
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ks", type=int, default=0)
+    ap.add_argument("--tile", type=int, default=0)
+    args = ap.parse_args()
+
+    from paper_1312_4188_b200 import workloads
+    w = workloads.WORKLOADS[args.config]
+    if args.packets:
+        w = workloads.Workload(w.name, w.rules, args.packets, w.model, w.description)
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        run_reference(args, w, world, rank)
+        return 0
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1312_4188_b200 import _native, parallel
+    from paper_1312_4188_b200.classifier import CompiledRuleset
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.ks:
+        _native.set_tuning("ks", args.ks)
+    if args.tile:
+        _native.set_tuning("tile", args.tile)
+    peaks = load_peaks()
+    dev = torch.device(f"cuda:{local}")
+    info = parallel.RankInfo(rank, world)
+
+    # ---------------------------------------------------------- workload
+    cols = workloads.rule_columns(w)
+    compiled = CompiledRuleset.from_columns(cols, device=local)
+    R = compiled.num_rules
+    if w.model == "function":
+        p_lo, p_hi = 0, w.packets                       # packets replicated
+        r_lo, r_hi = parallel.rule_shard(R, info)       # rules sharded
+    else:
+        p_lo, p_hi = parallel.packet_shard(w.packets, info)  # packets sharded
+        r_lo, r_hi = 0, R
+    pkts = workloads.packets(w, p_lo, p_hi - p_lo, local)
+    n = len(pkts)
+    first = torch.empty(n, dtype=torch.int32, device=dev)
+    comps = torch.empty(n, dtype=torch.int32, device=dev)
+    verdict = torch.empty(n, dtype=torch.uint8, device=dev)
+    stats = torch.zeros(2, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        stats.zero_()
+        if w.model == "function":
+            _native.check(_native.lib().pfw_accumulator_init(n, first.data_ptr(), comps.data_ptr(),
+                                                             stream.cuda_stream), "init")
+            compiled.scan_partition_accumulate(pkts, r_lo, r_hi, first, comps, stats,
+                                               stream=stream.cuda_stream)
+            parallel.function_parallel_combine(first, comps, None)
+        else:
+            compiled.scan_range_device(pkts, r_lo, r_hi, first=first, comps=comps, verdict=verdict,
+                                       stats=stats, stream=stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    barrier()
+    # algorithmic work of one step: sum of this rank's (per-task) comparisons
+    local_comps = int(stats[0].item())
+
+    times = []
+    launches0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        barrier()
+    launches = _native.launch_count() - launches0
+    total_ms = sum(times)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(n if w.model != "function" else 0), float(local_comps)],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    job_ms = float(t.item())
+    pk_per_step = w.packets if w.model == "function" else int(tot[0].item())
+    value = pk_per_step * args.steps / (job_ms / 1e3) / 1e6
+    ms_per_step = job_ms / args.steps
+
+    # --- roofline for the dominant kernel (the scan), per GPU
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    clk = float(peaks.get("sm_max_mhz", 1965.0))
+    int_peak = sms * INT32_LANES_PER_SM_CLK * clk * 1e6 / 1e12  # T int-ops/s
+    avg_launch_s = (total_ms / args.steps) / 1e3
+    achieved = local_comps * K_OPS / avg_launch_s / 1e12
+    hbm_achieved = n * (PKT_BYTES + OUT_BYTES) / avg_launch_s / 1e9
+    roof = {
+        "bound": "int32", "achieved": round(achieved, 3), "peak": round(int_peak, 3), "unit": "Tops/s",
+        "frac": round(achieved / int_peak, 4), "traffic": None,
+        "ops_per_rule_test": K_OPS, "rule_tests_per_launch": local_comps,
+        "peak_source": f"derived: {sms} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x "
+                       f"sm_max_mhz {clk:.0f} ({peaks['_source']})",
+        "hbm": {"achieved": round(hbm_achieved, 2), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": round(hbm_achieved / float(peaks.get("hbm_gbs", 6536.4)), 5),
+                "bytes_per_packet": PKT_BYTES + OUT_BYTES},
+    }
+
+    # --- end to end through the C-ABI with host buffers (pfw_classify_host)
+    e2e = None
+    if not args.no_e2e and w.model != "function":
+        host_pk = pkts.data.cpu().pin_memory()
+        h_first = torch.empty(n, dtype=torch.int32).pin_memory()
+        h_verd = torch.empty(n, dtype=torch.uint8).pin_memory()
+        h_stats = torch.zeros(2, dtype=torch.int64)
+        lib = _native.lib()
+
+        def e2e_step():
+            _native.check(lib.pfw_classify_host(compiled.handle, host_pk.data_ptr(), n, h_first.data_ptr(),
+                                                h_verd.data_ptr(), h_stats.data_ptr(), 1 << 22),
+                          "pfw_classify_host")
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        # parity of the e2e path with the device-resident path (bit-exact)
+        if not torch.equal(h_first, first.cpu()):
+            raise SystemExit("e2e first-match indices differ from the device path")
+        barrier()
+        et = []
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            et.append(time.perf_counter() - t0)
+        tt = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": pk_per_step * args.steps / float(tt.item()) / 1e6, "unit": "Mpps",
+               "h2d_bytes_per_step": n * PKT_BYTES, "d2h_bytes_per_step": n * 5,
+               "api": "pfw_classify_host (C-ABI, pinned host buffers, 4Mi-packet chunks, 2 streams)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sample = args.cpu_sample or {"oracle": 100_000, "data": 400_000, "grid": 400_000,
+                                     "function": 100_000, "adversarial": 20_000}[w.name]
+        c = cpu_arm(w, min(sample, w.packets))
+        cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "Mpps", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic: generate_ruleset(RulesetGenParams(R, seed=1)) x generate_traffic("
+                    "TrafficProfile(N, seed=2)), generated on the GPU bit-exactly",
+            "config": {"workload": w.description, "rules": R, "packets": w.packets,
+                       "packets_per_gpu": n, "model": w.model,
+                       "parallelism": f"{'rule' if w.model == 'function' else 'packet'}-sharded x{world}",
+                       "l2": "flushed between timed steps (256 MiB write)",
+                       "kernel": _native.version()},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": launches,
+            "comparisons_per_packet": round(local_comps / max(n, 1), 2) if w.model != "function" else None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

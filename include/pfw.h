@@ -1,0 +1,149 @@
+/*
+ * pfw.h -- C-ABI of the B200 packet-filter hot path (libpfw.so).
+ *
+ * The reference (parafw, pure Python) has no FFI; these entry points are the
+ * functions its classify path would bind if its numpy inner loop were moved
+ * behind a native library.  Each one names the reference interface it
+ * replaces (/root/reference/pkg/src/parafw/<file>:<line>).
+ * shows the ctypes binding a parafw maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no exceptions cross the ABI.  Every call
+ *    returns PFW_OK (0) or a PFW_ERR_* code; pfw_last_error() describes the
+ *    last failure on the calling thread.
+ *  - "d_" pointers are device pointers on the ruleset's device, "h_" pointers
+ *    are host pointers (pinned memory gives overlapped copies).
+ *  - stream arguments are cudaStream_t passed as void* (NULL = legacy stream).
+ *  - Device calls are asynchronous on the stream unless stated otherwise.
+ *  - Packets are 16-byte records: {src_ip, dst_ip, (src_port<<16)|dst_port,
+ *    proto} (uint32 x4), the packet-batch layout that replaces the 5-column
+ *    PacketArrays (classifier.py:62-95).
+ *  - A first-match index is a uint32 global rule index; PFW_NO_MATCH means no
+ *    rule in the scanned window matched (the reference's -1, default deny).
+ *    PFW_NO_MATCH is INT32_MAX so that it is also the identity of an int32 or
+ *    uint32 MIN reduction (the function-parallel combine).
+ *  - A handle is bound to one device and is not reentrant (mirrors Engine,
+ *    engines.py:221-228); different handles may be driven concurrently.
+ */
+#ifndef PFW_H
+#define PFW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PFW_NO_MATCH 0x7FFFFFFFu
+#define PFW_MAX_RULES 0x7FFFFFFE
+
+enum {
+    PFW_OK = 0,
+    PFW_ERR_INVALID = 1, /* bad argument (the reference's ValueError / ConfigError) */
+    PFW_ERR_CUDA = 2,    /* CUDA runtime failure */
+    PFW_ERR_NOMEM = 3,   /* device or host allocation failure */
+    PFW_ERR_GENERATION = 4 /* traffic generation failed */
+};
+
+typedef struct pfw_ruleset *pfw_ruleset_t;
+
+/* Description of the last failure on this thread ("" if none). */
+const char *pfw_last_error(void);
+
+/* Library / build information: "pfw <version> sm_100a ...". */
+const char *pfw_version(void);
+
+/* Number of visible CUDA devices (0 when no GPU); never fails. */
+int pfw_device_count(void);
+
+/* Ruleset packing + upload.  Replaces CompiledRuleset.__init__
+ * (classifier.py:120-134): takes exactly its ten SoA columns (proto u8 with
+ * ANY = 0, CIDR base/mask u32, inclusive port lo/hi u16, action_accept u8)
+ * and uploads the device form (range-test SoA) once. Rules
+ * whose base has host bits outside the mask, or whose port range is inverted,
+ * can never match under the reference predicate (model.py:222-230) and are
+ * packed as never-matching.  n_rules may be 0. */
+int pfw_ruleset_create(int device, int64_t n_rules, const uint8_t *proto,
+                       const uint32_t *src_base, const uint32_t *src_mask,
+                       const uint16_t *sport_lo, const uint16_t *sport_hi,
+                       const uint32_t *dst_base, const uint32_t *dst_mask,
+                       const uint16_t *dport_lo, const uint16_t *dport_hi,
+                       const uint8_t *action_accept, pfw_ruleset_t *out);
+int pfw_ruleset_destroy(pfw_ruleset_t h);
+int64_t pfw_ruleset_size(pfw_ruleset_t h);
+int pfw_ruleset_device(pfw_ruleset_t h);
+
+/* Host packet packing.  Replaces PacketArrays.from_packets
+ * (classifier.py:75-83) for column input: writes n 16-byte records. */
+int pfw_pack_packets_host(int64_t n, const uint8_t *proto, const uint32_t *src_ip,
+                          const uint16_t *src_port, const uint32_t *dst_ip,
+                          const uint16_t *dst_port, void *h_out);
+
+/* First-match scan over the rule window [lo, hi).  Replaces
+ * CompiledRuleset.scan_range (classifier.py:146-162) and the sequential /
+ * data-parallel comparison accounting (classifier.py:200, engines.py:312):
+ *   d_first[i]   = earliest matching global rule index in [lo, hi) or
+ *                  PFW_NO_MATCH (lo >= hi or n == 0: all PFW_NO_MATCH / no-op)
+ *   d_comps[i]   = first - lo + 1, or hi - lo on a miss     (nullable)
+ *   d_verdict[i] = 1 iff a rule matched and it is ACCEPT    (nullable)
+ *   d_stats[0] += sum of comps, d_stats[1] = max(d_stats[1], max comps)
+ *                                                            (nullable) */
+int pfw_scan_range(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
+                   uint32_t *d_first, uint32_t *d_comps, uint8_t *d_verdict,
+                   uint64_t *d_stats, void *stream);
+
+/* One partition of the function-parallel / hybrid models.  Replaces a
+ * _scan_partitions task + its share of _combine_rows (engines.py:349-369):
+ *   d_first[i]  = min(d_first[i], partition-local first match)
+ *   d_comps[i] += per-task comparisons (local - lo + 1, or hi - lo)
+ *   d_stats[0] += sum of per-task comparisons, d_stats[1] = max(..., per-task)
+ * d_first must start at PFW_NO_MATCH and d_comps at 0 (pfw_accumulator_init). */
+int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts,
+                                  int64_t n, uint32_t *d_first, uint32_t *d_comps,
+                                  uint64_t *d_stats, void *stream);
+int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *stream);
+
+/* Verdicts from final first-match indices (classifier.py:175-185). */
+int pfw_verdicts(pfw_ruleset_t h, const uint32_t *d_first, int64_t n, uint8_t *d_verdict,
+                 void *stream);
+
+/* Per-packet minimum over partitions (engines.py:202-212) for W rows of n
+ * indices laid out row-major: d_out[i] = min_w d_rows[w*n + i]. */
+int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d_out, void *stream);
+
+/* End-to-end sequential classification with HOST buffers.  Replaces
+ * classify_batch_sequential (classifier.py:192-209) minus object building:
+ * copies packets in `chunk`-packet pieces to the device, scans [0, R) and
+ * copies first-match indices / verdicts back, overlapping copies with the
+ * kernels on two streams.  Synchronous: all outputs are complete on return.
+ * h_verdict and h_stats ([sum, max] comparisons) are nullable. */
+int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *h_first,
+                      uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk);
+
+/* Bit-exact UNIFORM traffic generation on the device.  Replaces
+ * generate_traffic(TrafficProfile(...)) with match_mode UNIFORM
+ * (traffic.py:117-130, 148-160; rng.py:31-62): the pinned xorshift64* stream
+ * is split across threads by GF(2) jump-ahead.  Synchronous (it checks for
+ * the rare bounded-draw rejection and repairs the stream exactly).  Writes n
+ * packed packets to d_out. */
+int pfw_generate_traffic(int device, uint64_t seed, int64_t n, int proto, uint32_t src_base,
+                         int src_plen, uint32_t dst_base, int dst_plen, int sport_lo,
+                         int sport_hi, int dport_lo, int dport_hi, void *d_out, void *stream);
+
+/* Same stream, packets [first_packet, first_packet + n) only (one rank's
+ * shard of a global batch, engines.py:307 / partition_bounds).  first_packet
+ * > 0 requires power-of-two port spans, where every packet is exactly four
+ * draws; the default wildcard profile qualifies. */
+int pfw_generate_traffic_at(int device, uint64_t seed, int64_t first_packet, int64_t n, int proto,
+                            uint32_t src_base, int src_plen, uint32_t dst_base, int dst_plen,
+                            int sport_lo, int sport_hi, int dport_lo, int dport_hi, void *d_out,
+                            void *stream);
+
+/* Launch-count / tuning introspection (bench + tests). */
+int64_t pfw_launch_count(void);
+int pfw_set_tuning(const char *key, int64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFW_H */

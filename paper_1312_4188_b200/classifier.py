@@ -1,0 +1,380 @@
+"""First-match classification on the GPU (drop-in for ``parafw.classifier``).
+
+Public surface mirrors /root/reference/pkg/src/parafw/classifier.py:
+``ClassifyStats``, ``CompiledRuleset``, ``PacketArrays``, ``classify``,
+``classify_batch_sequential``, ``compile_ruleset``.  The difference is where
+the data lives and who scans it:
+
+* ``CompiledRuleset`` keeps the reference's ten SoA columns on the host
+  (classifier.py:120-134) and uploads the range-test form to the GPU once
+  (``pfw_ruleset_create``).
+* ``PacketArrays`` is a device-resident batch of 16-byte packet records
+  {src_ip, dst_ip, sport<<16|dport, proto} (the packet-batch layout that
+  replaces the five numpy columns of classifier.py:62-95).
+* ``CompiledRuleset.scan_range`` (classifier.py:146-162) is one launch of the
+  packet x rule grid kernel; comparison counts and stats are produced in the
+  kernel epilogue (classifier.py:200-208).
+
+There is no CPU fallback: without libpfw.so or a CUDA device every scan
+raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+import weakref
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from ._native import NO_MATCH, check
+from .model import Action, MatchResult, Packet, Protocol, Ruleset
+
+__all__ = [
+    "ClassifyStats",
+    "CompiledRuleset",
+    "PacketArrays",
+    "classify",
+    "classify_batch_sequential",
+    "compile_ruleset",
+    "NO_MATCH",
+]
+
+RULE_COLUMNS = ("proto", "src_base", "src_mask", "sport_lo", "sport_hi",
+                "dst_base", "dst_mask", "dport_lo", "dport_hi", "action_accept")
+_RULE_DTYPES = (np.uint8, np.uint32, np.uint32, np.uint16, np.uint16,
+                np.uint32, np.uint32, np.uint16, np.uint16, np.bool_)
+PACKET_COLUMNS = ("proto", "src_ip", "src_port", "dst_ip", "dst_port")
+_PACKET_DTYPES = (np.uint8, np.uint32, np.uint16, np.uint32, np.uint16)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+def _default_device() -> int:
+    _native.require_device()
+    torch = _torch()
+    return torch.cuda.current_device()
+
+
+def _stream(device: int) -> int:
+    torch = _torch()
+    return int(torch.cuda.current_stream(device).cuda_stream)
+
+
+@dataclass(frozen=True)
+class ClassifyStats:
+    """Aggregate counters of one run (classifier.py:38-51)."""
+
+    total_comparisons: int
+    packets_processed: int
+    wall_time_ns: int
+    max_worker_comparisons: int
+
+
+def classify(ruleset: Ruleset, packet: Packet) -> MatchResult:
+    """First match with early exit, default deny (classifier.py:54-59), on the GPU."""
+    compiled = compile_ruleset(ruleset)
+    first = compiled.scan_range(PacketArrays.from_packets([packet], compiled.device), 0,
+                                compiled.num_rules)
+    idx = int(first[0])
+    if idx < 0:
+        return MatchResult(Action.DROP, None, compiled.num_rules)
+    return MatchResult(Action.ACCEPT if compiled.action_accept[idx] else Action.DROP, idx, idx + 1)
+
+
+# ----------------------------------------------------------------- packets
+
+class PacketArrays:
+    """Device-resident packet batch: ``data`` is an int32 CUDA tensor [n, 4]
+    holding {src_ip, dst_ip, sport<<16|dport, proto} per packet.
+
+    Column attributes (``proto``, ``src_ip`` ...) are host numpy views
+    decoded on demand, for compatibility with classifier.py:62-95.
+    """
+
+    __slots__ = ("data",)
+
+    def __init__(self, data) -> None:
+        torch = _torch()
+        if not isinstance(data, torch.Tensor) or data.dtype != torch.int32 or data.dim() != 2 \
+                or data.shape[1] != 4:
+            raise TypeError("PacketArrays wraps an int32 tensor of shape [n, 4]")
+        if not data.is_cuda:
+            raise _native.NativeUnavailable("PacketArrays must live on a CUDA device")
+        if not data.is_contiguous():
+            data = data.contiguous()
+        self.data = data
+
+    # --- constructors
+    @staticmethod
+    def pack_host(proto, src_ip, src_port, dst_ip, dst_port) -> np.ndarray:
+        """Host [n, 4] uint32 records from the five reference columns."""
+        n = len(proto)
+        out = np.empty((n, 4), dtype=np.uint32)
+        out[:, 0] = np.asarray(src_ip, dtype=np.uint32)
+        out[:, 1] = np.asarray(dst_ip, dtype=np.uint32)
+        out[:, 2] = (np.asarray(src_port, dtype=np.uint32) << 16) | np.asarray(dst_port, dtype=np.uint32)
+        out[:, 3] = np.asarray(proto, dtype=np.uint32)
+        return out
+
+    @classmethod
+    def from_host_records(cls, records: np.ndarray, device: int | None = None) -> "PacketArrays":
+        torch = _torch()
+        device = _default_device() if device is None else device
+        rec = np.ascontiguousarray(records, dtype=np.uint32).reshape(-1, 4)
+        t = torch.from_numpy(rec.view(np.int32))
+        if rec.shape[0] >= (1 << 16):
+            t = t.pin_memory()
+        return cls(t.to(f"cuda:{device}", non_blocking=True))
+
+    @classmethod
+    def from_columns(cls, proto, src_ip, src_port, dst_ip, dst_port,
+                     device: int | None = None) -> "PacketArrays":
+        return cls.from_host_records(cls.pack_host(proto, src_ip, src_port, dst_ip, dst_port), device)
+
+    @classmethod
+    def from_packets(cls, packets: Sequence[Packet], device: int | None = None) -> "PacketArrays":
+        """classifier.py:75-83, packed straight into 16-byte records."""
+        n = len(packets)
+        rec = np.empty((n, 4), dtype=np.uint32)
+        if n:
+            rec[:, 0] = np.fromiter((p.src_ip for p in packets), dtype=np.uint32, count=n)
+            rec[:, 1] = np.fromiter((p.dst_ip for p in packets), dtype=np.uint32, count=n)
+            rec[:, 2] = np.fromiter(((p.src_port << 16) | p.dst_port for p in packets), dtype=np.uint32,
+                                    count=n)
+            rec[:, 3] = np.fromiter((int(p.proto) for p in packets), dtype=np.uint32, count=n)
+        return cls.from_host_records(rec, device)
+
+    @classmethod
+    def empty(cls, n: int, device: int | None = None) -> "PacketArrays":
+        torch = _torch()
+        device = _default_device() if device is None else device
+        return cls(torch.empty((n, 4), dtype=torch.int32, device=f"cuda:{device}"))
+
+    # --- views
+    def __len__(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def device(self) -> int:
+        return int(self.data.device.index)
+
+    def slice(self, start: int, stop: int) -> "PacketArrays":
+        return PacketArrays(self.data[start:stop])
+
+    def host_records(self) -> np.ndarray:
+        return self.data.cpu().numpy().view(np.uint32)
+
+    def columns(self) -> dict:
+        rec = self.host_records()
+        return {
+            "proto": rec[:, 3].astype(np.uint8),
+            "src_ip": rec[:, 0].copy(),
+            "src_port": (rec[:, 2] >> 16).astype(np.uint16),
+            "dst_ip": rec[:, 1].copy(),
+            "dst_port": (rec[:, 2] & 0xFFFF).astype(np.uint16),
+        }
+
+    def to_packets(self) -> list[Packet]:
+        c = self.columns()
+        return [Packet(i, Protocol(int(pr)), int(s), int(sp), int(d), int(dp))
+                for i, (pr, s, sp, d, dp) in enumerate(zip(c["proto"].tolist(), c["src_ip"].tolist(),
+                                                          c["src_port"].tolist(), c["dst_ip"].tolist(),
+                                                          c["dst_port"].tolist()))]
+
+    def __getattr__(self, name):
+        if name in PACKET_COLUMNS:
+            return self.columns()[name]
+        raise AttributeError(name)
+
+
+# ------------------------------------------------------------------- rules
+
+def _rule_columns(ruleset: Ruleset) -> dict:
+    """classifier.py:120-134 column form of a Ruleset."""
+    n = len(ruleset)
+    rs = ruleset.rules
+    return {
+        "proto": np.fromiter((int(r.proto) for r in rs), dtype=np.uint8, count=n),
+        "src_base": np.fromiter((r.src.base for r in rs), dtype=np.uint32, count=n),
+        "src_mask": np.fromiter((r.src.mask for r in rs), dtype=np.uint32, count=n),
+        "sport_lo": np.fromiter((r.sport.lo for r in rs), dtype=np.uint16, count=n),
+        "sport_hi": np.fromiter((r.sport.hi for r in rs), dtype=np.uint16, count=n),
+        "dst_base": np.fromiter((r.dst.base for r in rs), dtype=np.uint32, count=n),
+        "dst_mask": np.fromiter((r.dst.mask for r in rs), dtype=np.uint32, count=n),
+        "dport_lo": np.fromiter((r.dport.lo for r in rs), dtype=np.uint16, count=n),
+        "dport_hi": np.fromiter((r.dport.hi for r in rs), dtype=np.uint16, count=n),
+        "action_accept": np.fromiter((r.action is Action.ACCEPT for r in rs), dtype=np.bool_, count=n),
+    }
+
+
+class CompiledRuleset:
+    """Ruleset uploaded to one GPU (drop-in for classifier.py:98-185)."""
+
+    def __init__(self, ruleset: Ruleset | None = None, device: int | None = None, *,
+                 columns: dict | None = None) -> None:
+        if (ruleset is None) == (columns is None):
+            raise TypeError("pass exactly one of ruleset or columns")
+        if columns is not None:
+            cols = {f: np.ascontiguousarray(columns[f], dtype=d) for f, d in zip(RULE_COLUMNS, _RULE_DTYPES)}
+        else:
+            cols = _rule_columns(ruleset)
+        n = len(cols["proto"])
+        for f in RULE_COLUMNS:
+            if len(cols[f]) != n:
+                raise ValueError(f"rule column {f} has {len(cols[f])} entries, expected {n}")
+            setattr(self, f, cols[f])
+        self.num_rules = n
+        self.device = _default_device() if device is None else int(device)
+        acc_u8 = cols["action_accept"].astype(np.uint8)
+        self._keep = [cols[f] for f in RULE_COLUMNS[:-1]] + [acc_u8]
+        h = ctypes.c_void_p()
+        check(_native.lib().pfw_ruleset_create(self.device, n, *[a.ctypes.data for a in self._keep],
+                                                ctypes.byref(h)), "pfw_ruleset_create")
+        self._h = h
+        self._finalizer = weakref.finalize(self, _native.lib().pfw_ruleset_destroy, h)
+
+    @classmethod
+    def from_columns(cls, columns: dict, device: int | None = None) -> "CompiledRuleset":
+        return cls(None, device, columns=columns)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def close(self) -> None:
+        self._finalizer()
+
+    def columns(self) -> dict:
+        return {f: getattr(self, f) for f in RULE_COLUMNS}
+
+    # --- device scans -----------------------------------------------------
+    def _packets(self, pkts) -> PacketArrays:
+        if isinstance(pkts, PacketArrays):
+            if pkts.device != self.device:
+                return PacketArrays(pkts.data.to(f"cuda:{self.device}"))
+            return pkts
+        return PacketArrays.from_packets(pkts, self.device)
+
+    def scan_range_device(self, pkts: PacketArrays, lo: int, hi: int, *, first=None, comps=None,
+                          verdict=None, stats=None, stream: int | None = None):
+        """One kernel launch: int32 first-match tensor (NO_MATCH = none) on the device.
+        Optional device outputs: ``comps`` (int32), ``verdict`` (uint8), ``stats``
+        (int64 [2]: += sum of comps, max= max comps)."""
+        torch = _torch()
+        pkts = self._packets(pkts)
+        n = len(pkts)
+        if first is None:
+            first = torch.empty(n, dtype=torch.int32, device=pkts.data.device)
+        lo, hi = int(lo), int(hi)
+        if lo > hi:
+            lo = hi
+        st = _stream(self.device) if stream is None else stream
+        check(_native.lib().pfw_scan_range(self._h, lo, hi, _ptr(pkts.data), n, _ptr(first),
+                                           _ptr(comps), _ptr(verdict), _ptr(stats), st),
+              "pfw_scan_range")
+        return first
+
+    def scan_partition_accumulate(self, pkts: PacketArrays, lo: int, hi: int, first, comps, stats=None,
+                                  stream: int | None = None) -> None:
+        """Function-parallel / hybrid partition task folded into running min / sums."""
+        st = _stream(self.device) if stream is None else stream
+        check(_native.lib().pfw_scan_partition_accumulate(self._h, int(lo), int(hi), _ptr(pkts.data),
+                                                          len(pkts), _ptr(first), _ptr(comps),
+                                                          _ptr(stats), st),
+              "pfw_scan_partition_accumulate")
+
+    def verdicts_device(self, first, verdict=None, stream: int | None = None):
+        torch = _torch()
+        if verdict is None:
+            verdict = torch.empty(first.numel(), dtype=torch.uint8, device=first.device)
+        st = _stream(self.device) if stream is None else stream
+        check(_native.lib().pfw_verdicts(self._h, _ptr(first), first.numel(), _ptr(verdict), st),
+              "pfw_verdicts")
+        return verdict
+
+    # --- reference-shaped API ---------------------------------------------
+    def scan_range(self, pkts, lo: int, hi: int) -> np.ndarray:
+        """Earliest matching rule index in [lo, hi) per packet, or -1 (int64, host)."""
+        pkts = self._packets(pkts)
+        if len(pkts) == 0:
+            return np.full(0, -1, dtype=np.int64)
+        first = self.scan_range_device(pkts, lo, hi)
+        return first_to_host(first)
+
+    def first_match(self, packet: Packet) -> int:
+        return int(self.scan_range([packet], 0, self.num_rules)[0])
+
+    def build_results(self, first: np.ndarray, comparisons: np.ndarray) -> list[MatchResult]:
+        """MatchResults from first-match indices and counts (classifier.py:175-185)."""
+        accept = self.action_accept
+        acc, drop = Action.ACCEPT, Action.DROP
+        out = []
+        append = out.append
+        for idx, comps in zip(first.tolist(), comparisons.tolist()):
+            if idx < 0:
+                append(MatchResult(drop, None, comps))
+            else:
+                append(MatchResult(acc if accept[idx] else drop, idx, comps))
+        return out
+
+
+def first_to_host(first) -> np.ndarray:
+    """int32 device first-match tensor -> int64 host array with -1 for no match."""
+    f = first.cpu().numpy().astype(np.int64)
+    f[f == NO_MATCH] = -1
+    return f
+
+
+# one compiled copy per live Ruleset object (the reference recompiles per
+# call; uploading 100K rules per call would dominate small batches)
+_cache: dict[tuple[int, int], tuple] = {}
+
+
+def compile_ruleset(ruleset: Ruleset, device: int | None = None) -> CompiledRuleset:
+    device = _default_device() if device is None else int(device)
+    key = (id(ruleset), device)
+    hit = _cache.get(key)
+    if hit is not None and hit[0]() is ruleset:
+        return hit[1]
+    compiled = CompiledRuleset(ruleset, device)
+    try:
+        ref = weakref.ref(ruleset, lambda _r, k=key: _cache.pop(k, None))
+    except TypeError:
+        return compiled
+    _cache[key] = (ref, compiled)
+    return compiled
+
+
+def classify_batch_sequential(ruleset: Ruleset, packets) -> tuple[list[MatchResult], ClassifyStats]:
+    """Classify a batch in packet order (classifier.py:192-209) on the GPU.
+
+    ``packets`` may be a sequence of Packet (drop-in) or a PacketArrays."""
+    torch = _torch()
+    start = time.perf_counter_ns()
+    compiled = compile_ruleset(ruleset)
+    pkts = compiled._packets(packets)
+    n = len(pkts)
+    R = compiled.num_rules
+    if n == 0:
+        return [], ClassifyStats(0, 0, time.perf_counter_ns() - start, 0)
+    dev = pkts.data.device
+    comps = torch.empty(n, dtype=torch.int32, device=dev)
+    stats = torch.zeros(2, dtype=torch.int64, device=dev)
+    first = compiled.scan_range_device(pkts, 0, R, comps=comps, stats=stats)
+    first_h = first_to_host(first)
+    comps_h = comps.cpu().numpy().astype(np.int64)
+    st = stats.cpu().numpy()
+    results = compiled.build_results(first_h, comps_h)
+    wall = time.perf_counter_ns() - start
+    return results, ClassifyStats(int(st[0]), n, wall, int(st[1]))

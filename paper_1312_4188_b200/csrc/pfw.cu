@@ -1,0 +1,993 @@
+// pfw.cu -- B200 (sm_100a) packet-filter hot path behind the C-ABI of include/pfw.h.
+//
+// Reference semantics (parafw, /root/reference/pkg/src/parafw):
+//   rule predicate            model.py:222-230, classifier.py:136-144
+//   first-match in [lo,hi)    classifier.py:146-162
+//   comparison accounting     classifier.py:200, engines.py:312, engines.py:366-368
+//   min-combine               engines.py:202-212
+//   traffic generator         rng.py:31-62, traffic.py:117-130, 148-160
+//
+// Design (DESIGN.md has the full rationale and rooflines):
+//   * every rule field is a range test  (x - lo) <=u width  on 32-bit lanes:
+//       src/dst CIDR  -> lo = base, width = ~mask      (x & mask) == base
+//       ports         -> lo = lo,   width = hi - lo    lo <= x <= hi
+//       proto         -> ANY: width = ~0; else lo = proto, width = 0
+//     one IMAD (FMA pipe, "x*1 + (-lo)") + one ISETP (ALU pipe) per field, so
+//     a 5-field rule test is 10 integer ops split evenly over the two pipes.
+//   * packet x rule grid: a CTA owns a tile of packets in shared memory; all
+//     of its warps hold the same 32*KS-rule stage in registers (lane l holds
+//     rules stage+32j+l, j < KS) and split the tile's LIVE packets.  Per packet
+//     each lane evaluates its KS rules, one __any_sync decides whether the
+//     stage hit, and __ballot_sync/__ffs over the sub-chunks in order yields
+//     the lowest matching index.  Stages run in rule order and matched packets
+//     retire from the live list after every stage, so no packet is tested
+//     past the stage that holds its first match (early exit at 32*KS rules).
+//   * stage rules are TMA-bulk-copied (cp.async.bulk + mbarrier) into a
+//     double-buffered shared-memory ring while the previous stage computes.
+//   * persistent grid (SMs x resident CTAs), tiles handed out by an atomic
+//     counter (dynamic load balance: tiles differ in work by >10x).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdarg.h>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <atomic>
+
+#include "../../include/pfw.h"
+
+#define PFW_VERSION "0.1.0"
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int set_err(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t e__ = (expr);                                                        \
+        if (e__ != cudaSuccess)                                                          \
+            return set_err(PFW_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e__), \
+                           __FILE__, __LINE__);                                          \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ---------------------------------------------------------- rule encoding
+// Device rule table: SoA of NF words, field f of rule r at rules[f * rpad + r].
+constexpr int NF = 10;
+enum { F_SRC_NLO = 0, F_SRC_W, F_DST_NLO, F_DST_W, F_SP_NLO, F_SP_W, F_DP_NLO, F_DP_W,
+       F_PR_NLO, F_PR_W };
+constexpr uint32_t NEVER_NLO = 0x80000000u;  // proto + 2^31 != 0 for every u8 proto
+constexpr uint32_t NEVER_W = 0u;
+
+// Tunables (pfw_set_tuning)
+int g_ks = 8;            // rules per lane per stage (stage = 32*KS rules)
+int g_tile = 2048;       // packets per CTA tile
+int g_ctas_per_sm = 0;   // 0 = occupancy query
+int g_force_imad = 1;    // route the subtract through IMAD (FMA pipe)
+
+}  // namespace
+
+struct pfw_ruleset {
+    int device;
+    int64_t n;       // rules
+    int64_t rpad;    // padded row length (multiple of 32, >= n + max stage)
+    uint32_t *d_rules = nullptr;   // NF * rpad
+    uint8_t *d_accept = nullptr;   // rpad
+    unsigned int *d_counter = nullptr;  // tile counters (one per launch slot)
+    int sms = 148;
+    // e2e workspace
+    void *d_ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaStream_t streams[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done = nullptr;
+    int counter_slot = 0;
+};
+
+namespace {
+
+constexpr int COUNTER_SLOTS = 1024;
+
+// ================================================================ kernels
+
+struct ScanParams {
+    const uint32_t *rules;
+    const uint8_t *accept;
+    int64_t rpad;
+    int64_t lo, hi;
+    const uint4 *pkts;
+    int64_t n;
+    uint32_t *first;
+    uint32_t *comps;
+    uint8_t *verdict;
+    unsigned long long *stats;
+    unsigned int *tile_counter;
+    int64_t ntiles;
+    int tile;
+    uint32_t one;  // runtime 1: keeps ptxas from folding x*1+c into IADD3
+};
+
+__device__ __forceinline__ uint32_t sub_fma(uint32_t x, uint32_t one, uint32_t nlo) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(one), "r"(nlo));
+    return d;
+}
+
+template <bool FMA>
+__device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src, uint32_t dst,
+                                          uint32_t sp, uint32_t dp, uint32_t pr, uint32_t one) {
+    uint32_t a, b, c, d, e;
+    if (FMA) {
+        a = sub_fma(src, one, r[F_SRC_NLO]);
+        b = sub_fma(dst, one, r[F_DST_NLO]);
+        c = sub_fma(sp, one, r[F_SP_NLO]);
+        d = sub_fma(dp, one, r[F_DP_NLO]);
+        e = sub_fma(pr, one, r[F_PR_NLO]);
+    } else {
+        a = src + r[F_SRC_NLO];
+        b = dst + r[F_DST_NLO];
+        c = sp + r[F_SP_NLO];
+        d = dp + r[F_DP_NLO];
+        e = pr + r[F_PR_NLO];
+    }
+    return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (c <= r[F_SP_W]) & (d <= r[F_DP_W]) &
+           (e <= r[F_PR_W]);
+}
+
+constexpr int BLOCK = 256;
+constexpr int NWARPS = BLOCK / 32;
+
+// shared-memory layout for a tile of T packets (T <= 65535)
+__host__ __device__ constexpr size_t smem_bytes(int T, int KS) {
+    return (size_t)T * 16      // packet (src, dst, sport, dport)
+           + (size_t)T * 4     // proto
+           + (size_t)T * 4     // first
+           + (size_t)T * 2 * 2 // live lists (ping-pong)
+           + 2 * (size_t)NF * 32 * KS * 4  // rule stage ring (2 buffers)
+           + 64;               // mbarriers + counters
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *sdst, const void *gsrc, unsigned bytes,
+                                             uint64_t *bar) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+    unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(gsrc), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Issue the TMA copies of one stage (NF field rows of 32*KS words each).
+// Stage start `s` is 32-aligned relative to the table (the kernel aligns lo
+// down and masks the rules below lo), so every row copy is 16B aligned.
+template <int KS>
+__device__ __forceinline__ void issue_stage(const ScanParams &p, int64_t s, uint32_t *buf,
+                                            uint64_t *bar) {
+    constexpr unsigned ROW = 32 * KS * 4;
+    mbar_expect_tx(bar, NF * ROW);
+#pragma unroll
+    for (int f = 0; f < NF; f++) tma_bulk_g2s(buf + f * 32 * KS, p.rules + f * p.rpad + s, ROW, bar);
+}
+
+template <int KS, bool ACC, bool FMA>
+__global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int T = p.tile;
+    uint4 *s_pk = reinterpret_cast<uint4 *>(smem_raw);
+    uint32_t *s_rules = reinterpret_cast<uint32_t *>(s_pk + T);      // 2 * NF * 32 * KS
+    uint32_t *s_pr = s_rules + 2 * NF * 32 * KS;
+    uint32_t *s_first = s_pr + T;
+    uint16_t *s_liveA = reinterpret_cast<uint16_t *>(s_first + T);
+    uint16_t *s_liveB = s_liveA + T;
+    uint64_t *s_bar = reinterpret_cast<uint64_t *>(
+        (reinterpret_cast<uintptr_t>(s_liveB + T) + 15) & ~uintptr_t(15));
+    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t one = p.one;
+    constexpr int STAGE = 32 * KS;
+    // Stages are aligned to 32 rules of the table; rules below lo in the
+    // first stage are masked to never-match.
+    const int64_t s0 = p.lo & ~int64_t(31);
+
+    unsigned long long st_sum = 0;
+    unsigned st_max = 0;
+
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unsigned phase = 0u;  // bit b = parity of barrier b
+    __syncthreads();
+
+    for (;;) {
+        if (tid == 0) s_misc[1] = (int)atomicAdd(p.tile_counter, 1u);
+        __syncthreads();
+        const int64_t tile = s_misc[1];
+        if (tile >= p.ntiles) break;
+        const int64_t base = tile * T;
+        const int cnt = (int)((p.n - base) < T ? (p.n - base) : (int64_t)T);
+
+        // prefetch the first stage while the packet tile loads
+        const bool any_rules = p.lo < p.hi;
+        if (tid == 0 && any_rules) {
+            fence_proxy_async();
+            issue_stage<KS>(p, s0, s_rules, &s_bar[0]);
+        }
+
+        for (int i = tid; i < cnt; i += BLOCK) {
+            uint4 v = __ldg(p.pkts + base + i);
+            s_pk[i] = make_uint4(v.x, v.y, v.z >> 16, v.z & 0xFFFFu);
+            s_pr[i] = v.w;
+            s_first[i] = PFW_NO_MATCH;
+            s_liveA[i] = (uint16_t)i;
+        }
+        __syncthreads();
+
+        int nlive = any_rules ? cnt : 0;
+        uint16_t *live = s_liveA, *live2 = s_liveB;
+        int buf = 0, kc = 0;
+        int64_t s = s0;
+        while (nlive > 0 && s < p.hi) {
+            // prefetch next stage into the other buffer (its previous reader
+            // finished: every warp passed the __syncthreads that ended it)
+            const int64_t sn = s + STAGE;
+            if (tid == 0 && sn < p.hi) {
+                fence_proxy_async();
+                issue_stage<KS>(p, sn, s_rules + (buf ^ 1) * NF * STAGE, &s_bar[buf ^ 1]);
+            }
+            mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
+
+            // stage rules -> registers (lane l: rules s + 32j + l)
+            const uint32_t *sr = s_rules + buf * NF * STAGE;
+            uint32_t r[KS][NF];
+#pragma unroll
+            for (int j = 0; j < KS; j++) {
+#pragma unroll
+                for (int f = 0; f < NF; f++) r[j][f] = sr[f * STAGE + j * 32 + lane];
+                const int64_t ri = s + j * 32 + lane;
+                if (ri < p.lo || ri >= p.hi) {
+                    r[j][F_PR_NLO] = NEVER_NLO;
+                    r[j][F_PR_W] = NEVER_W;
+                }
+            }
+
+            for (int i = warp; i < nlive; i += NWARPS) {
+                const int q = live[i];
+                const uint4 v = s_pk[q];
+                const uint32_t pr = s_pr[q];
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < KS; j++) any |= rule_test<FMA>(r[j], v.x, v.y, v.z, v.w, pr, one);
+                if (__any_sync(0xFFFFFFFFu, any)) {
+                    // slow path (once per packet): re-evaluate with the other
+                    // arithmetic form so the compiler cannot CSE it with the
+                    // fast path and keep KS predicates alive across the vote
+#pragma unroll
+                    for (int j = 0; j < KS; j++) {
+                        const unsigned b =
+                            __ballot_sync(0xFFFFFFFFu, rule_test<!FMA>(r[j], v.x, v.y, v.z, v.w, pr, one));
+                        if (b) {
+                            if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
+                            break;
+                        }
+                    }
+                }
+            }
+            // live counter alternates between two slots so that resetting one
+            // never races with a late reader of the previous stage's count
+            int *ctr = &s_misc[kc ? 2 : 0];
+            if (tid == 0) *ctr = 0;
+            __syncthreads();
+            // retire matched packets: compact the live list (order is free)
+            for (int i0 = 0; i0 < nlive; i0 += BLOCK) {
+                const int i = i0 + tid;
+                int q = 0;
+                bool keep = false;
+                if (i < nlive) {
+                    q = live[i];
+                    keep = s_first[q] == PFW_NO_MATCH;
+                }
+                const unsigned b = __ballot_sync(0xFFFFFFFFu, keep);
+                int off = 0;
+                if (lane == 0 && b) off = atomicAdd(ctr, __popc(b));
+                off = __shfl_sync(0xFFFFFFFFu, off, 0);
+                if (keep) live2[off + __popc(b & ((1u << lane) - 1u))] = (uint16_t)q;
+            }
+            __syncthreads();
+            nlive = *ctr;
+            kc ^= 1;
+            uint16_t *t = live;
+            live = live2;
+            live2 = t;
+            buf ^= 1;
+            s = sn;
+        }
+        // drain a prefetched stage that was not consumed (tile ended early)
+        if (any_rules && s < p.hi) {
+            mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
+        }
+
+        // epilogue: results, comparisons, verdicts, stats
+        const uint32_t span = (uint32_t)(p.hi > p.lo ? p.hi - p.lo : 0);
+        for (int i = tid; i < cnt; i += BLOCK) {
+            const uint32_t f = s_first[i];
+            const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.lo + 1) : span;
+            const int64_t g = base + i;
+            if (ACC) {
+                const uint32_t old = p.first[g];
+                p.first[g] = min(old, f);
+                p.comps[g] += c;
+            } else {
+                p.first[g] = f;
+                if (p.comps) p.comps[g] = c;
+                if (p.verdict) p.verdict[g] = (f != PFW_NO_MATCH) ? p.accept[f] : (uint8_t)0;
+            }
+            st_sum += c;
+            st_max = max(st_max, c);
+        }
+        __syncthreads();
+    }
+    if (p.stats) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            st_sum += __shfl_xor_sync(0xFFFFFFFFu, st_sum, o);
+            st_max = max(st_max, __shfl_xor_sync(0xFFFFFFFFu, st_max, o));
+        }
+        if (lane == 0) {
+            if (st_sum) atomicAdd(&p.stats[0], st_sum);
+            if (st_max) atomicMax(&p.stats[1], (unsigned long long)st_max);
+        }
+    }
+}
+
+__global__ void acc_init_kernel(int64_t n, uint32_t *first, uint32_t *comps) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        first[i] = PFW_NO_MATCH;
+        if (comps) comps[i] = 0;
+    }
+}
+
+__global__ void verdict_kernel(const uint8_t *accept, const uint32_t *first, int64_t n,
+                               uint8_t *verdict) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = first[i];
+        verdict[i] = f != PFW_NO_MATCH ? accept[f] : 0;
+    }
+}
+
+__global__ void combine_min_kernel(const uint32_t *rows, int64_t nrows, int64_t n, uint32_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t m = PFW_NO_MATCH;
+        for (int64_t w = 0; w < nrows; w++) m = min(m, rows[w * n + i]);
+        out[i] = m;
+    }
+}
+
+// ============================================================ generator
+// xorshift64* is GF(2)-linear in its state, so the state after k steps is
+// M^k s.  Matrices are stored as 64 columns: col[i] = M e_i.
+struct Mat64 {
+    uint64_t c[64];
+};
+
+__host__ __device__ inline uint64_t matvec(const uint64_t *col, uint64_t s) {
+    uint64_t r = 0;
+#pragma unroll 8
+    for (int i = 0; i < 64; i++)
+        if ((s >> i) & 1) r ^= col[i];
+    return r;
+}
+
+inline uint64_t xs_step_state(uint64_t x) {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    return x;
+}
+
+Mat64 mat_step() {
+    Mat64 m;
+    for (int i = 0; i < 64; i++) m.c[i] = xs_step_state(1ULL << i);
+    return m;
+}
+Mat64 mat_mul(const Mat64 &a, const Mat64 &b) {  // a*b
+    Mat64 r;
+    for (int i = 0; i < 64; i++) r.c[i] = matvec(a.c, b.c[i]);
+    return r;
+}
+Mat64 mat_pow(Mat64 m, uint64_t k) {
+    Mat64 r;
+    for (int i = 0; i < 64; i++) r.c[i] = 1ULL << i;
+    while (k) {
+        if (k & 1) r = mat_mul(r, m);
+        m = mat_mul(m, m);
+        k >>= 1;
+    }
+    return r;
+}
+
+constexpr int GEN_BLOCK = 128;
+constexpr int GEN_PER_THREAD = 16;
+constexpr int GEN_PER_BLOCK = GEN_BLOCK * GEN_PER_THREAD;  // packets per block
+constexpr int GEN_LOG_BLOCK = 7;
+__constant__ uint64_t c_jump[GEN_LOG_BLOCK][64];  // (M^(4*GEN_PER_THREAD))^(2^b)
+
+struct GenParams {
+    uint32_t proto, src_base, dst_base;
+    uint64_t sspan, dspan;  // powers of two <= 2^32
+    uint32_t sp_lo, dp_lo;
+    uint64_t sp_n, dp_n;    // port counts (1..65536)
+    uint64_t sp_lim, dp_lim;  // rejection limits (0 = power of two, never rejects)
+};
+
+__device__ __forceinline__ uint64_t xs_next(uint64_t &x) {
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    return x * 0x2545F4914F6CDD1DULL;
+}
+
+__global__ void __launch_bounds__(GEN_BLOCK) gen_kernel(GenParams g, const uint64_t *block_state,
+                                                        int64_t start, int64_t n, uint4 *out,
+                                                        unsigned long long *reject_at) {
+    __shared__ uint4 stage[GEN_PER_BLOCK];
+    const int64_t b0 = start + (int64_t)blockIdx.x * GEN_PER_BLOCK;
+    uint64_t x = block_state[blockIdx.x];
+    for (int bit = 0; bit < GEN_LOG_BLOCK; bit++)
+        if ((threadIdx.x >> bit) & 1) x = matvec(c_jump[bit], x);
+    const int64_t p0 = b0 + (int64_t)threadIdx.x * GEN_PER_THREAD;
+    bool rej = false;
+    int64_t rej_at = 0;
+    for (int k = 0; k < GEN_PER_THREAD; k++) {
+        const uint64_t d0 = xs_next(x), d1 = xs_next(x), d2 = xs_next(x), d3 = xs_next(x);
+        if (!rej && ((g.sp_lim && d1 >= g.sp_lim) || (g.dp_lim && d3 >= g.dp_lim))) {
+            rej = true;
+            rej_at = p0 + k;
+        }
+        uint4 v;
+        v.x = g.src_base + (uint32_t)(d0 & (g.sspan - 1));
+        const uint32_t sp = g.sp_lo + (uint32_t)(d1 % g.sp_n);
+        v.y = g.dst_base + (uint32_t)(d2 & (g.dspan - 1));
+        const uint32_t dp = g.dp_lo + (uint32_t)(d3 % g.dp_n);
+        v.z = (sp << 16) | dp;
+        v.w = g.proto;
+        stage[threadIdx.x * GEN_PER_THREAD + k] = v;
+    }
+    if (rej && rej_at < n) atomicMin(reject_at, (unsigned long long)rej_at);
+    __syncthreads();
+    for (int i = threadIdx.x; i < GEN_PER_BLOCK; i += GEN_BLOCK) {
+        const int64_t q = b0 + i;
+        if (q < n) out[q] = stage[i];
+    }
+}
+
+uint64_t host_seed_state(uint64_t seed) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    return z ? z : 0x9E3779B97F4A7C15ULL;
+}
+
+uint64_t host_next(uint64_t &x) {
+    x = xs_step_state(x);
+    return x * 0x2545F4914F6CDD1DULL;
+}
+
+uint64_t host_randbelow(uint64_t &x, uint64_t n) {
+    const uint64_t rem = (0 - n) % n;
+    if (rem == 0) return host_next(x) % n;
+    const uint64_t lim = 0 - rem;
+    for (;;) {
+        const uint64_t r = host_next(x);
+        if (r < lim) return r % n;
+    }
+}
+
+bool stage_fits(int T, int KS, int dev) {
+    int maxsm = 0;
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return smem_bytes(T, KS) <= (size_t)maxsm;
+}
+
+template <int KS, bool ACC, bool FMA>
+int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, cudaStream_t st) {
+    ScanParams p = p0;
+    const size_t sm = smem_bytes(p.tile, KS);
+    auto kern = scan_kernel<KS, ACC, FMA>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int occ = g_ctas_per_sm;
+    if (occ <= 0) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, sm));
+        if (occ < 1) occ = 1;
+    }
+    int64_t grid = (int64_t)h->sms * occ;
+    if (grid > p.ntiles) grid = p.ntiles;
+    if (grid < 1) grid = 1;
+    unsigned int *ctr = h->d_counter + h->counter_slot;
+    h->counter_slot = (h->counter_slot + 1) % COUNTER_SLOTS;
+    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), st));
+    p.tile_counter = ctr;
+    kern<<<(unsigned)grid, BLOCK, sm, st>>>(p);
+    CUDA_TRY(cudaGetLastError());
+    g_launches++;
+    return PFW_OK;
+}
+
+template <bool ACC, bool FMA>
+int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
+    switch (g_ks) {
+        case 2: return launch_scan_t<2, ACC, FMA>(h, p, st);
+        case 4: return launch_scan_t<4, ACC, FMA>(h, p, st);
+        case 8: return launch_scan_t<8, ACC, FMA>(h, p, st);
+        default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4 or 8)", g_ks);
+    }
+}
+
+int launch_scan(pfw_ruleset *h, bool acc, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
+                uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
+                cudaStream_t st) {
+    if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
+    if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count %lld", (long long)n);
+    if (lo < 0 || hi < 0) return set_err(PFW_ERR_INVALID, "negative rule window [%lld, %lld)",
+                                         (long long)lo, (long long)hi);
+    if (hi > h->n) return set_err(PFW_ERR_INVALID, "rule window end %lld beyond ruleset of %lld",
+                                  (long long)hi, (long long)h->n);
+    if (n == 0) return PFW_OK;
+    if (!d_pkts || !first) return set_err(PFW_ERR_INVALID, "null packet or output pointer");
+    if (acc && !comps) return set_err(PFW_ERR_INVALID, "accumulate needs a comps buffer");
+    if (lo > hi) lo = hi;  // empty window: scan_range returns all -1
+    ScanParams p{};
+    p.rules = h->d_rules;
+    p.accept = h->d_accept;
+    p.rpad = h->rpad;
+    p.lo = lo;
+    p.hi = hi;
+    p.pkts = reinterpret_cast<const uint4 *>(d_pkts);
+    p.n = n;
+    p.first = first;
+    p.comps = comps;
+    p.verdict = verdict;
+    p.stats = reinterpret_cast<unsigned long long *>(stats);
+    p.tile = g_tile;
+    p.ntiles = (n + p.tile - 1) / p.tile;
+    p.one = 1;
+    DeviceGuard g(h->device);
+    if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
+    if (acc) return g_force_imad ? launch_scan_ks<true, true>(h, p, st) : launch_scan_ks<true, false>(h, p, st);
+    return g_force_imad ? launch_scan_ks<false, true>(h, p, st) : launch_scan_ks<false, false>(h, p, st);
+}
+
+int grid_for(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 8) g = 148 * 8;
+    return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char *pfw_last_error(void) { return g_err.c_str(); }
+
+const char *pfw_version(void) {
+    return "pfw " PFW_VERSION " sm_100a range-test packet x rule grid (KS=2/4/8) + TMA bulk stage ring";
+}
+
+int pfw_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int64_t pfw_launch_count(void) { return g_launches.load(); }
+
+int pfw_set_tuning(const char *key, int64_t value) {
+    if (!key) return set_err(PFW_ERR_INVALID, "null key");
+    if (!strcmp(key, "ks")) {
+        if (value != 2 && value != 4 && value != 8) return set_err(PFW_ERR_INVALID, "ks must be 2, 4 or 8");
+        g_ks = (int)value;
+    } else if (!strcmp(key, "tile")) {
+        if (value < 256 || value > 8192 || value % 256) return set_err(PFW_ERR_INVALID, "tile must be a multiple of 256 in [256, 8192]");
+        g_tile = (int)value;
+    } else if (!strcmp(key, "ctas_per_sm")) {
+        if (value < 0 || value > 8) return set_err(PFW_ERR_INVALID, "ctas_per_sm in [0, 8]");
+        g_ctas_per_sm = (int)value;
+    } else if (!strcmp(key, "force_imad")) {
+        g_force_imad = value != 0;
+    } else {
+        return set_err(PFW_ERR_INVALID, "unknown tuning key '%s'", key);
+    }
+    return PFW_OK;
+}
+
+int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32_t *src_base,
+                       const uint32_t *src_mask, const uint16_t *sport_lo, const uint16_t *sport_hi,
+                       const uint32_t *dst_base, const uint32_t *dst_mask, const uint16_t *dport_lo,
+                       const uint16_t *dport_hi, const uint8_t *accept, pfw_ruleset_t *out) {
+    if (!out) return set_err(PFW_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    if (n < 0 || n > PFW_MAX_RULES) return set_err(PFW_ERR_INVALID, "rule count %lld out of range", (long long)n);
+    if (n > 0 && (!proto || !src_base || !src_mask || !sport_lo || !sport_hi || !dst_base ||
+                  !dst_mask || !dport_lo || !dport_hi || !accept))
+        return set_err(PFW_ERR_INVALID, "null rule column");
+    int ndev = pfw_device_count();
+    if (device < 0 || device >= ndev)
+        return set_err(PFW_ERR_CUDA, "CUDA device %d not available (%d visible)", device, ndev);
+    DeviceGuard g(device);
+    if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", device);
+
+    pfw_ruleset *h = new pfw_ruleset();
+    h->device = device;
+    h->n = n;
+    // pad: one full max-size stage (8 * 32 rules) past the last 32-aligned row
+    h->rpad = ((n + 31) / 32) * 32 + 8 * 32;
+    std::vector<uint32_t> host((size_t)NF * h->rpad);
+    std::vector<uint8_t> acc((size_t)h->rpad, 0);
+    for (int64_t r = 0; r < h->rpad; r++) {
+        uint32_t w[NF];
+        bool never = r >= n;
+        if (!never) {
+            const uint32_t sb = src_base[r], sm = src_mask[r], db = dst_base[r], dm = dst_mask[r];
+            // (ip & mask) == base can only hold if base has no bits outside mask
+            if ((sb & ~sm) || (db & ~dm)) never = true;
+            if (sport_lo[r] > sport_hi[r] || dport_lo[r] > dport_hi[r]) never = true;
+            w[F_SRC_NLO] = 0u - sb;
+            w[F_SRC_W] = ~sm;
+            w[F_DST_NLO] = 0u - db;
+            w[F_DST_W] = ~dm;
+            w[F_SP_NLO] = 0u - (uint32_t)sport_lo[r];
+            w[F_SP_W] = (uint32_t)sport_hi[r] - (uint32_t)sport_lo[r];
+            w[F_DP_NLO] = 0u - (uint32_t)dport_lo[r];
+            w[F_DP_W] = (uint32_t)dport_hi[r] - (uint32_t)dport_lo[r];
+            if (proto[r] == 0) {  // Protocol.ANY (model.py:68)
+                w[F_PR_NLO] = 0u;
+                w[F_PR_W] = 0xFFFFFFFFu;
+            } else {
+                w[F_PR_NLO] = 0u - (uint32_t)proto[r];
+                w[F_PR_W] = 0u;
+            }
+            acc[r] = accept[r] ? 1 : 0;
+        }
+        if (never) {
+            for (int f = 0; f < NF; f++) w[f] = 0;
+            w[F_PR_NLO] = NEVER_NLO;
+            w[F_PR_W] = NEVER_W;
+        }
+        for (int f = 0; f < NF; f++) host[(size_t)f * h->rpad + r] = w[f];
+    }
+    cudaError_t e = cudaMalloc(&h->d_rules, host.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_accept, acc.size());
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_counter, COUNTER_SLOTS * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_rules, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_accept, acc.data(), acc.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) {
+        const int code = e == cudaErrorMemoryAllocation ? PFW_ERR_NOMEM : PFW_ERR_CUDA;
+        pfw_ruleset_destroy(h);
+        return set_err(code, "ruleset upload failed: %s", cudaGetErrorString(e));
+    }
+    *out = h;
+    return PFW_OK;
+}
+
+int pfw_ruleset_destroy(pfw_ruleset_t h) {
+    if (!h) return PFW_OK;
+    DeviceGuard g(h->device);
+    if (h->d_rules) cudaFree(h->d_rules);
+    if (h->d_accept) cudaFree(h->d_accept);
+    if (h->d_counter) cudaFree(h->d_counter);
+    if (h->d_ws) cudaFree(h->d_ws);
+    for (auto &s : h->streams)
+        if (s) cudaStreamDestroy(s);
+    if (h->ev_done) cudaEventDestroy(h->ev_done);
+    delete h;
+    return PFW_OK;
+}
+
+int64_t pfw_ruleset_size(pfw_ruleset_t h) { return h ? h->n : -1; }
+int pfw_ruleset_device(pfw_ruleset_t h) { return h ? h->device : -1; }
+
+int pfw_pack_packets_host(int64_t n, const uint8_t *proto, const uint32_t *src_ip,
+                          const uint16_t *src_port, const uint32_t *dst_ip,
+                          const uint16_t *dst_port, void *h_out) {
+    if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count");
+    if (n == 0) return PFW_OK;
+    if (!proto || !src_ip || !src_port || !dst_ip || !dst_port || !h_out)
+        return set_err(PFW_ERR_INVALID, "null packet column");
+    uint32_t *o = static_cast<uint32_t *>(h_out);
+    for (int64_t i = 0; i < n; i++) {
+        o[4 * i + 0] = src_ip[i];
+        o[4 * i + 1] = dst_ip[i];
+        o[4 * i + 2] = ((uint32_t)src_port[i] << 16) | dst_port[i];
+        o[4 * i + 3] = proto[i];
+    }
+    return PFW_OK;
+}
+
+int pfw_scan_range(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
+                   uint32_t *d_first, uint32_t *d_comps, uint8_t *d_verdict, uint64_t *d_stats,
+                   void *stream) {
+    return launch_scan(h, false, lo, hi, d_pkts, n, d_first, d_comps, d_verdict, d_stats,
+                       (cudaStream_t)stream);
+}
+
+int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts,
+                                  int64_t n, uint32_t *d_first, uint32_t *d_comps,
+                                  uint64_t *d_stats, void *stream) {
+    return launch_scan(h, true, lo, hi, d_pkts, n, d_first, d_comps, nullptr, d_stats,
+                       (cudaStream_t)stream);
+}
+
+int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *stream) {
+    if (n < 0 || (n > 0 && !d_first)) return set_err(PFW_ERR_INVALID, "bad accumulator arguments");
+    if (n == 0) return PFW_OK;
+    acc_init_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(n, d_first, d_comps);
+    CUDA_TRY(cudaGetLastError());
+    g_launches++;
+    return PFW_OK;
+}
+
+int pfw_verdicts(pfw_ruleset_t h, const uint32_t *d_first, int64_t n, uint8_t *d_verdict,
+                 void *stream) {
+    if (!h || n < 0 || (n > 0 && (!d_first || !d_verdict)))
+        return set_err(PFW_ERR_INVALID, "bad verdict arguments");
+    if (n == 0) return PFW_OK;
+    DeviceGuard g(h->device);
+    verdict_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(h->d_accept, d_first, n, d_verdict);
+    CUDA_TRY(cudaGetLastError());
+    g_launches++;
+    return PFW_OK;
+}
+
+int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d_out, void *stream) {
+    if (rows < 0 || n < 0 || (n > 0 && (!d_out || (rows > 0 && !d_rows))))
+        return set_err(PFW_ERR_INVALID, "bad combine arguments");
+    if (n == 0) return PFW_OK;
+    combine_min_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(d_rows, rows, n, d_out);
+    CUDA_TRY(cudaGetLastError());
+    g_launches++;
+    return PFW_OK;
+}
+
+int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *h_first,
+                      uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
+    if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
+    if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count");
+    if (h_stats) h_stats[0] = h_stats[1] = 0;
+    if (n == 0) return PFW_OK;
+    if (!h_pkts || !h_first) return set_err(PFW_ERR_INVALID, "null host buffer");
+    if (chunk <= 0) chunk = 1 << 22;
+    if (chunk > n) chunk = n;
+    DeviceGuard g(h->device);
+    if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
+    // per-slot layout: packets (16B) + first (4B) + verdict (1B), 2 slots + stats
+    const size_t slot = (size_t)chunk * 21 + 256;
+    const size_t need = 2 * slot + 256;
+    if (h->ws_bytes < need) {
+        if (h->d_ws) cudaFree(h->d_ws);
+        h->d_ws = nullptr;
+        h->ws_bytes = 0;
+        CUDA_TRY(cudaMalloc(&h->d_ws, need));
+        h->ws_bytes = need;
+    }
+    for (auto &s : h->streams)
+        if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    char *ws = static_cast<char *>(h->d_ws);
+    uint64_t *d_stats = reinterpret_cast<uint64_t *>(ws + 2 * slot);
+    CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16, h->streams[0]));
+    cudaEvent_t ev_stats;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_stats, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev_stats, h->streams[0]));
+    CUDA_TRY(cudaStreamWaitEvent(h->streams[1], ev_stats, 0));
+    int rc = PFW_OK;
+    for (int64_t c0 = 0, k = 0; c0 < n && rc == PFW_OK; c0 += chunk, k++) {
+        const int64_t m = (n - c0 < chunk) ? n - c0 : chunk;
+        cudaStream_t st = h->streams[k & 1];
+        char *base = ws + (k & 1) * slot;
+        uint4 *dp = reinterpret_cast<uint4 *>(base);
+        uint32_t *df = reinterpret_cast<uint32_t *>(base + (size_t)chunk * 16);
+        uint8_t *dv = reinterpret_cast<uint8_t *>(base + (size_t)chunk * 20);
+        CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
+                                 cudaMemcpyHostToDevice, st));
+        rc = launch_scan(h, false, 0, h->n, dp, m, df, nullptr, h_verdict ? dv : nullptr,
+                         h_stats ? d_stats : nullptr, st);
+        if (rc != PFW_OK) break;
+        CUDA_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, st));
+        if (h_verdict)
+            CUDA_TRY(cudaMemcpyAsync(h_verdict + c0, dv, m, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->streams[0]));
+    CUDA_TRY(cudaStreamSynchronize(h->streams[1]));
+    cudaEventDestroy(ev_stats);
+    if (rc != PFW_OK) return rc;
+    if (h_stats) CUDA_TRY(cudaMemcpy(h_stats, d_stats, 16, cudaMemcpyDeviceToHost));
+    return PFW_OK;
+}
+
+int pfw_generate_traffic(int device, uint64_t seed, int64_t n, int proto, uint32_t src_base,
+                         int src_plen, uint32_t dst_base, int dst_plen, int sport_lo, int sport_hi,
+                         int dport_lo, int dport_hi, void *d_out, void *stream) {
+    return pfw_generate_traffic_at(device, seed, 0, n, proto, src_base, src_plen, dst_base, dst_plen,
+                                   sport_lo, sport_hi, dport_lo, dport_hi, d_out, stream);
+}
+
+int pfw_generate_traffic_at(int device, uint64_t seed, int64_t first_packet, int64_t n, int proto,
+                            uint32_t src_base, int src_plen, uint32_t dst_base, int dst_plen,
+                            int sport_lo, int sport_hi, int dport_lo, int dport_hi, void *d_out,
+                            void *stream) {
+    if (n < 0 || first_packet < 0) return set_err(PFW_ERR_INVALID, "count and first_packet must be >= 0");
+    if (proto <= 0 || proto > 255) return set_err(PFW_ERR_INVALID, "traffic protocol must be concrete (1..255)");
+    if (src_plen < 0 || src_plen > 32 || dst_plen < 0 || dst_plen > 32)
+        return set_err(PFW_ERR_INVALID, "prefix length outside 0..32");
+    if (sport_lo < 0 || sport_hi > 65535 || sport_lo > sport_hi || dport_lo < 0 ||
+        dport_hi > 65535 || dport_lo > dport_hi)
+        return set_err(PFW_ERR_INVALID, "bad port range");
+    if (first_packet > 0 && (((sport_hi - sport_lo + 1) & (sport_hi - sport_lo)) != 0 ||
+                             ((dport_hi - dport_lo + 1) & (dport_hi - dport_lo)) != 0))
+        return set_err(PFW_ERR_INVALID,
+                       "first_packet > 0 needs power-of-two port spans (then every packet is exactly "
+                       "4 draws and the stream position is known)");
+    if (n == 0) return PFW_OK;
+    if (!d_out) return set_err(PFW_ERR_INVALID, "null output");
+    int ndev = pfw_device_count();
+    if (device < 0 || device >= ndev) return set_err(PFW_ERR_CUDA, "CUDA device %d not available", device);
+    DeviceGuard g(device);
+    cudaStream_t st = (cudaStream_t)stream;
+
+    GenParams gp{};
+    gp.proto = (uint32_t)proto;
+    const uint32_t smask = src_plen ? (uint32_t)(0xFFFFFFFFull << (32 - src_plen)) : 0u;
+    const uint32_t dmask = dst_plen ? (uint32_t)(0xFFFFFFFFull << (32 - dst_plen)) : 0u;
+    gp.src_base = src_base & smask;  // TrafficProfile subnets are normalised CidrMatchers
+    gp.dst_base = dst_base & dmask;
+    gp.sspan = 1ULL << (32 - src_plen);
+    gp.dspan = 1ULL << (32 - dst_plen);
+    gp.sp_lo = (uint32_t)sport_lo;
+    gp.dp_lo = (uint32_t)dport_lo;
+    gp.sp_n = (uint64_t)(sport_hi - sport_lo + 1);
+    gp.dp_n = (uint64_t)(dport_hi - dport_lo + 1);
+    {
+        const uint64_t r1 = (0 - gp.sp_n) % gp.sp_n, r2 = (0 - gp.dp_n) % gp.dp_n;
+        gp.sp_lim = r1 ? 0 - r1 : 0;
+        gp.dp_lim = r2 ? 0 - r2 : 0;
+    }
+    // jump matrices: per-thread jump = M^(4*GEN_PER_THREAD); per-block = M^(4*GEN_PER_BLOCK)
+    static std::mutex mu;
+    static bool ready = false;
+    static Mat64 jblock;
+    static uint64_t jthread[GEN_LOG_BLOCK][64];
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!ready) {
+            Mat64 m = mat_step();
+            Mat64 jt = mat_pow(m, 4ULL * GEN_PER_THREAD);
+            for (int b = 0; b < GEN_LOG_BLOCK; b++) {
+                memcpy(jthread[b], jt.c, sizeof jt.c);
+                jt = mat_mul(jt, jt);
+            }
+            jblock = mat_pow(m, 4ULL * GEN_PER_BLOCK);
+            ready = true;
+        }
+    }
+    static thread_local int uploaded_dev_mask = 0;
+    if (!(uploaded_dev_mask & (1 << device))) {
+        CUDA_TRY(cudaMemcpyToSymbol(c_jump, jthread, sizeof jthread));
+        uploaded_dev_mask |= 1 << device;
+    }
+
+    uint64_t *d_state = nullptr;
+    unsigned long long *d_rej = nullptr;
+    int64_t start = 0;
+    Mat64 m1 = mat_step();
+    uint64_t x = host_seed_state(seed);  // state before packet `start`
+    if (first_packet > 0) x = matvec(mat_pow(m1, 4ULL * (uint64_t)first_packet).c, x);
+    int rc = PFW_OK;
+    int rounds = 0;
+    while (start < n) {
+        const int64_t rem = n - start;
+        const int64_t nblocks = (rem + GEN_PER_BLOCK - 1) / GEN_PER_BLOCK;
+        std::vector<uint64_t> states((size_t)nblocks);
+        uint64_t s = x;
+        for (int64_t b = 0; b < nblocks; b++) {
+            states[(size_t)b] = s;
+            s = matvec(jblock.c, s);
+        }
+        if (d_state) cudaFree(d_state);
+        d_state = nullptr;
+        CUDA_TRY(cudaMalloc(&d_state, states.size() * 8));
+        if (!d_rej) CUDA_TRY(cudaMalloc(&d_rej, 8));
+        CUDA_TRY(cudaMemcpyAsync(d_state, states.data(), states.size() * 8, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaMemsetAsync(d_rej, 0xFF, 8, st));
+        gen_kernel<<<(unsigned)nblocks, GEN_BLOCK, 0, st>>>(gp, d_state, start, n,
+                                                           static_cast<uint4 *>(d_out), d_rej);
+        CUDA_TRY(cudaGetLastError());
+        g_launches++;
+        unsigned long long rej = 0;
+        CUDA_TRY(cudaMemcpyAsync(&rej, d_rej, 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (rej == ~0ULL) break;
+        // A bounded draw was rejected inside packet `rej`: every packet before
+        // it is exact.  Regenerate packet `rej` on the host with the exact
+        // rejection loop (rng.py:54-62), then resume the device stream after it.
+        if (++rounds > 1000000) { rc = set_err(PFW_ERR_GENERATION, "too many rejection repairs"); break; }
+        uint64_t y = matvec(mat_pow(m1, 4ULL * (uint64_t)(rej - start)).c, x);
+        uint4 v;
+        v.x = gp.src_base + (uint32_t)host_randbelow(y, gp.sspan);
+        const uint32_t sp = gp.sp_lo + (uint32_t)host_randbelow(y, gp.sp_n);
+        v.y = gp.dst_base + (uint32_t)host_randbelow(y, gp.dspan);
+        const uint32_t dp = gp.dp_lo + (uint32_t)host_randbelow(y, gp.dp_n);
+        v.z = (sp << 16) | dp;
+        v.w = gp.proto;
+        CUDA_TRY(cudaMemcpyAsync(static_cast<uint4 *>(d_out) + rej, &v, 16, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        start = (int64_t)rej + 1;
+        x = y;
+    }
+    if (d_state) cudaFree(d_state);
+    if (d_rej) cudaFree(d_rej);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,347 @@
+"""GPU parity: the CUDA path (through libpfw.so's C-ABI) against the oracle and
+the reference's golden vectors.  Integer work: every comparison is bit-exact.
+
+Mirrors the reference's own KATs (pkg/tests/test_classifier.py,
+test_engines.py) and adds full-size properties that the oracle cannot
+enumerate.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_rules, golden_traffic
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1312_4188_b200 as pfw  # noqa: E402
+from paper_1312_4188_b200 import _native  # noqa: E402
+from paper_1312_4188_b200.classifier import NO_MATCH, first_to_host  # noqa: E402
+from oracle import oracle  # noqa: E402
+from oracle.oracle import PKT_FIELDS  # noqa: E402
+
+
+def dev_pkts(cols: dict) -> pfw.PacketArrays:
+    return pfw.PacketArrays.from_columns(*[cols[f] for f in PKT_FIELDS], device=0)
+
+
+def compiled(rules: dict) -> pfw.CompiledRuleset:
+    return pfw.CompiledRuleset.from_columns(rules, device=0)
+
+
+@pytest.fixture(autouse=True)
+def _reset_tuning():
+    yield
+    for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1)):
+        _native.set_tuning(k, v)
+
+
+def mk_rule(action, proto, src="*", sport=None, dst="*", dport=None):
+    import ipaddress
+
+    def cidr(spec):
+        if spec == "*":
+            return pfw.CidrMatcher(0, 0)
+        b, _, p = spec.partition("/")
+        return pfw.CidrMatcher(int(ipaddress.IPv4Address(b)), int(p))
+    ports = lambda s: pfw.PortRange(0, 65535) if s is None else pfw.PortRange(*s)  # noqa: E731
+    return pfw.Rule(action, proto, cidr(src), ports(sport), cidr(dst), ports(dport))
+
+
+def mk_packet(pid=0, proto=pfw.Protocol.TCP, sport=5555, dport=80):
+    return pfw.Packet(pid, proto, 0x0A010203, sport, 0x08080808, dport)
+
+
+# ----------------------------------------------------------------- reference KATs
+
+def test_empty_ruleset_default_deny():
+    r = pfw.classify(pfw.Ruleset(), mk_packet())
+    assert (r.verdict, r.matched_index, r.comparisons) == (pfw.Action.DROP, None, 0)
+
+
+def test_first_match_shadows_later_rules():
+    rs = pfw.Ruleset((mk_rule(pfw.Action.DROP, pfw.Protocol.TCP),
+                      mk_rule(pfw.Action.ACCEPT, pfw.Protocol.TCP, dport=(80, 80))))
+    r = pfw.classify(rs, mk_packet(dport=80))
+    assert (r.verdict, r.matched_index, r.comparisons) == (pfw.Action.DROP, 0, 1)
+
+
+def test_no_match_scans_everything():
+    rs = pfw.Ruleset((mk_rule(pfw.Action.ACCEPT, pfw.Protocol.UDP),) * 37)
+    results, stats = pfw.classify_batch_sequential(rs, [mk_packet(i) for i in range(25)])
+    assert all(r.comparisons == 37 and r.matched_index is None for r in results)
+    assert stats.total_comparisons == 25 * 37
+
+
+def test_batch_empty():
+    results, stats = pfw.classify_batch_sequential(pfw.Ruleset(), [])
+    assert results == [] and stats.total_comparisons == 0 and stats.max_worker_comparisons == 0
+
+
+SCANS = [("oracle_r1000_t100000", "r1000_s1", "t100000_s2"),
+         ("r2048_t1000", "r2048_s21_w15", "t1000_s22"),
+         ("r300_t10000", "r300_s40_w30", "t10000_s41"),
+         ("r64_t600", "r64_s30_w40", "t600_s25"),
+         ("r1000_t5000ports", "r1000_s1", "t5000_s9_ports"),
+         ("r1000_t3000icmp", "r1000_s1", "t3000_s11_icmp")]
+
+
+@pytest.mark.parametrize("name,rn,tn", SCANS)
+def test_scan_matches_reference_golden(name, rn, tn):
+    g = golden(f"scan_{name}.npz")
+    rules, pk = golden_rules(rn), golden_traffic(tn)
+    c = compiled(rules)
+    R = c.num_rules
+    p = dev_pkts(pk)
+    n = len(p)
+    comps = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    verdict = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+    first = c.scan_range_device(p, 0, R, comps=comps, verdict=verdict, stats=stats)
+    np.testing.assert_array_equal(first_to_host(first), g["first"])
+    np.testing.assert_array_equal(verdict.cpu().numpy().astype(bool), g["verdict"])
+    want = oracle.sequential_comparisons(g["first"].astype(np.int64), R)
+    np.testing.assert_array_equal(comps.cpu().numpy(), want)
+    assert stats.cpu().tolist() == [int(g["total_comparisons"]), int(g["max_worker_comparisons"])]
+
+
+def test_oracle_config_through_drop_in_api():
+    g = golden("scan_oracle_r1000_t100000.npz")
+    rs = pfw.generate_ruleset(pfw.RulesetGenParams(1000, seed=1))
+    packets = pfw.generate_traffic(pfw.TrafficProfile(count=100_000, seed=2))
+    results, stats = pfw.classify_batch_sequential(rs, packets)
+    assert stats.total_comparisons == 69_698_223
+    got = np.array([-1 if r.matched_index is None else r.matched_index for r in results])
+    np.testing.assert_array_equal(got, g["first"])
+    assert [r.verdict is pfw.Action.ACCEPT for r in results] == g["verdict"].tolist()
+
+
+def test_scan_windows():
+    g = golden("scan_windows_r100_t150.npz")
+    c = compiled(golden_rules("r100_s60_w35"))
+    p = dev_pkts(golden_traffic("t150_s61"))
+    for (lo, hi), want in zip(g["windows"].tolist(), g["first"]):
+        np.testing.assert_array_equal(c.scan_range(p, lo, hi), want)
+
+
+def test_windows_every_alignment_vs_oracle():
+    rules = golden_rules("r300_s40_w30")
+    pk = golden_traffic("t10000_s41")
+    c, p = compiled(rules), dev_pkts(pk)
+    for lo, hi in [(0, 300), (1, 300), (31, 33), (32, 64), (33, 290), (255, 257), (256, 300),
+                   (299, 300), (5, 5), (7, 3), (0, 1)]:
+        np.testing.assert_array_equal(c.scan_range(p, lo, hi), oracle.scan_range(rules, pk, lo, hi))
+
+
+@pytest.mark.parametrize("rn", ["r4096_s1", "r10000_s1", "r100000_s1"])
+def test_config_rulesets_sample(rn):
+    g = golden(f"scan_{rn}_t20000.npz")
+    c = compiled(golden_rules(rn))
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=20_000, seed=2), device=0)
+    np.testing.assert_array_equal(c.scan_range(p, 0, c.num_rules), g["first"])
+
+
+def test_adversarial_recipe_sample():
+    g = golden("adversarial.npz")
+    c = compiled(oracle.adversarial_rules(50_000))
+    pk = oracle.adversarial_traffic(20_000)
+    np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 0, 50_000), g["first"])
+
+
+# ------------------------------------------------------------------- engine models
+
+@pytest.mark.parametrize("model", ["data", "function", "hybrid"])
+def test_engine_models_match_reference_golden(model):
+    g = golden("engine_r503_t600.npz")
+    c = compiled(golden_rules("r503_s24_w30"))
+    p = dev_pkts(golden_traffic("t600_s25"))
+    for nodes in (1, 2, 3, 4, 8, 16, 64, 512):
+        res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=nodes)).run_arrays(c, p)
+        key = f"{model}_{nodes}"
+        np.testing.assert_array_equal(res.first, g[f"{key}_first"])
+        np.testing.assert_array_equal(res.comparisons, g[f"{key}_comps"])
+        s = res.stats
+        assert [s.total_comparisons, s.max_worker_comparisons, s.packets_processed] == g[f"{key}_stats"].tolist()
+
+
+def test_function_parallel_100k_rules():
+    g = golden("engine_r100000_t2000.npz")
+    c = compiled(golden_rules("r100000_s1"))
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=2000, seed=2), device=0)
+    for nodes in (1, 2, 4, 8):
+        res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=nodes)).run_arrays(c, p)
+        np.testing.assert_array_equal(res.first, g[f"function_{nodes}_first"])
+        np.testing.assert_array_equal(res.comparisons, g[f"function_{nodes}_comps"])
+        assert [res.stats.total_comparisons, res.stats.max_worker_comparisons, 2000] == \
+            g[f"function_{nodes}_stats"].tolist()
+
+
+def test_engine_drop_in_run_all_models():
+    rs = pfw.generate_ruleset(pfw.RulesetGenParams(170, seed=29, wildcard_probability=0.3))
+    packets = pfw.generate_traffic(pfw.TrafficProfile(count=350, seed=30))
+    outs = []
+    for model in ("sequential", "data", "function", "hybrid"):
+        results, _ = pfw.run(rs, packets, pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=3))
+        outs.append([(r.verdict, r.matched_index) for r in results])
+    assert all(o == outs[0] for o in outs)
+    # empty batch / empty ruleset under every model (test_engines.py:249-263)
+    for model in ("sequential", "data", "function", "hybrid"):
+        cfg = pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=4)
+        results, stats = pfw.run(rs, [], cfg)
+        assert results == [] and stats.packets_processed == 0 and stats.total_comparisons == 0
+        results, stats = pfw.run(pfw.Ruleset(), packets[:50], cfg)
+        assert all(r.verdict is pfw.Action.DROP and r.matched_index is None for r in results)
+        assert stats.total_comparisons == 0
+    with pytest.raises(pfw.ConfigError, match="expected"):
+        pfw.run_data_parallel(rs, packets, pfw.EngineConfig(pfw.ExecutionModel.HYBRID))
+
+
+def test_function_parallel_speculative_scan_bounds():
+    rs = pfw.Ruleset((mk_rule(pfw.Action.ACCEPT, pfw.Protocol.TCP),)
+                     + tuple(mk_rule(pfw.Action.DROP, pfw.Protocol.UDP) for _ in range(2047)))
+    parts = pfw.partition_rules(rs, 4)
+    partials = [pfw.scan_partition(p, mk_packet()) for p in parts]
+    assert partials[0].comparisons == 1 and all(p.comparisons == 512 for p in partials[1:])
+    results, stats = pfw.run_function_parallel(rs, [mk_packet()], pfw.EngineConfig(
+        pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=4))
+    assert results[0].comparisons == 1 + 3 * 512 and stats.max_worker_comparisons == 512
+    combined = pfw.aggregate(partials, len(rs))
+    assert (combined.verdict, combined.matched_index) == (pfw.Action.ACCEPT, 0)
+
+
+def test_combine_partition_matches():
+    rows = np.array([[-1, 5, 7, -1], [3, -1, 2, -1], [4, 9, -1, 11]], dtype=np.int64)
+    np.testing.assert_array_equal(pfw.combine_partition_matches(rows, 12), [3, 5, 2, 11])
+    np.testing.assert_array_equal(pfw.combine_partition_matches(rows, 10), [3, 5, 2, -1])
+    assert pfw.combine_partition_matches(np.zeros((0, 0), np.int64), 5).shape == (0,)
+
+
+# --------------------------------------------------------------------- generator
+
+@pytest.mark.parametrize("name", ["t100000_s2", "t2000_s7_dst0_1", "t2000_s8_dst192_2", "t5000_s9_ports",
+                                  "t3000_s11_icmp", "t150_s61"])
+def test_device_generator_matches_reference(name):
+    g = golden(f"traffic_{name}.npz")
+    prof = pfw.TrafficProfile(
+        count=int(g["count"]), seed=int(g["seed"]), proto=pfw.Protocol(int(g["p_proto"])),
+        src_subnet=pfw.CidrMatcher(int(g["p_src_base"]), int(g["p_src_plen"])),
+        dst_subnet=pfw.CidrMatcher(int(g["p_dst_base"]), int(g["p_dst_plen"])),
+        sport_range=pfw.PortRange(int(g["p_sport_lo"]), int(g["p_sport_hi"])),
+        dport_range=pfw.PortRange(int(g["p_dport_lo"]), int(g["p_dport_hi"])))
+    cols = pfw.generate_traffic_device(prof, device=0).columns()
+    want = golden_traffic(name)
+    for f in PKT_FIELDS:
+        np.testing.assert_array_equal(cols[f], want[f])
+
+
+def test_device_generator_large_jump_ahead():
+    # 5M packets: the device stream must equal the sequential C oracle everywhere
+    n = 5_000_123
+    got = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=12345), device=0).columns()
+    want = oracle.gen_traffic_uniform(n, 12345)
+    for f in PKT_FIELDS:
+        np.testing.assert_array_equal(got[f], want[f])
+
+
+def test_worst_case_generation():
+    rs = pfw.generate_ruleset(pfw.RulesetGenParams(64, seed=3, wildcard_probability=0.3))
+    prof = pfw.TrafficProfile(count=300, seed=4, match_mode=pfw.MatchMode.WORST_CASE)
+    packets = pfw.generate_traffic(prof, rs)
+    assert [p.id for p in packets] == list(range(300))
+    results, _ = pfw.classify_batch_sequential(rs, packets)
+    assert all(r.matched_index is None for r in results)
+
+
+# ------------------------------------------------------------------ edge cases / tuning
+
+def test_ragged_sizes_and_empty():
+    rules = oracle.gen_ruleset(777, 5, wp=0.4)
+    c = compiled(rules)
+    for n in (0, 1, 31, 33, 255, 257, 2047, 2049, 4097):
+        pk = oracle.gen_traffic_uniform(n, 100 + n)
+        if n == 0:
+            assert c.scan_range(pfw.PacketArrays.empty(0, 0), 0, 777).shape == (0,)
+            continue
+        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 0, 777), oracle.scan_range(rules, pk, 0, 777))
+
+
+def test_unnormalised_and_inverted_rules_never_match():
+    # raw C-ABI columns outside the Rule invariants follow the reference
+    # predicate literally: (ip & mask) == base can never hold with host bits
+    # in base, and lo <= p <= hi never holds for an inverted range.
+    rules = {f: np.zeros(4, dtype=d) for f, d in zip(oracle.RULE_FIELDS, oracle.RULE_DTYPES)}
+    rules["sport_hi"][:] = 65535
+    rules["dport_hi"][:] = 65535
+    rules["src_base"][0], rules["src_mask"][0] = 0x0A000001, 0xFF000000  # host bit set
+    rules["sport_lo"][1], rules["sport_hi"][1] = 100, 50                 # inverted
+    rules["proto"][2] = 99                                               # unusual concrete proto
+    pk = oracle.gen_traffic_uniform(1000, 9, src_base=0x0A000000, src_plen=8)
+    pk["proto"][:500] = 99
+    want = oracle.scan_range(rules, pk, 0, 4)
+    np.testing.assert_array_equal(compiled(rules).scan_range(dev_pkts(pk), 0, 4), want)
+    assert (want[:500] == 2).all() and (want[500:] == 3).all()
+
+
+@pytest.mark.parametrize("ks,tile,imad", [(2, 256, 1), (4, 1024, 0), (8, 4096, 1), (8, 8192, 0), (4, 2048, 1)])
+def test_tuning_variants_identical(ks, tile, imad):
+    _native.set_tuning("ks", ks)
+    _native.set_tuning("tile", tile)
+    _native.set_tuning("force_imad", imad)
+    rules = golden_rules("r2048_s21_w15")
+    pk = golden_traffic("t10000_s41")
+    c = compiled(rules)
+    np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 0, 2048), oracle.scan_range(rules, pk, 0, 2048))
+    np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 100, 1500), oracle.scan_range(rules, pk, 100, 1500))
+
+
+def test_classify_host_e2e_matches_device():
+    rules = oracle.gen_ruleset(4096, 1)
+    c = compiled(rules)
+    n = 1_000_003
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=2), device=0)
+    dev_first = c.scan_range_device(p, 0, 4096)
+    host_pk = p.data.cpu().pin_memory()
+    h_first = torch.empty(n, dtype=torch.int32).pin_memory()
+    h_verd = torch.empty(n, dtype=torch.uint8).pin_memory()
+    h_stats = torch.zeros(2, dtype=torch.int64)
+    _native.check(_native.lib().pfw_classify_host(c.handle, host_pk.data_ptr(), n, h_first.data_ptr(),
+                                                  h_verd.data_ptr(), h_stats.data_ptr(), 300_000),
+                  "pfw_classify_host")
+    np.testing.assert_array_equal(h_first.numpy(), dev_first.cpu().numpy())
+    f = first_to_host(dev_first)
+    comps = oracle.sequential_comparisons(f, 4096)
+    assert h_stats.tolist() == [int(comps.sum()), int(comps.max())]
+    acc = np.where(f >= 0, rules["action_accept"][np.maximum(f, 0)], False)
+    np.testing.assert_array_equal(h_verd.numpy().astype(bool), acc)
+
+
+def test_full_size_properties_data_parallel():
+    """10K rules x 16Mi packets: oracle on a strided subsample, plus
+    size-independent properties on every packet (index range, verdict
+    consistency, comparison checksum = sum of per-packet counts)."""
+    R, n = 10_000, 1 << 24
+    rules = oracle.gen_ruleset(R, 1)
+    c = compiled(rules)
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=2), device=0)
+    comps = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    verdict = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+    first = c.scan_range_device(p, 0, R, comps=comps, verdict=verdict, stats=stats)
+    f = first.cpu().numpy()
+    hit = f != NO_MATCH
+    assert ((f[hit] >= 0) & (f[hit] < R)).all()
+    cm = comps.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(cm, np.where(hit, f.astype(np.int64) + 1, R))
+    assert stats.cpu().tolist() == [int(cm.sum()), int(cm.max())]
+    acc = np.zeros(n, np.uint8)
+    acc[hit] = rules["action_accept"][f[hit]]
+    np.testing.assert_array_equal(verdict.cpu().numpy(), acc)
+    idx = np.arange(0, n, 797)
+    sub = {k: v[idx] for k, v in p.columns().items()}
+    want = oracle.scan_range(rules, sub, 0, R)
+    got = np.where(hit[idx], f[idx].astype(np.int64), -1)
+    np.testing.assert_array_equal(got, want)
