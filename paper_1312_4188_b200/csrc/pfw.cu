@@ -81,10 +81,21 @@ struct DeviceGuard {
 // ---------------------------------------------------------- rule encoding
 // Device rule table: SoA of NF words, field f of rule r at rules[f * rpad + r].
 constexpr int NF = 10;
-enum { F_SRC_NLO = 0, F_SRC_W, F_DST_NLO, F_DST_W, F_SP_NLO, F_SP_W, F_DP_NLO, F_DP_W,
-       F_PR_NLO, F_PR_W };
-constexpr uint32_t NEVER_NLO = 0x80000000u;  // proto + 2^31 != 0 for every u8 proto
-constexpr uint32_t NEVER_W = 0u;
+// Per rule (one register each when staged):
+//   IP fields, 32-bit integer range tests on the FMA-heavy + ALU pipes:
+//     F_SRC_NLO = -src_base, F_SRC_W = ~src_mask  ->  (src - base) <=u ~mask
+//   port/proto fields, fp32 range tests on exact integers < 2^24 (FFMA runs on
+//   both FMA halves), the protocol folded into the port words:
+//     packet A  = (proto << 16) | sport   proto-major: concrete-proto rules
+//     packet A2 = (sport << 8)  | proto   proto-minor: ANY-proto rules
+//     packet B  = (dport << 8)  | proto   proto-minor: every rule
+//     dA = A*c1 + (A2*c2 - loA) with (c1, c2) = (1, 0) concrete, (0, 1) ANY;
+//     dB = B - loB; a field matches iff 0 <= d <= w, tested as
+//     float_bits(d) <=u float_bits(w) (negative d has the sign bit set).
+enum { F_SRC_NLO = 0, F_SRC_W, F_DST_NLO, F_DST_W, F_A_C1, F_A_C2, F_A_NLO, F_A_W, F_B_NLO,
+       F_B_W };
+constexpr uint32_t NEVER_B_NLO = 0x4C000000u;  // +2^25: dB >= 2^25 > any width (< 2^24)
+constexpr uint32_t NEVER_B_W = 0u;             // +0.0f
 
 // Tunables (pfw_set_tuning)
 int g_ks = 8;            // rules per lane per stage (stage = 32*KS rules)
@@ -139,25 +150,47 @@ __device__ __forceinline__ uint32_t sub_fma(uint32_t x, uint32_t one, uint32_t n
     return d;
 }
 
+// Fast-path test.  FMA: IP subtractions as IMAD with a runtime 1 (FMA-heavy
+// pipe) instead of IADD3 (ALU pipe, the bottleneck).
 template <bool FMA>
-__device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src, uint32_t dst,
-                                          uint32_t sp, uint32_t dp, uint32_t pr, uint32_t one) {
-    uint32_t a, b, c, d, e;
+__device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src, uint32_t dst, float A,
+                                          float A2, float B, uint32_t one) {
+    uint32_t a, b;
     if (FMA) {
         a = sub_fma(src, one, r[F_SRC_NLO]);
         b = sub_fma(dst, one, r[F_DST_NLO]);
-        c = sub_fma(sp, one, r[F_SP_NLO]);
-        d = sub_fma(dp, one, r[F_DP_NLO]);
-        e = sub_fma(pr, one, r[F_PR_NLO]);
     } else {
         a = src + r[F_SRC_NLO];
         b = dst + r[F_DST_NLO];
-        c = sp + r[F_SP_NLO];
-        d = dp + r[F_DP_NLO];
-        e = pr + r[F_PR_NLO];
     }
-    return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (c <= r[F_SP_W]) & (d <= r[F_DP_W]) &
-           (e <= r[F_PR_W]);
+    const float x = fmaf(A2, __uint_as_float(r[F_A_C2]), __uint_as_float(r[F_A_NLO]));
+    const float dA = fmaf(A, __uint_as_float(r[F_A_C1]), x);
+    const float dB = B + __uint_as_float(r[F_B_NLO]);
+    return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
+           (__float_as_uint(dB) <= r[F_B_W]);
+}
+
+// Slow-path re-evaluation (once per packet, after a stage hit).  Written with a
+// different instruction sequence so the compiler cannot CSE it with the fast
+// path and keep KS predicates / values alive across the vote.  Exact for the
+// same reasons: all float operands are integers < 2^24 and c1, c2 are 0 or 1.
+template <bool FMA>
+__device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t src, uint32_t dst,
+                                               float A, float A2, float B, uint32_t one) {
+    uint32_t a, b;
+    if (FMA) {
+        a = src + r[F_SRC_NLO];
+        b = dst + r[F_DST_NLO];
+    } else {
+        a = sub_fma(src, one, r[F_SRC_NLO]);
+        b = sub_fma(dst, one, r[F_DST_NLO]);
+    }
+    const float dA = __fadd_rn(__fadd_rn(__fmul_rn(A, __uint_as_float(r[F_A_C1])),
+                                         __fmul_rn(A2, __uint_as_float(r[F_A_C2]))),
+                               __uint_as_float(r[F_A_NLO]));
+    const float dB = __fsub_rn(B, -__uint_as_float(r[F_B_NLO]));
+    return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
+           (__float_as_uint(dB) <= r[F_B_W]);
 }
 
 constexpr int BLOCK = 256;
@@ -165,8 +198,8 @@ constexpr int NWARPS = BLOCK / 32;
 
 // shared-memory layout for a tile of T packets (T <= 65535)
 __host__ __device__ constexpr size_t smem_bytes(int T, int KS) {
-    return (size_t)T * 16      // packet (src, dst, sport, dport)
-           + (size_t)T * 4     // proto
+    return (size_t)T * 16      // packet {src, dst, A, A2}
+           + (size_t)T * 4     // packet B
            + (size_t)T * 4     // first
            + (size_t)T * 2 * 2 // live lists (ping-pong)
            + 2 * (size_t)NF * 32 * KS * 4  // rule stage ring (2 buffers)
@@ -267,9 +300,13 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
         }
 
         for (int i = tid; i < cnt; i += BLOCK) {
-            uint4 v = __ldg(p.pkts + base + i);
-            s_pk[i] = make_uint4(v.x, v.y, v.z >> 16, v.z & 0xFFFFu);
-            s_pr[i] = v.w;
+            // per-packet precompute, amortised over every stage of the tile:
+            // the fp32 port/proto words (exact integers < 2^24)
+            const uint4 v = __ldg(p.pkts + base + i);
+            const uint32_t sp = v.z >> 16, dp = v.z & 0xFFFFu, pr = v.w & 0xFFu;
+            s_pk[i] = make_uint4(v.x, v.y, __float_as_uint((float)((pr << 16) | sp)),
+                                 __float_as_uint((float)((sp << 8) | pr)));
+            s_pr[i] = __float_as_uint((float)((dp << 8) | pr));
             s_first[i] = PFW_NO_MATCH;
             s_liveA[i] = (uint16_t)i;
         }
@@ -299,26 +336,63 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 for (int f = 0; f < NF; f++) r[j][f] = sr[f * STAGE + j * 32 + lane];
                 const int64_t ri = s + j * 32 + lane;
                 if (ri < p.lo || ri >= p.hi) {
-                    r[j][F_PR_NLO] = NEVER_NLO;
-                    r[j][F_PR_W] = NEVER_W;
+                    r[j][F_B_NLO] = NEVER_B_NLO;
+                    r[j][F_B_W] = NEVER_B_W;
                 }
             }
 
-            for (int i = warp; i < nlive; i += NWARPS) {
+            // Two live packets per iteration: independent chains for ILP and
+            // half the loop overhead.  Packets are warp-uniform, so every
+            // branch below is warp-uniform too.
+            int i = warp;
+            for (; i + NWARPS < nlive; i += 2 * NWARPS) {
+                const int q0 = live[i], q1 = live[i + NWARPS];
+                const uint4 v0 = s_pk[q0], v1 = s_pk[q1];
+                const float b0 = __uint_as_float(s_pr[q0]), b1 = __uint_as_float(s_pr[q1]);
+                const float a0 = __uint_as_float(v0.z), c0 = __uint_as_float(v0.w);
+                const float a1 = __uint_as_float(v1.z), c1 = __uint_as_float(v1.w);
+                bool any0 = false, any1 = false;
+#pragma unroll
+                for (int j = 0; j < KS; j++) {
+                    any0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
+                    any1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
+                }
+                if (__any_sync(0xFFFFFFFFu, any0)) {
+#pragma unroll
+                    for (int j = 0; j < KS; j++) {
+                        const unsigned b = __ballot_sync(
+                            0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one));
+                        if (b) {
+                            if (lane == 0) s_first[q0] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
+                            break;
+                        }
+                    }
+                }
+                if (__any_sync(0xFFFFFFFFu, any1)) {
+#pragma unroll
+                    for (int j = 0; j < KS; j++) {
+                        const unsigned b = __ballot_sync(
+                            0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one));
+                        if (b) {
+                            if (lane == 0) s_first[q1] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
+                            break;
+                        }
+                    }
+                }
+            }
+            if (i < nlive) {
                 const int q = live[i];
                 const uint4 v = s_pk[q];
-                const uint32_t pr = s_pr[q];
+                const float bb = __uint_as_float(s_pr[q]);
+                const float a = __uint_as_float(v.z), c = __uint_as_float(v.w);
                 bool any = false;
 #pragma unroll
-                for (int j = 0; j < KS; j++) any |= rule_test<FMA>(r[j], v.x, v.y, v.z, v.w, pr, one);
+                for (int j = 0; j < KS; j++) any |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
                 if (__any_sync(0xFFFFFFFFu, any)) {
-                    // slow path (once per packet): re-evaluate with the other
-                    // arithmetic form so the compiler cannot CSE it with the
-                    // fast path and keep KS predicates alive across the vote
 #pragma unroll
                     for (int j = 0; j < KS; j++) {
                         const unsigned b =
-                            __ballot_sync(0xFFFFFFFFu, rule_test<!FMA>(r[j], v.x, v.y, v.z, v.w, pr, one));
+                            __ballot_sync(0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v.x, v.y, a, c, bb, one));
                         if (b) {
                             if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
                             break;
@@ -552,6 +626,11 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, cudaStream_t st) {
     ScanParams p = p0;
     const size_t sm = smem_bytes(p.tile, KS);
     auto kern = scan_kernel<KS, ACC, FMA>;
+    int maxsm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+    if (sm > (size_t)maxsm)
+        return set_err(PFW_ERR_INVALID, "tile %d x ks %d needs %zu B of shared memory (max %d)", p.tile,
+                       KS, sm, maxsm);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int occ = g_ctas_per_sm;
     if (occ <= 0) {
@@ -643,6 +722,12 @@ int pfw_device_count(void) {
 
 int64_t pfw_launch_count(void) { return g_launches.load(); }
 
+static uint32_t f2u(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return u;
+}
+
 int pfw_set_tuning(const char *key, int64_t value) {
     if (!key) return set_err(PFW_ERR_INVALID, "null key");
     if (!strcmp(key, "ks")) {
@@ -697,23 +782,31 @@ int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32
             w[F_SRC_W] = ~sm;
             w[F_DST_NLO] = 0u - db;
             w[F_DST_W] = ~dm;
-            w[F_SP_NLO] = 0u - (uint32_t)sport_lo[r];
-            w[F_SP_W] = (uint32_t)sport_hi[r] - (uint32_t)sport_lo[r];
-            w[F_DP_NLO] = 0u - (uint32_t)dport_lo[r];
-            w[F_DP_W] = (uint32_t)dport_hi[r] - (uint32_t)dport_lo[r];
-            if (proto[r] == 0) {  // Protocol.ANY (model.py:68)
-                w[F_PR_NLO] = 0u;
-                w[F_PR_W] = 0xFFFFFFFFu;
-            } else {
-                w[F_PR_NLO] = 0u - (uint32_t)proto[r];
-                w[F_PR_W] = 0u;
+            const uint32_t slo = sport_lo[r], shi = sport_hi[r], dlo = dport_lo[r], dhi = dport_hi[r];
+            uint32_t loA, widA;
+            float c1, c2;
+            if (proto[r] == 0) {  // Protocol.ANY (model.py:68): A2 = sport<<8 | proto
+                c1 = 0.f, c2 = 1.f;
+                loA = slo << 8;
+                widA = ((shi << 8) | 0xFFu) - loA;
+            } else {              // concrete: A = proto<<16 | sport
+                c1 = 1.f, c2 = 0.f;
+                loA = ((uint32_t)proto[r] << 16) | slo;
+                widA = shi - slo;
             }
+            const uint32_t loB = dlo << 8, widB = ((dhi << 8) | 0xFFu) - loB;
+            w[F_A_C1] = f2u(c1);
+            w[F_A_C2] = f2u(c2);
+            w[F_A_NLO] = f2u(-(float)loA);
+            w[F_A_W] = f2u((float)widA);
+            w[F_B_NLO] = f2u(-(float)loB);
+            w[F_B_W] = f2u((float)widB);
             acc[r] = accept[r] ? 1 : 0;
         }
         if (never) {
             for (int f = 0; f < NF; f++) w[f] = 0;
-            w[F_PR_NLO] = NEVER_NLO;
-            w[F_PR_W] = NEVER_W;
+            w[F_B_NLO] = NEVER_B_NLO;
+            w[F_B_W] = NEVER_B_W;
         }
         for (int f = 0; f < NF; f++) host[(size_t)f * h->rpad + r] = w[f];
     }

@@ -286,7 +286,7 @@ def test_unnormalised_and_inverted_rules_never_match():
     assert (want[:500] == 2).all() and (want[500:] == 3).all()
 
 
-@pytest.mark.parametrize("ks,tile,imad", [(2, 256, 1), (4, 1024, 0), (8, 4096, 1), (8, 8192, 0), (4, 2048, 1)])
+@pytest.mark.parametrize("ks,tile,imad", [(2, 256, 1), (4, 1024, 0), (8, 4096, 1), (8, 6144, 0), (4, 2048, 1)])
 def test_tuning_variants_identical(ks, tile, imad):
     _native.set_tuning("ks", ks)
     _native.set_tuning("tile", tile)
@@ -296,6 +296,13 @@ def test_tuning_variants_identical(ks, tile, imad):
     c = compiled(rules)
     np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 0, 2048), oracle.scan_range(rules, pk, 0, 2048))
     np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 100, 1500), oracle.scan_range(rules, pk, 100, 1500))
+
+
+def test_tile_too_large_is_rejected_loudly():
+    _native.set_tuning("tile", 8192)
+    c = compiled(golden_rules("r64_s30_w40"))
+    with pytest.raises(ValueError, match="shared memory"):
+        c.scan_range(dev_pkts(golden_traffic("t600_s25")), 0, 64)
 
 
 def test_classify_host_e2e_matches_device():
