@@ -178,6 +178,7 @@ def main() -> int:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--first-pass", type=int, default=-1, help="rules in the first pass (0 = single pass)")
     args = ap.parse_args()
 
     from paper_1312_4188_b200 import workloads
@@ -203,6 +204,8 @@ def main() -> int:
         _native.set_tuning("ks", args.ks)
     if args.tile:
         _native.set_tuning("tile", args.tile)
+    if args.first_pass >= 0:
+        _native.set_tuning("first_pass", args.first_pass)
     peaks = load_peaks()
     dev = torch.device(f"cuda:{local}")
     info = parallel.RankInfo(rank, world)

@@ -102,8 +102,17 @@ int g_ks = 8;            // rules per lane per stage (stage = 32*KS rules)
 int g_tile = 2048;       // packets per CTA tile
 int g_ctas_per_sm = 0;   // 0 = occupancy query
 int g_force_imad = 1;    // route the subtract through IMAD (FMA pipe)
+int g_first_pass = 1024; // rules in the first pass (0 = single pass); passes double
+constexpr int MAX_PASSES = 32;
 
 }  // namespace
+
+// Per-scan scratch: ping-pong live-id lists for the passes + counters.
+struct ScanWs {
+    uint32_t *ids = nullptr;       // 2 * cap
+    unsigned int *ctr = nullptr;   // 2 * MAX_PASSES
+    int64_t cap = 0;
+};
 
 struct pfw_ruleset {
     int device;
@@ -111,19 +120,18 @@ struct pfw_ruleset {
     int64_t rpad;    // padded row length (multiple of 32, >= n + max stage)
     uint32_t *d_rules = nullptr;   // NF * rpad
     uint8_t *d_accept = nullptr;   // rpad
-    unsigned int *d_counter = nullptr;  // tile counters (one per launch slot)
     int sms = 148;
     // e2e workspace
     void *d_ws = nullptr;
     size_t ws_bytes = 0;
     cudaStream_t streams[2] = {nullptr, nullptr};
     cudaEvent_t ev_done = nullptr;
-    int counter_slot = 0;
+    ScanWs ws;         // default (calls on the caller's stream)
+    ScanWs ws_e2e[2];  // pfw_classify_host slots
 };
 
 namespace {
 
-constexpr int COUNTER_SLOTS = 1024;
 
 // ================================================================ kernels
 
@@ -131,15 +139,19 @@ struct ScanParams {
     const uint32_t *rules;
     const uint8_t *accept;
     int64_t rpad;
-    int64_t lo, hi;
+    int64_t lo, hi;            // rule window [lo, hi): masking + comparison counts
+    int64_t s_begin, s_end;    // this pass: stage starts s_begin, s_begin+STAGE, ... < s_end
     const uint4 *pkts;
-    int64_t n;
+    int64_t n;                 // packets in the batch (pass 0 count when in_ids == null)
+    const uint32_t *in_ids;    // live packet ids of this pass (null = 0..n-1)
+    const unsigned int *in_count;  // device count of in_ids (null = n)
+    uint32_t *out_ids;         // survivors of this pass (null = final pass)
+    unsigned int *out_count;
     uint32_t *first;
     uint32_t *comps;
     uint8_t *verdict;
     unsigned long long *stats;
     unsigned int *tile_counter;
-    int64_t ntiles;
     int tile;
     uint32_t one;  // runtime 1: keeps ptxas from folding x*1+c into IADD3
 };
@@ -200,6 +212,7 @@ constexpr int NWARPS = BLOCK / 32;
 __host__ __device__ constexpr size_t smem_bytes(int T, int KS) {
     return (size_t)T * 16      // packet {src, dst, A, A2}
            + (size_t)T * 4     // packet B
+           + (size_t)T * 4     // packet id
            + (size_t)T * 4     // first
            + (size_t)T * 2 * 2 // live lists (ping-pong)
            + 2 * (size_t)NF * 32 * KS * 4  // rule stage ring (2 buffers)
@@ -259,19 +272,20 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     uint4 *s_pk = reinterpret_cast<uint4 *>(smem_raw);
     uint32_t *s_rules = reinterpret_cast<uint32_t *>(s_pk + T);      // 2 * NF * 32 * KS
     uint32_t *s_pr = s_rules + 2 * NF * 32 * KS;
-    uint32_t *s_first = s_pr + T;
+    uint32_t *s_id = s_pr + T;
+    uint32_t *s_first = s_id + T;
     uint16_t *s_liveA = reinterpret_cast<uint16_t *>(s_first + T);
     uint16_t *s_liveB = s_liveA + T;
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(s_liveB + T) + 15) & ~uintptr_t(15));
-    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile
+    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile, [3]=out base
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t one = p.one;
     constexpr int STAGE = 32 * KS;
-    // Stages are aligned to 32 rules of the table; rules below lo in the
-    // first stage are masked to never-match.
-    const int64_t s0 = p.lo & ~int64_t(31);
+    const bool final_pass = p.out_ids == nullptr;
+    const int64_t count = p.in_count ? (int64_t)*p.in_count : p.n;
+    const int64_t ntiles = (count + T - 1) / T;
 
     unsigned long long st_sum = 0;
     unsigned st_max = 0;
@@ -288,25 +302,27 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
         if (tid == 0) s_misc[1] = (int)atomicAdd(p.tile_counter, 1u);
         __syncthreads();
         const int64_t tile = s_misc[1];
-        if (tile >= p.ntiles) break;
+        if (tile >= ntiles) break;
         const int64_t base = tile * T;
-        const int cnt = (int)((p.n - base) < T ? (p.n - base) : (int64_t)T);
+        const int cnt = (int)((count - base) < T ? (count - base) : (int64_t)T);
 
-        // prefetch the first stage while the packet tile loads
-        const bool any_rules = p.lo < p.hi;
+        // prefetch the pass's first stage while the packet tile loads
+        const bool any_rules = p.s_begin < p.s_end;
         if (tid == 0 && any_rules) {
             fence_proxy_async();
-            issue_stage<KS>(p, s0, s_rules, &s_bar[0]);
+            issue_stage<KS>(p, p.s_begin, s_rules, &s_bar[0]);
         }
 
         for (int i = tid; i < cnt; i += BLOCK) {
-            // per-packet precompute, amortised over every stage of the tile:
+            // per-packet precompute, amortised over every stage of the pass:
             // the fp32 port/proto words (exact integers < 2^24)
-            const uint4 v = __ldg(p.pkts + base + i);
+            const uint32_t id = p.in_ids ? __ldg(p.in_ids + base + i) : (uint32_t)(base + i);
+            const uint4 v = __ldg(p.pkts + id);
             const uint32_t sp = v.z >> 16, dp = v.z & 0xFFFFu, pr = v.w & 0xFFu;
             s_pk[i] = make_uint4(v.x, v.y, __float_as_uint((float)((pr << 16) | sp)),
                                  __float_as_uint((float)((sp << 8) | pr)));
             s_pr[i] = __float_as_uint((float)((dp << 8) | pr));
+            s_id[i] = id;
             s_first[i] = PFW_NO_MATCH;
             s_liveA[i] = (uint16_t)i;
         }
@@ -315,12 +331,12 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
         int nlive = any_rules ? cnt : 0;
         uint16_t *live = s_liveA, *live2 = s_liveB;
         int buf = 0, kc = 0;
-        int64_t s = s0;
-        while (nlive > 0 && s < p.hi) {
+        int64_t s = p.s_begin;
+        while (nlive > 0 && s < p.s_end) {
             // prefetch next stage into the other buffer (its previous reader
             // finished: every warp passed the __syncthreads that ended it)
             const int64_t sn = s + STAGE;
-            if (tid == 0 && sn < p.hi) {
+            if (tid == 0 && sn < p.s_end) {
                 fence_proxy_async();
                 issue_stage<KS>(p, sn, s_rules + (buf ^ 1) * NF * STAGE, &s_bar[buf ^ 1]);
             }
@@ -340,7 +356,6 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                     r[j][F_B_W] = NEVER_B_W;
                 }
             }
-
             // Two live packets per iteration: independent chains for ILP and
             // half the loop overhead.  Packets are warp-uniform, so every
             // branch below is warp-uniform too.
@@ -430,28 +445,43 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
             s = sn;
         }
         // drain a prefetched stage that was not consumed (tile ended early)
-        if (any_rules && s < p.hi) {
+        if (any_rules && s < p.s_end) {
             mbar_wait(&s_bar[buf], (phase >> buf) & 1u);
             phase ^= 1u << buf;
         }
 
-        // epilogue: results, comparisons, verdicts, stats
+        // epilogue: resolve matched packets (and, in the final pass, the
+        // unmatched ones); survivors of a non-final pass go to the next pass
         const uint32_t span = (uint32_t)(p.hi > p.lo ? p.hi - p.lo : 0);
-        for (int i = tid; i < cnt; i += BLOCK) {
-            const uint32_t f = s_first[i];
-            const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.lo + 1) : span;
-            const int64_t g = base + i;
-            if (ACC) {
-                const uint32_t old = p.first[g];
-                p.first[g] = min(old, f);
-                p.comps[g] += c;
-            } else {
-                p.first[g] = f;
-                if (p.comps) p.comps[g] = c;
-                if (p.verdict) p.verdict[g] = (f != PFW_NO_MATCH) ? p.accept[f] : (uint8_t)0;
+        for (int i0 = 0; i0 < cnt; i0 += BLOCK) {
+            const int i = i0 + tid;
+            bool survive = false;
+            uint32_t id = 0;
+            if (i < cnt) {
+                const uint32_t f = s_first[i];
+                id = s_id[i];
+                survive = !final_pass && f == PFW_NO_MATCH;
+                if (!survive) {
+                    const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.lo + 1) : span;
+                    if (ACC) {
+                        if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
+                        p.comps[id] += c;
+                    } else {
+                        p.first[id] = f;
+                        if (p.comps) p.comps[id] = c;
+                        if (p.verdict) p.verdict[id] = (f != PFW_NO_MATCH) ? p.accept[f] : (uint8_t)0;
+                    }
+                    st_sum += c;
+                    st_max = max(st_max, c);
+                }
             }
-            st_sum += c;
-            st_max = max(st_max, c);
+            const unsigned b = __ballot_sync(0xFFFFFFFFu, survive);
+            if (b) {
+                unsigned off = 0;
+                if (lane == 0) off = atomicAdd(p.out_count, (unsigned)__popc(b));
+                off = __shfl_sync(0xFFFFFFFFu, off, 0);
+                if (survive) p.out_ids[off + __popc(b & ((1u << lane) - 1u))] = id;
+            }
         }
         __syncthreads();
     }
@@ -621,15 +651,57 @@ bool stage_fits(int T, int KS, int dev) {
     return smem_bytes(T, KS) <= (size_t)maxsm;
 }
 
+int ensure_ws(ScanWs &ws, int64_t n) {
+    if (!ws.ctr) CUDA_TRY(cudaMalloc(&ws.ctr, 2 * MAX_PASSES * sizeof(unsigned int)));
+    if (ws.cap < n) {
+        if (ws.ids) cudaFree(ws.ids);
+        ws.ids = nullptr;
+        ws.cap = 0;
+        const int64_t cap = n < 4096 ? 4096 : n;
+        CUDA_TRY(cudaMalloc(&ws.ids, 2 * (size_t)cap * sizeof(uint32_t)));
+        ws.cap = cap;
+    }
+    return PFW_OK;
+}
+
+void free_ws(ScanWs &ws) {
+    if (ws.ids) cudaFree(ws.ids);
+    if (ws.ctr) cudaFree(ws.ctr);
+    ws = ScanWs{};
+}
+
+// Pass plan over the window [lo, hi): stage-aligned boundaries starting at
+// lo & ~31, first pass g_first_pass rules, then doubling.  Each pass scans
+// only the packets the previous passes left unmatched, compacted into dense
+// tiles, so the long tail of late-matching / default-deny packets never runs
+// on near-empty tiles.
+std::vector<int64_t> plan_passes(int64_t lo, int64_t hi, int stage) {
+    std::vector<int64_t> b;
+    const int64_t s0 = lo & ~int64_t(31);
+    b.push_back(s0);
+    if (lo >= hi) {
+        b.push_back(s0);
+        return b;
+    }
+    int64_t len = g_first_pass > 0 ? ((g_first_pass + stage - 1) / stage) * (int64_t)stage : 0;
+    int64_t cur = s0;
+    while (len > 0 && cur + len < hi && (int)b.size() < MAX_PASSES) {
+        cur += len;
+        b.push_back(cur);
+        len *= 2;
+    }
+    b.push_back(hi);
+    return b;
+}
+
 template <int KS, bool ACC, bool FMA>
-int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, cudaStream_t st) {
-    ScanParams p = p0;
-    const size_t sm = smem_bytes(p.tile, KS);
+int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t st) {
+    const size_t sm = smem_bytes(p0.tile, KS);
     auto kern = scan_kernel<KS, ACC, FMA>;
     int maxsm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     if (sm > (size_t)maxsm)
-        return set_err(PFW_ERR_INVALID, "tile %d x ks %d needs %zu B of shared memory (max %d)", p.tile,
+        return set_err(PFW_ERR_INVALID, "tile %d x ks %d needs %zu B of shared memory (max %d)", p0.tile,
                        KS, sm, maxsm);
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int occ = g_ctas_per_sm;
@@ -637,34 +709,53 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, cudaStream_t st) {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, sm));
         if (occ < 1) occ = 1;
     }
+    const int64_t ntiles0 = (p0.n + p0.tile - 1) / p0.tile;
     int64_t grid = (int64_t)h->sms * occ;
-    if (grid > p.ntiles) grid = p.ntiles;
+    if (grid > ntiles0) grid = ntiles0;
     if (grid < 1) grid = 1;
-    unsigned int *ctr = h->d_counter + h->counter_slot;
-    h->counter_slot = (h->counter_slot + 1) % COUNTER_SLOTS;
-    CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), st));
-    p.tile_counter = ctr;
-    kern<<<(unsigned)grid, BLOCK, sm, st>>>(p);
-    CUDA_TRY(cudaGetLastError());
-    g_launches++;
+
+    const std::vector<int64_t> b = plan_passes(p0.lo, p0.hi, 32 * KS);
+    const int npass = (int)b.size() - 1;
+    if (npass > 1) {
+        int rc = ensure_ws(ws, p0.n);
+        if (rc != PFW_OK) return rc;
+    } else if (!ws.ctr) {
+        CUDA_TRY(cudaMalloc(&ws.ctr, 2 * MAX_PASSES * sizeof(unsigned int)));
+    }
+    CUDA_TRY(cudaMemsetAsync(ws.ctr, 0, 2 * (size_t)npass * sizeof(unsigned int), st));
+    for (int k = 0; k < npass; k++) {
+        ScanParams p = p0;
+        p.s_begin = b[k];
+        p.s_end = b[k + 1];
+        p.tile_counter = ws.ctr + 2 * k;
+        p.in_ids = k == 0 ? nullptr : ws.ids + (size_t)((k - 1) & 1) * ws.cap;
+        p.in_count = k == 0 ? nullptr : ws.ctr + 2 * (k - 1) + 1;
+        const bool last = k == npass - 1;
+        p.out_ids = last ? nullptr : ws.ids + (size_t)(k & 1) * ws.cap;
+        p.out_count = last ? nullptr : ws.ctr + 2 * k + 1;
+        kern<<<(unsigned)grid, BLOCK, sm, st>>>(p);
+        CUDA_TRY(cudaGetLastError());
+        g_launches++;
+    }
     return PFW_OK;
 }
 
 template <bool ACC, bool FMA>
-int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
+int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t st) {
     switch (g_ks) {
-        case 2: return launch_scan_t<2, ACC, FMA>(h, p, st);
-        case 4: return launch_scan_t<4, ACC, FMA>(h, p, st);
-        case 8: return launch_scan_t<8, ACC, FMA>(h, p, st);
+        case 2: return launch_scan_t<2, ACC, FMA>(h, p, ws, st);
+        case 4: return launch_scan_t<4, ACC, FMA>(h, p, ws, st);
+        case 8: return launch_scan_t<8, ACC, FMA>(h, p, ws, st);
         default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4 or 8)", g_ks);
     }
 }
 
 int launch_scan(pfw_ruleset *h, bool acc, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                 uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
-                cudaStream_t st) {
+                cudaStream_t st, ScanWs *ws = nullptr) {
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count %lld", (long long)n);
+    if (n > 0xFFFFFFFFll) return set_err(PFW_ERR_INVALID, "more than 2^32-1 packets in one call");
     if (lo < 0 || hi < 0) return set_err(PFW_ERR_INVALID, "negative rule window [%lld, %lld)",
                                          (long long)lo, (long long)hi);
     if (hi > h->n) return set_err(PFW_ERR_INVALID, "rule window end %lld beyond ruleset of %lld",
@@ -686,12 +777,12 @@ int launch_scan(pfw_ruleset *h, bool acc, int64_t lo, int64_t hi, const void *d_
     p.verdict = verdict;
     p.stats = reinterpret_cast<unsigned long long *>(stats);
     p.tile = g_tile;
-    p.ntiles = (n + p.tile - 1) / p.tile;
     p.one = 1;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
-    if (acc) return g_force_imad ? launch_scan_ks<true, true>(h, p, st) : launch_scan_ks<true, false>(h, p, st);
-    return g_force_imad ? launch_scan_ks<false, true>(h, p, st) : launch_scan_ks<false, false>(h, p, st);
+    ScanWs &w = ws ? *ws : h->ws;
+    if (acc) return g_force_imad ? launch_scan_ks<true, true>(h, p, w, st) : launch_scan_ks<true, false>(h, p, w, st);
+    return g_force_imad ? launch_scan_ks<false, true>(h, p, w, st) : launch_scan_ks<false, false>(h, p, w, st);
 }
 
 int grid_for(int64_t n) {
@@ -739,6 +830,9 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "ctas_per_sm")) {
         if (value < 0 || value > 8) return set_err(PFW_ERR_INVALID, "ctas_per_sm in [0, 8]");
         g_ctas_per_sm = (int)value;
+    } else if (!strcmp(key, "first_pass")) {
+        if (value < 0 || value > (1 << 24)) return set_err(PFW_ERR_INVALID, "first_pass in [0, 2^24]");
+        g_first_pass = (int)value;
     } else if (!strcmp(key, "force_imad")) {
         g_force_imad = value != 0;
     } else {
@@ -812,7 +906,6 @@ int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32
     }
     cudaError_t e = cudaMalloc(&h->d_rules, host.size() * 4);
     if (e == cudaSuccess) e = cudaMalloc(&h->d_accept, acc.size());
-    if (e == cudaSuccess) e = cudaMalloc(&h->d_counter, COUNTER_SLOTS * sizeof(unsigned int));
     if (e == cudaSuccess) e = cudaMemcpy(h->d_rules, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_accept, acc.data(), acc.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
@@ -830,8 +923,10 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     DeviceGuard g(h->device);
     if (h->d_rules) cudaFree(h->d_rules);
     if (h->d_accept) cudaFree(h->d_accept);
-    if (h->d_counter) cudaFree(h->d_counter);
     if (h->d_ws) cudaFree(h->d_ws);
+    free_ws(h->ws);
+    free_ws(h->ws_e2e[0]);
+    free_ws(h->ws_e2e[1]);
     for (auto &s : h->streams)
         if (s) cudaStreamDestroy(s);
     if (h->ev_done) cudaEventDestroy(h->ev_done);
@@ -945,7 +1040,7 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
         CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
                                  cudaMemcpyHostToDevice, st));
         rc = launch_scan(h, false, 0, h->n, dp, m, df, nullptr, h_verdict ? dv : nullptr,
-                         h_stats ? d_stats : nullptr, st);
+                         h_stats ? d_stats : nullptr, st, &h->ws_e2e[k & 1]);
         if (rc != PFW_OK) break;
         CUDA_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, st));
         if (h_verdict)

@@ -36,7 +36,7 @@ def compiled(rules: dict) -> pfw.CompiledRuleset:
 @pytest.fixture(autouse=True)
 def _reset_tuning():
     yield
-    for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1)):
+    for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024)):
         _native.set_tuning(k, v)
 
 
@@ -286,16 +286,26 @@ def test_unnormalised_and_inverted_rules_never_match():
     assert (want[:500] == 2).all() and (want[500:] == 3).all()
 
 
-@pytest.mark.parametrize("ks,tile,imad", [(2, 256, 1), (4, 1024, 0), (8, 4096, 1), (8, 6144, 0), (4, 2048, 1)])
-def test_tuning_variants_identical(ks, tile, imad):
+@pytest.mark.parametrize("ks,tile,imad,fp", [(2, 256, 1, 64), (4, 1024, 0, 0), (8, 4096, 1, 256),
+                                             (8, 6144, 0, 1024), (4, 2048, 1, 100), (8, 2048, 1, 32)])
+def test_tuning_variants_identical(ks, tile, imad, fp):
     _native.set_tuning("ks", ks)
     _native.set_tuning("tile", tile)
     _native.set_tuning("force_imad", imad)
+    _native.set_tuning("first_pass", fp)
     rules = golden_rules("r2048_s21_w15")
     pk = golden_traffic("t10000_s41")
     c = compiled(rules)
     np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 0, 2048), oracle.scan_range(rules, pk, 0, 2048))
     np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), 100, 1500), oracle.scan_range(rules, pk, 100, 1500))
+    # multi-pass accumulate (function-parallel partitions) under the same tuning
+    g = golden("engine_r503_t600.npz")
+    c5 = compiled(golden_rules("r503_s24_w30"))
+    p5 = dev_pkts(golden_traffic("t600_s25"))
+    for nodes in (1, 3, 64):
+        res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=nodes)).run_arrays(c5, p5)
+        np.testing.assert_array_equal(res.first, g[f"function_{nodes}_first"])
+        np.testing.assert_array_equal(res.comparisons, g[f"function_{nodes}_comps"])
 
 
 def test_tile_too_large_is_rejected_loudly():
