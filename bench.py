@@ -197,9 +197,19 @@ def main() -> int:
     from paper_1312_4188_b200 import _native, parallel
     from paper_1312_4188_b200.classifier import CompiledRuleset
 
+    # PFW_SHARE_GPU=1: every rank on cuda:0 with gloo collectives on host copies --
+    # a functional check of the N-rank path on a 1-GPU box (kernels of
+    # different ranks never wait on each other).  Normal runs: one GPU per
+    # rank, NCCL over NVLink/NVSwitch.
+    share = os.environ.get("PFW_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     if args.ks:
         _native.set_tuning("ks", args.ks)
     if args.tile:
@@ -242,8 +252,12 @@ def main() -> int:
                                        stats=stats, stream=stream.cuda_stream)
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if share:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -271,9 +285,8 @@ def main() -> int:
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     tot = torch.tensor([float(n if w.model != "function" else 0), float(local_comps)],
                        dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    parallel.all_reduce(t, dist.ReduceOp.MAX)
+    parallel.all_reduce(tot, dist.ReduceOp.SUM)
     job_ms = float(t.item())
     pk_per_step = w.packets if w.model == "function" else int(tot[0].item())
     value = pk_per_step * args.steps / (job_ms / 1e3) / 1e6
@@ -323,8 +336,7 @@ def main() -> int:
             e2e_step()
             et.append(time.perf_counter() - t0)
         tt = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        parallel.all_reduce(tt, dist.ReduceOp.MAX)
         e2e = {"value": pk_per_step * args.steps / float(tt.item()) / 1e6, "unit": "Mpps",
                "h2d_bytes_per_step": n * PKT_BYTES, "d2h_bytes_per_step": n * 5,
                "api": "pfw_classify_host (C-ABI, pinned host buffers, 4Mi-packet chunks, 2 streams)"}

@@ -268,16 +268,16 @@ __device__ __forceinline__ void issue_stage(const ScanParams &p, int64_t s, uint
 template <int KS, bool ACC, bool FMA>
 __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int T = p.tile;
+    const int TMAX = p.tile;  // shared-memory capacity in packets
     uint4 *s_pk = reinterpret_cast<uint4 *>(smem_raw);
-    uint32_t *s_rules = reinterpret_cast<uint32_t *>(s_pk + T);      // 2 * NF * 32 * KS
+    uint32_t *s_rules = reinterpret_cast<uint32_t *>(s_pk + TMAX);      // 2 * NF * 32 * KS
     uint32_t *s_pr = s_rules + 2 * NF * 32 * KS;
-    uint32_t *s_id = s_pr + T;
-    uint32_t *s_first = s_id + T;
-    uint16_t *s_liveA = reinterpret_cast<uint16_t *>(s_first + T);
-    uint16_t *s_liveB = s_liveA + T;
+    uint32_t *s_id = s_pr + TMAX;
+    uint32_t *s_first = s_id + TMAX;
+    uint16_t *s_liveA = reinterpret_cast<uint16_t *>(s_first + TMAX);
+    uint16_t *s_liveB = s_liveA + TMAX;
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(s_liveB + T) + 15) & ~uintptr_t(15));
+        (reinterpret_cast<uintptr_t>(s_liveB + TMAX) + 15) & ~uintptr_t(15));
     int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile, [3]=out base
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -285,6 +285,16 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     constexpr int STAGE = 32 * KS;
     const bool final_pass = p.out_ids == nullptr;
     const int64_t count = p.in_count ? (int64_t)*p.in_count : p.n;
+    // Tile size for this pass: the full capacity when there is enough work,
+    // otherwise small enough to give every CTA ~2 tiles (late passes carry
+    // few survivors; a handful of huge tiles would idle most SMs).  Every
+    // CTA derives the same T from the same count.
+    int T = TMAX;
+    {
+        const int64_t want = (count + 2 * (int64_t)gridDim.x - 1) / (2 * (int64_t)gridDim.x);
+        if (want < T) T = (int)(want < 256 ? 256 : ((want + 31) & ~int64_t(31)));
+        if (T > TMAX) T = TMAX;
+    }
     const int64_t ntiles = (count + T - 1) / T;
 
     unsigned long long st_sum = 0;
@@ -709,7 +719,7 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BLOCK, sm));
         if (occ < 1) occ = 1;
     }
-    const int64_t ntiles0 = (p0.n + p0.tile - 1) / p0.tile;
+    const int64_t ntiles0 = (p0.n + 255) / 256;  // smallest tile the kernel adapts to
     int64_t grid = (int64_t)h->sms * occ;
     if (grid > ntiles0) grid = ntiles0;
     if (grid < 1) grid = 1;

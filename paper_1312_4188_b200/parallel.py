@@ -53,37 +53,52 @@ def rule_shard(num_rules: int, info: RankInfo) -> tuple[int, int]:
     return partition_bounds(num_rules, info.world)[info.rank]
 
 
-def function_parallel_combine(local_first, local_comps=None, local_stats=None, group=None,
-                              async_op: bool = False):
-    """Fold every rank's shard-local results into global ones, in place.
+def _active(group) -> bool:
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
 
-    local_first: int32 tensor (global rule indices, NO_MATCH = none)
-    local_comps: optional int32 per-packet per-task comparisons -> SUM
-    local_stats: optional int64 [sum, max] -> [SUM, MAX]
+
+def all_reduce(t, op, group=None) -> None:
+    """In-place all-reduce.  NCCL reduces device tensors directly (NVLink /
+    NVSwitch); the gloo backend (CPU tests, shared-GPU smoke runs) reduces a
+    host copy."""
+    import torch.distributed as dist
+    if not _active(group):
+        return
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
+def function_parallel_combine(local_first, local_comps=None, local_stats=None, group=None) -> None:
+    """Fold every rank's shard-local results into global ones, in place
+    (engines.py:202-212 and 359-369 across GPUs).
+
+    local_first: int32 tensor (global rule indices, NO_MATCH = none) -> MIN
+    local_comps: optional int32 per-packet per-task comparisons      -> SUM
+    local_stats: optional int64 [sum, max]                           -> [SUM, MAX]
     """
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
-        return None
-    works = [dist.all_reduce(local_first, op=dist.ReduceOp.MIN, group=group, async_op=async_op)]
+    if not _active(group):
+        return
+    all_reduce(local_first, dist.ReduceOp.MIN, group)
     if local_comps is not None:
-        works.append(dist.all_reduce(local_comps, op=dist.ReduceOp.SUM, group=group, async_op=async_op))
+        all_reduce(local_comps, dist.ReduceOp.SUM, group)
     if local_stats is not None:
-        s, m = local_stats[0:1].clone(), local_stats[1:2].clone()
-        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
-        local_stats[0:1].copy_(s)
-        local_stats[1:2].copy_(m)
-    return works if async_op else None
+        reduce_stats(local_stats, group)
 
 
 def reduce_stats(stats, group=None) -> None:
-    """Data-parallel stats: [SUM of comparisons, MAX of comparisons] over ranks."""
+    """[SUM of comparisons, MAX of per-task comparisons] over ranks."""
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not _active(group):
         return
     s, m = stats[0:1].clone(), stats[1:2].clone()
-    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    all_reduce(s, dist.ReduceOp.SUM, group)
+    all_reduce(m, dist.ReduceOp.MAX, group)
     stats[0:1].copy_(s)
     stats[1:2].copy_(m)
 
