@@ -102,6 +102,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def measured_traffic(config: str, n: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one step, from the
+    committed ncu --set full capture (profiles/traffic.json), scaled to n."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh).get(config)
+    except (OSError, ValueError):
+        return None
+    if not d:
+        return None
+    return {"bytes_per_step": round(d["dram_bytes_per_step"] * n / d["packets"]),
+            "bytes_per_packet": round(d["dram_bytes_per_step"] / d["packets"], 1),
+            "algorithmic_bytes_per_packet": PKT_BYTES + OUT_BYTES, "source": d["source"]}
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -248,7 +264,7 @@ def main() -> int:
                                                stream=stream.cuda_stream)
             parallel.function_parallel_combine(first, comps, None)
         else:
-            compiled.scan_range_device(pkts, r_lo, r_hi, first=first, comps=comps, verdict=verdict,
+            compiled.scan_range_device(pkts, r_lo, r_hi, first=first, verdict=verdict,
                                        stats=stats, stream=stream.cuda_stream)
 
     def barrier():
@@ -301,7 +317,7 @@ def main() -> int:
     hbm_achieved = n * (PKT_BYTES + OUT_BYTES) / avg_launch_s / 1e9
     roof = {
         "bound": "int32", "achieved": round(achieved, 3), "peak": round(int_peak, 3), "unit": "Tops/s",
-        "frac": round(achieved / int_peak, 4), "traffic": None,
+        "frac": round(achieved / int_peak, 4), "traffic": measured_traffic(w.name, n),
         "ops_per_rule_test": K_OPS, "rule_tests_per_launch": local_comps,
         "peak_source": f"derived: {sms} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x "
                        f"sm_max_mhz {clk:.0f} ({peaks['_source']})",
