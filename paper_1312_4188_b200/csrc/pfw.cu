@@ -205,20 +205,6 @@ __device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t
            (__float_as_uint(dB) <= r[F_B_W]);
 }
 
-// Lowest matching rule of a stage for one packet, given that some lane hit:
-// every lane re-evaluates its KS rules (rows j: rule s + 32j + lane) and keeps
-// the lowest matching row, then one warp MIN reduction (REDUX) over the keys
-// 32j + lane picks the stage-local first match -- no serial ballot/branch chain.
-template <int KS, bool FMA>
-__device__ __forceinline__ unsigned stage_first(const uint32_t (&r)[KS][NF], uint32_t src, uint32_t dst,
-                                                float A, float A2, float B, uint32_t one, int lane) {
-    unsigned key = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = KS - 1; j >= 0; j--)
-        if (rule_test_slow<FMA>(r[j], src, dst, A, A2, B, one)) key = (unsigned)(j * 32 + lane);
-    return __reduce_min_sync(0xFFFFFFFFu, key);
-}
-
 constexpr int BLOCK = 256;
 constexpr int NWARPS = BLOCK / 32;
 
@@ -396,14 +382,26 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                     any0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
                     any1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
                 }
-                if (__any_sync(0xFFFFFFFFu, any0 | any1)) {
-                    if (__any_sync(0xFFFFFFFFu, any0)) {
-                        const unsigned k = stage_first<KS, FMA>(r, v0.x, v0.y, a0, c0, b0, one, lane);
-                        if (lane == 0) s_first[q0] = (uint32_t)(s + k);
+                if (__any_sync(0xFFFFFFFFu, any0)) {
+#pragma unroll
+                    for (int j = 0; j < KS; j++) {
+                        const unsigned b = __ballot_sync(
+                            0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one));
+                        if (b) {
+                            if (lane == 0) s_first[q0] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
+                            break;
+                        }
                     }
-                    if (__any_sync(0xFFFFFFFFu, any1)) {
-                        const unsigned k = stage_first<KS, FMA>(r, v1.x, v1.y, a1, c1, b1, one, lane);
-                        if (lane == 0) s_first[q1] = (uint32_t)(s + k);
+                }
+                if (__any_sync(0xFFFFFFFFu, any1)) {
+#pragma unroll
+                    for (int j = 0; j < KS; j++) {
+                        const unsigned b = __ballot_sync(
+                            0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one));
+                        if (b) {
+                            if (lane == 0) s_first[q1] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
+                            break;
+                        }
                     }
                 }
             }
@@ -416,8 +414,15 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
 #pragma unroll
                 for (int j = 0; j < KS; j++) any |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
                 if (__any_sync(0xFFFFFFFFu, any)) {
-                    const unsigned k = stage_first<KS, FMA>(r, v.x, v.y, a, c, bb, one, lane);
-                    if (lane == 0) s_first[q] = (uint32_t)(s + k);
+#pragma unroll
+                    for (int j = 0; j < KS; j++) {
+                        const unsigned b =
+                            __ballot_sync(0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v.x, v.y, a, c, bb, one));
+                        if (b) {
+                            if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
+                            break;
+                        }
+                    }
                 }
             }
             // live counter alternates between two slots so that resetting one
