@@ -195,6 +195,9 @@ def main() -> int:
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--first-pass", type=int, default=-1, help="rules in the first pass (0 = single pass)")
+    ap.add_argument("--fused", action="store_true",
+                    help="function config: combine fused into the scan epilogue (NVLink atomics via "
+                         "CUDA IPC, reduce-scatter result) instead of the NCCL all-reduce")
     args = ap.parse_args()
 
     from paper_1312_4188_b200 import workloads
@@ -255,9 +258,15 @@ def main() -> int:
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    fused = None
+    if args.fused and w.model == "function":
+        fused = parallel.FusedFunctionParallel(compiled, n, scatter=True, with_comps=True)
+
     def step():
         stats.zero_()
-        if w.model == "function":
+        if fused is not None:
+            fused.run(pkts, stats=stats, stream=stream.cuda_stream)
+        elif w.model == "function":
             _native.check(_native.lib().pfw_accumulator_init(n, first.data_ptr(), comps.data_ptr(),
                                                              stream.cuda_stream), "init")
             compiled.scan_partition_accumulate(pkts, r_lo, r_hi, first, comps, stats,
@@ -373,7 +382,9 @@ def main() -> int:
                     "TrafficProfile(N, seed=2)), generated on the GPU bit-exactly",
             "config": {"workload": w.description, "rules": R, "packets": w.packets,
                        "packets_per_gpu": n, "model": w.model,
-                       "parallelism": f"{'rule' if w.model == 'function' else 'packet'}-sharded x{world}",
+                       "parallelism": f"{'rule' if w.model == 'function' else 'packet'}-sharded x{world}"
+                                      + (" (fused NVLink-atomic combine)" if fused is not None else
+                                         " (NCCL MIN all-reduce)" if w.model == "function" else ""),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "kernel": _native.version()},
             "roofline": roof,

@@ -103,6 +103,32 @@ int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const
                                   uint64_t *d_stats, void *stream);
 int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *stream);
 
+/* Fused function-parallel combine.  Scans the rule shard
+ * [lo, hi) like pfw_scan_partition_accumulate, but the kernel epilogue folds
+ * each resolved packet straight into the ranks' result buffers with NVLink
+ * atomics (atomicMin of the first match, atomicAdd of the per-task
+ * comparisons), replacing the separate NCCL MIN all-reduce of
+ * engines.py:202-212 and the sum of engines.py:366-367.
+ *   h_peer_first[t] / h_peer_comps[t]: rank t's buffers as mapped in this
+ *     process (pfw_ipc_open; the caller's own buffer for its own rank);
+ *     h_peer_comps may be NULL.  Buffers start at PFW_NO_MATCH / 0.
+ *   scatter = 0: every rank's buffer holds all n packets (all-reduce result);
+ *   scatter = 1: packet i is held by its owner rank (balanced contiguous
+ *     shards of n, partition_bounds semantics) at offset i - shard start
+ *     (reduce-scatter result, one atomic per packet).
+ * Completion: the combine is complete on every rank once all ranks' kernels
+ * have finished (e.g. stream synchronize + a host barrier). */
+int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
+                       uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps, int npeers,
+                       int scatter, uint64_t *d_stats, void *stream);
+
+/* CUDA IPC plumbing for the fused combine: export a device allocation, map a
+ * peer's allocation into this process (NVLink peer access), unmap it. */
+int pfw_ipc_handle_size(void);
+int pfw_ipc_get_handle(const void *d_ptr, void *out_handle);
+int pfw_ipc_open(int device, const void *handle, void **out_ptr);
+int pfw_ipc_close(int device, void *ptr);
+
 /* Verdicts from final first-match indices (classifier.py:175-185). */
 int pfw_verdicts(pfw_ruleset_t h, const uint32_t *d_first, int64_t n, uint8_t *d_verdict,
                  void *stream);

@@ -104,6 +104,7 @@ int g_ctas_per_sm = 0;   // 0 = occupancy query
 int g_force_imad = 1;    // route the subtract through IMAD (FMA pipe)
 int g_first_pass = 1024; // rules in the first pass (0 = single pass); passes double
 constexpr int MAX_PASSES = 32;
+constexpr int MAX_PEERS = 64;
 
 }  // namespace
 
@@ -127,6 +128,7 @@ struct pfw_ruleset {
     cudaStream_t streams[2] = {nullptr, nullptr};
     cudaEvent_t ev_done = nullptr;
     ScanWs ws;         // default (calls on the caller's stream)
+    uint32_t **d_peers = nullptr;  // 2 * MAX_PEERS device pointer table (fused combine)
     ScanWs ws_e2e[2];  // pfw_classify_host slots
 };
 
@@ -154,7 +156,15 @@ struct ScanParams {
     unsigned int *tile_counter;
     int tile;
     uint32_t one;  // runtime 1: keeps ptxas from folding x*1+c into IADD3
+    // MODE_PEER (fused function-parallel combine): result buffers of every
+    // rank, reached over NVLink through CUDA IPC mappings
+    uint32_t *const *peer_first;
+    uint32_t *const *peer_comps;
+    int npeers;
+    int scatter;  // 1: packet id lives on its owner rank (balanced shards of n)
 };
+
+enum { MODE_WRITE = 0, MODE_ACC = 1, MODE_PEER = 2 };
 
 __device__ __forceinline__ uint32_t sub_fma(uint32_t x, uint32_t one, uint32_t nlo) {
     uint32_t d;
@@ -203,6 +213,28 @@ __device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t
     const float dB = __fsub_rn(B, -__uint_as_float(r[F_B_NLO]));
     return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
            (__float_as_uint(dB) <= r[F_B_W]);
+}
+
+// Stage-local first match among rows [J0, J1) for one packet (some lane hit
+// there): rows in rule order, one ballot each, stop at the first non-empty.
+template <int KS, int J0, int J1, bool FMA>
+__device__ __forceinline__ unsigned rows_first(const uint32_t (&r)[KS][NF], uint32_t src, uint32_t dst,
+                                               float A, float A2, float B, uint32_t one) {
+#pragma unroll
+    for (int j = J0; j < J1; j++) {
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, rule_test_slow<FMA>(r[j], src, dst, A, A2, B, one));
+        if (b) return (unsigned)(j * 32 + __ffs(b) - 1);
+    }
+    return 0xFFFFFFFFu;  // unreachable when the caller's vote hit
+}
+
+// Slow path: the stage hit; the half-stage accumulators say which half holds
+// the first match, so at most KS/2 rows are re-evaluated.
+template <int KS, bool FMA>
+__device__ __forceinline__ unsigned stage_first(const uint32_t (&r)[KS][NF], bool accA, uint32_t src,
+                                                uint32_t dst, float A, float A2, float B, uint32_t one) {
+    if (__any_sync(0xFFFFFFFFu, accA)) return rows_first<KS, 0, KS / 2, FMA>(r, src, dst, A, A2, B, one);
+    return rows_first<KS, KS / 2, KS, FMA>(r, src, dst, A, A2, B, one);
 }
 
 constexpr int BLOCK = 256;
@@ -265,7 +297,7 @@ __device__ __forceinline__ void issue_stage(const ScanParams &p, int64_t s, uint
     for (int f = 0; f < NF; f++) tma_bulk_g2s(buf + f * 32 * KS, p.rules + f * p.rpad + s, ROW, bar);
 }
 
-template <int KS, bool ACC, bool FMA>
+template <int KS, int MODE, bool FMA>
 __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int TMAX = p.tile;  // shared-memory capacity in packets
@@ -368,7 +400,9 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
             }
             // Two live packets per iteration: independent chains for ILP and
             // half the loop overhead.  Packets are warp-uniform, so every
-            // branch below is warp-uniform too.
+            // branch below is warp-uniform too.  Rows are OR-ed into two
+            // half-stage accumulators (same PLOP3 count as one) so the slow
+            // path knows which half holds the first match.
             int i = warp;
             for (; i + NWARPS < nlive; i += 2 * NWARPS) {
                 const int q0 = live[i], q1 = live[i + NWARPS];
@@ -376,33 +410,24 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 const float b0 = __uint_as_float(s_pr[q0]), b1 = __uint_as_float(s_pr[q1]);
                 const float a0 = __uint_as_float(v0.z), c0 = __uint_as_float(v0.w);
                 const float a1 = __uint_as_float(v1.z), c1 = __uint_as_float(v1.w);
-                bool any0 = false, any1 = false;
+                bool lo0 = false, hi0 = false, lo1 = false, hi1 = false;
 #pragma unroll
-                for (int j = 0; j < KS; j++) {
-                    any0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
-                    any1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
+                for (int j = 0; j < KS / 2; j++) {
+                    lo0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
+                    lo1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
                 }
-                if (__any_sync(0xFFFFFFFFu, any0)) {
 #pragma unroll
-                    for (int j = 0; j < KS; j++) {
-                        const unsigned b = __ballot_sync(
-                            0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one));
-                        if (b) {
-                            if (lane == 0) s_first[q0] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
-                            break;
-                        }
-                    }
+                for (int j = KS / 2; j < KS; j++) {
+                    hi0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
+                    hi1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
                 }
-                if (__any_sync(0xFFFFFFFFu, any1)) {
-#pragma unroll
-                    for (int j = 0; j < KS; j++) {
-                        const unsigned b = __ballot_sync(
-                            0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one));
-                        if (b) {
-                            if (lane == 0) s_first[q1] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
-                            break;
-                        }
-                    }
+                if (__any_sync(0xFFFFFFFFu, lo0 | hi0)) {
+                    const unsigned k = stage_first<KS, FMA>(r, lo0, v0.x, v0.y, a0, c0, b0, one);
+                    if (lane == 0) s_first[q0] = (uint32_t)(s + k);
+                }
+                if (__any_sync(0xFFFFFFFFu, lo1 | hi1)) {
+                    const unsigned k = stage_first<KS, FMA>(r, lo1, v1.x, v1.y, a1, c1, b1, one);
+                    if (lane == 0) s_first[q1] = (uint32_t)(s + k);
                 }
             }
             if (i < nlive) {
@@ -410,19 +435,14 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 const uint4 v = s_pk[q];
                 const float bb = __uint_as_float(s_pr[q]);
                 const float a = __uint_as_float(v.z), c = __uint_as_float(v.w);
-                bool any = false;
+                bool lo = false, hi = false;
 #pragma unroll
-                for (int j = 0; j < KS; j++) any |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
-                if (__any_sync(0xFFFFFFFFu, any)) {
+                for (int j = 0; j < KS / 2; j++) lo |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
 #pragma unroll
-                    for (int j = 0; j < KS; j++) {
-                        const unsigned b =
-                            __ballot_sync(0xFFFFFFFFu, rule_test_slow<FMA>(r[j], v.x, v.y, a, c, bb, one));
-                        if (b) {
-                            if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(b) - 1);
-                            break;
-                        }
-                    }
+                for (int j = KS / 2; j < KS; j++) hi |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
+                if (__any_sync(0xFFFFFFFFu, lo | hi)) {
+                    const unsigned k = stage_first<KS, FMA>(r, lo, v.x, v.y, a, c, bb, one);
+                    if (lane == 0) s_first[q] = (uint32_t)(s + k);
                 }
             }
             // live counter alternates between two slots so that resetting one
@@ -473,9 +493,28 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 survive = !final_pass && f == PFW_NO_MATCH;
                 if (!survive) {
                     const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.lo + 1) : span;
-                    if (ACC) {
+                    if (MODE == MODE_ACC) {
                         if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
                         p.comps[id] += c;
+                    } else if (MODE == MODE_PEER) {
+                        // the engines.py:202-212 min-combine and :366-367 sum,
+                        // issued straight from the scan epilogue into the
+                        // ranks' buffers (NVLink atomics), overlapping the
+                        // transfer with the remaining tiles' compute
+                        if (p.scatter) {
+                            const uint64_t q = (uint64_t)p.n / (uint64_t)p.npeers;
+                            const uint64_t r = (uint64_t)p.n % (uint64_t)p.npeers;
+                            const uint64_t big = (q + 1) * r;
+                            const uint64_t o = id < big ? id / (q + 1) : r + (id - big) / q;
+                            const uint64_t off = id - (o < r ? o * (q + 1) : big + (o - r) * q);
+                            if (f != PFW_NO_MATCH) atomicMin(p.peer_first[o] + off, f);
+                            if (p.peer_comps) atomicAdd(p.peer_comps[o] + off, c);
+                        } else {
+                            for (int t = 0; t < p.npeers; t++) {
+                                if (f != PFW_NO_MATCH) atomicMin(p.peer_first[t] + id, f);
+                                if (p.peer_comps) atomicAdd(p.peer_comps[t] + id, c);
+                            }
+                        }
                     } else {
                         p.first[id] = f;
                         if (p.comps) p.comps[id] = c;
@@ -704,10 +743,10 @@ std::vector<int64_t> plan_passes(int64_t lo, int64_t hi, int stage) {
     return b;
 }
 
-template <int KS, bool ACC, bool FMA>
+template <int KS, int MODE, bool FMA>
 int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t st) {
     const size_t sm = smem_bytes(p0.tile, KS);
-    auto kern = scan_kernel<KS, ACC, FMA>;
+    auto kern = scan_kernel<KS, MODE, FMA>;
     int maxsm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     if (sm > (size_t)maxsm)
@@ -750,19 +789,20 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
     return PFW_OK;
 }
 
-template <bool ACC, bool FMA>
+template <int MODE, bool FMA>
 int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t st) {
     switch (g_ks) {
-        case 2: return launch_scan_t<2, ACC, FMA>(h, p, ws, st);
-        case 4: return launch_scan_t<4, ACC, FMA>(h, p, ws, st);
-        case 8: return launch_scan_t<8, ACC, FMA>(h, p, ws, st);
+        case 2: return launch_scan_t<2, MODE, FMA>(h, p, ws, st);
+        case 4: return launch_scan_t<4, MODE, FMA>(h, p, ws, st);
+        case 8: return launch_scan_t<8, MODE, FMA>(h, p, ws, st);
         default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4 or 8)", g_ks);
     }
 }
 
-int launch_scan(pfw_ruleset *h, bool acc, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
+int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                 uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
-                cudaStream_t st, ScanWs *ws = nullptr) {
+                cudaStream_t st, ScanWs *ws = nullptr, const ScanParams *peer = nullptr) {
+    const bool acc = mode == MODE_ACC;
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count %lld", (long long)n);
     if (n > 0xFFFFFFFFll) return set_err(PFW_ERR_INVALID, "more than 2^32-1 packets in one call");
@@ -771,7 +811,7 @@ int launch_scan(pfw_ruleset *h, bool acc, int64_t lo, int64_t hi, const void *d_
     if (hi > h->n) return set_err(PFW_ERR_INVALID, "rule window end %lld beyond ruleset of %lld",
                                   (long long)hi, (long long)h->n);
     if (n == 0) return PFW_OK;
-    if (!d_pkts || !first) return set_err(PFW_ERR_INVALID, "null packet or output pointer");
+    if (!d_pkts || (!first && mode != MODE_PEER)) return set_err(PFW_ERR_INVALID, "null packet or output pointer");
     if (acc && !comps) return set_err(PFW_ERR_INVALID, "accumulate needs a comps buffer");
     if (lo > hi) lo = hi;  // empty window: scan_range returns all -1
     ScanParams p{};
@@ -790,9 +830,21 @@ int launch_scan(pfw_ruleset *h, bool acc, int64_t lo, int64_t hi, const void *d_
     p.one = 1;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
+    if (peer) {
+        p.peer_first = peer->peer_first;
+        p.peer_comps = peer->peer_comps;
+        p.npeers = peer->npeers;
+        p.scatter = peer->scatter;
+    }
     ScanWs &w = ws ? *ws : h->ws;
-    if (acc) return g_force_imad ? launch_scan_ks<true, true>(h, p, w, st) : launch_scan_ks<true, false>(h, p, w, st);
-    return g_force_imad ? launch_scan_ks<false, true>(h, p, w, st) : launch_scan_ks<false, false>(h, p, w, st);
+    switch (mode) {
+        case MODE_ACC:
+            return g_force_imad ? launch_scan_ks<MODE_ACC, true>(h, p, w, st) : launch_scan_ks<MODE_ACC, false>(h, p, w, st);
+        case MODE_PEER:
+            return g_force_imad ? launch_scan_ks<MODE_PEER, true>(h, p, w, st) : launch_scan_ks<MODE_PEER, false>(h, p, w, st);
+        default:
+            return g_force_imad ? launch_scan_ks<MODE_WRITE, true>(h, p, w, st) : launch_scan_ks<MODE_WRITE, false>(h, p, w, st);
+    }
 }
 
 int grid_for(int64_t n) {
@@ -935,6 +987,7 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     if (h->d_accept) cudaFree(h->d_accept);
     if (h->d_ws) cudaFree(h->d_ws);
     free_ws(h->ws);
+    if (h->d_peers) cudaFree(h->d_peers);
     free_ws(h->ws_e2e[0]);
     free_ws(h->ws_e2e[1]);
     for (auto &s : h->streams)
@@ -967,15 +1020,71 @@ int pfw_pack_packets_host(int64_t n, const uint8_t *proto, const uint32_t *src_i
 int pfw_scan_range(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                    uint32_t *d_first, uint32_t *d_comps, uint8_t *d_verdict, uint64_t *d_stats,
                    void *stream) {
-    return launch_scan(h, false, lo, hi, d_pkts, n, d_first, d_comps, d_verdict, d_stats,
+    return launch_scan(h, MODE_WRITE, lo, hi, d_pkts, n, d_first, d_comps, d_verdict, d_stats,
                        (cudaStream_t)stream);
 }
 
 int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts,
                                   int64_t n, uint32_t *d_first, uint32_t *d_comps,
                                   uint64_t *d_stats, void *stream) {
-    return launch_scan(h, true, lo, hi, d_pkts, n, d_first, d_comps, nullptr, d_stats,
+    return launch_scan(h, MODE_ACC, lo, hi, d_pkts, n, d_first, d_comps, nullptr, d_stats,
                        (cudaStream_t)stream);
+}
+
+int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
+                       uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps, int npeers,
+                       int scatter, uint64_t *d_stats, void *stream) {
+    if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
+    if (npeers < 1 || npeers > MAX_PEERS) return set_err(PFW_ERR_INVALID, "npeers must be in 1..%d", MAX_PEERS);
+    if (!h_peer_first) return set_err(PFW_ERR_INVALID, "null peer table");
+    for (int i = 0; i < npeers; i++)
+        if (!h_peer_first[i] || (h_peer_comps && !h_peer_comps[i]))
+            return set_err(PFW_ERR_INVALID, "null peer buffer %d", i);
+    if (n == 0) return PFW_OK;
+    DeviceGuard g(h->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!h->d_peers) CUDA_TRY(cudaMalloc(&h->d_peers, 2 * MAX_PEERS * sizeof(uint32_t *)));
+    uint32_t *tab[2 * MAX_PEERS] = {};
+    for (int i = 0; i < npeers; i++) {
+        tab[i] = h_peer_first[i];
+        tab[MAX_PEERS + i] = h_peer_comps ? h_peer_comps[i] : nullptr;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->d_peers, tab, sizeof tab, cudaMemcpyHostToDevice, st));
+    // the table is read by the kernel later on the same stream; keep the host
+    // copy alive until the copy has been issued (pageable -> staged now)
+    ScanParams peer{};
+    peer.peer_first = h->d_peers;
+    peer.peer_comps = h_peer_comps ? h->d_peers + MAX_PEERS : nullptr;
+    peer.npeers = npeers;
+    peer.scatter = scatter ? 1 : 0;
+    return launch_scan(h, MODE_PEER, lo, hi, d_pkts, n, nullptr, nullptr, nullptr, d_stats, st, nullptr,
+                       &peer);
+}
+
+int pfw_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int pfw_ipc_get_handle(const void *d_ptr, void *out) {
+    if (!d_ptr || !out) return set_err(PFW_ERR_INVALID, "null pointer");
+    cudaIpcMemHandle_t hd;
+    CUDA_TRY(cudaIpcGetMemHandle(&hd, const_cast<void *>(d_ptr)));
+    memcpy(out, &hd, sizeof hd);
+    return PFW_OK;
+}
+
+int pfw_ipc_open(int device, const void *handle, void **out_ptr) {
+    if (!handle || !out_ptr) return set_err(PFW_ERR_INVALID, "null pointer");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, handle, sizeof hd);
+    CUDA_TRY(cudaIpcOpenMemHandle(out_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    return PFW_OK;
+}
+
+int pfw_ipc_close(int device, void *ptr) {
+    if (!ptr) return PFW_OK;
+    DeviceGuard g(device);
+    CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return PFW_OK;
 }
 
 int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *stream) {
@@ -1049,7 +1158,7 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
         uint8_t *dv = reinterpret_cast<uint8_t *>(base + (size_t)chunk * 20);
         CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
                                  cudaMemcpyHostToDevice, st));
-        rc = launch_scan(h, false, 0, h->n, dp, m, df, nullptr, h_verdict ? dv : nullptr,
+        rc = launch_scan(h, MODE_WRITE, 0, h->n, dp, m, df, nullptr, h_verdict ? dv : nullptr,
                          h_stats ? d_stats : nullptr, st, &h->ws_e2e[k & 1]);
         if (rc != PFW_OK) break;
         CUDA_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, st));

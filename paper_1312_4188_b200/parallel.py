@@ -129,3 +129,98 @@ def run_data_parallel(scan: Callable[[int, int], tuple], total_packets: int, gro
     if reduce and stats is not None:
         reduce_stats(stats, group)
     return (a, b), first, comps, stats
+
+
+class FusedFunctionParallel:
+    """Function-parallel across ranks with the MIN / SUM combine fused into the
+    scan kernel's epilogue: every rank scans its rule shard
+    of the replicated batch and writes resolved packets straight into the
+    owner rank's result buffer with NVLink atomics (CUDA IPC mappings), so
+    the exchange overlaps the scan tile by tile instead of following it as a
+    separate all-reduce.
+
+    scatter=True (default): rank t ends up holding packets
+    ``packet_shard(n, t)`` (reduce-scatter result, one atomic per packet);
+    scatter=False: every rank holds all n results (all-reduce result,
+    world atomics per packet).
+    """
+
+    def __init__(self, compiled, n: int, scatter: bool = True, with_comps: bool = True, group=None):
+        import ctypes
+        import torch
+        import torch.distributed as dist
+        from . import _native
+        self.compiled, self.n, self.scatter, self.group = compiled, n, scatter, group
+        self.info = rank_info(group)
+        self.device = compiled.device
+        dev = f"cuda:{self.device}"
+        self.own_range = packet_shard(n, self.info) if scatter else (0, n)
+        m = self.own_range[1] - self.own_range[0]
+        # never allocate 0 bytes: IPC needs a real allocation on every rank
+        self.first = torch.full((max(m, 1),), NO_MATCH, dtype=torch.int32, device=dev)
+        self.comps = torch.zeros(max(m, 1), dtype=torch.int32, device=dev) if with_comps else None
+        lib = _native.lib()
+        hs = lib.pfw_ipc_handle_size()
+
+        def handle(t):
+            buf = ctypes.create_string_buffer(hs)
+            _native.check(lib.pfw_ipc_get_handle(t.data_ptr(), buf), "pfw_ipc_get_handle")
+            return buf.raw
+
+        mine = (handle(self.first), handle(self.comps) if with_comps else None)
+        world = self.info.world
+        if world > 1:
+            allh = [None] * world
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self._opened = []
+        firsts, comps = [], []
+        for t, (hf, hc) in enumerate(allh):
+            if t == self.info.rank:
+                firsts.append(self.first.data_ptr())
+                comps.append(self.comps.data_ptr() if with_comps else None)
+                continue
+            for hnd, out in ((hf, firsts), (hc, comps)):
+                if hnd is None:
+                    out.append(None)
+                    continue
+                ptr = ctypes.c_void_p()
+                _native.check(lib.pfw_ipc_open(self.device, hnd, ctypes.byref(ptr)), "pfw_ipc_open")
+                self._opened.append(ptr.value)
+                out.append(ptr.value)
+        P = ctypes.c_void_p
+        self._peer_first = (P * world)(*firsts)
+        self._peer_comps = (P * world)(*comps) if with_comps else None
+
+    def _barrier(self):
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        if self.info.world > 1:
+            dist.barrier(group=self.group)
+
+    def run(self, pkts, stats=None, stream: int | None = None):
+        """Reset, scan this rank's rule shard with the fused combine, and return
+        this rank's (first, comps) once every rank's scan has completed."""
+        import torch
+        from . import _native
+        self.first.fill_(NO_MATCH)
+        if self.comps is not None:
+            self.comps.zero_()
+        self._barrier()  # nobody writes into a buffer before its owner reset it
+        lo, hi = rule_shard(self.compiled.num_rules, self.info)
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        _native.check(_native.lib().pfw_scan_fused_min(
+            self.compiled.handle, lo, hi, pkts.data.data_ptr(), len(pkts), self._peer_first,
+            self._peer_comps, self.info.world, 1 if self.scatter else 0,
+            None if stats is None else stats.data_ptr(), st), "pfw_scan_fused_min")
+        self._barrier()  # every rank's atomics have landed
+        m = self.own_range[1] - self.own_range[0]
+        return self.first[:m], (self.comps[:m] if self.comps is not None else None)
+
+    def close(self):
+        from . import _native
+        for ptr in self._opened:
+            _native.lib().pfw_ipc_close(self.device, ptr)
+        self._opened = []

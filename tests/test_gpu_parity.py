@@ -362,3 +362,54 @@ def test_full_size_properties_data_parallel():
     want = oracle.scan_range(rules, sub, 0, R)
     got = np.where(hit[idx], f[idx].astype(np.int64), -1)
     np.testing.assert_array_equal(got, want)
+
+
+# ------------------------------------------------------ fused function-parallel
+
+@pytest.mark.parametrize("scatter", [0, 1])
+def test_fused_min_combine_virtual_ranks(scatter):
+    """G virtual ranks on one GPU: each scans its rule shard with the fused
+    epilogue into the G result buffers (local memory stands in for the IPC
+    peer mappings) -- equals the function-parallel model with nodes = G."""
+    import ctypes
+    g = golden("engine_r503_t600.npz")
+    c = compiled(golden_rules("r503_s24_w30"))
+    p = dev_pkts(golden_traffic("t600_s25"))
+    n = len(p)
+    for G in (1, 2, 3, 8):
+        bounds = pfw.partition_bounds(n, G)
+        if scatter:
+            first = torch.full((n,), NO_MATCH, dtype=torch.int32, device="cuda:0")
+            comps = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+            fptr = [first.data_ptr() + 4 * a for a, _ in bounds]
+            cptr = [comps.data_ptr() + 4 * a for a, _ in bounds]
+            bufs = [(first, comps)]
+        else:
+            bufs = [(torch.full((n,), NO_MATCH, dtype=torch.int32, device="cuda:0"),
+                     torch.zeros(n, dtype=torch.int32, device="cuda:0")) for _ in range(G)]
+            fptr = [b[0].data_ptr() for b in bufs]
+            cptr = [b[1].data_ptr() for b in bufs]
+        P = ctypes.c_void_p
+        stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+        for lo, hi in pfw.partition_bounds(c.num_rules, G):
+            _native.check(_native.lib().pfw_scan_fused_min(
+                c.handle, lo, hi, p.data.data_ptr(), n, (P * G)(*fptr), (P * G)(*cptr), G, scatter,
+                stats.data_ptr(), torch.cuda.current_stream().cuda_stream), "fused")
+        torch.cuda.synchronize()
+        for first, comps in bufs:
+            np.testing.assert_array_equal(first_to_host(first), g[f"function_{G}_first"])
+            np.testing.assert_array_equal(comps.cpu().numpy(), g[f"function_{G}_comps"])
+        total, mx, _ = g[f"function_{G}_stats"].tolist()
+        assert stats.cpu().tolist() == [total, mx]
+
+
+def test_fused_function_parallel_single_rank_class():
+    from paper_1312_4188_b200.parallel import FusedFunctionParallel
+    g = golden("engine_r100000_t2000.npz")
+    c = compiled(golden_rules("r100000_s1"))
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=2000, seed=2), device=0)
+    fused = FusedFunctionParallel(c, len(p))
+    first, comps = fused.run(p)
+    np.testing.assert_array_equal(first_to_host(first), g["function_1_first"])
+    np.testing.assert_array_equal(comps.cpu().numpy(), g["function_1_comps"])
+    fused.close()
