@@ -122,12 +122,14 @@ int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pk
                        uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps, int npeers,
                        int scatter, uint64_t *d_stats, void *stream);
 
-/* CUDA IPC plumbing for the fused combine: export a device allocation, map a
- * peer's allocation into this process (NVLink peer access), unmap it. */
+/* CUDA IPC plumbing for the fused combine.  pfw_ipc_get_handle exports the
+ * allocation containing d_ptr and returns d_ptr's byte offset in it;
+ * pfw_ipc_open maps a peer's allocation (NVLink peer access) and returns its
+ * BASE -- add the exported offset; pfw_ipc_close unmaps that base. */
 int pfw_ipc_handle_size(void);
-int pfw_ipc_get_handle(const void *d_ptr, void *out_handle);
-int pfw_ipc_open(int device, const void *handle, void **out_ptr);
-int pfw_ipc_close(int device, void *ptr);
+int pfw_ipc_get_handle(const void *d_ptr, void *out_handle, uint64_t *offset);
+int pfw_ipc_open(int device, const void *handle, void **out_base);
+int pfw_ipc_close(int device, void *base);
 
 /* Verdicts from final first-match indices (classifier.py:175-185). */
 int pfw_verdicts(pfw_ruleset_t h, const uint32_t *d_first, int64_t n, uint8_t *d_verdict,

@@ -1063,20 +1063,40 @@ int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pk
 
 int pfw_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 
-int pfw_ipc_get_handle(const void *d_ptr, void *out) {
-    if (!d_ptr || !out) return set_err(PFW_ERR_INVALID, "null pointer");
+// cudaIpcGetMemHandle exports the whole allocation that contains d_ptr; a
+// caching allocator (torch) hands out pointers inside larger blocks, so the
+// byte offset of d_ptr from the allocation base travels with the handle.
+// The base comes from the driver's cuMemGetAddressRange, fetched through the
+// runtime so that libpfw.so does not link libcuda (it must load without a GPU).
+int pfw_ipc_get_handle(const void *d_ptr, void *out, uint64_t *offset) {
+    if (!d_ptr || !out || !offset) return set_err(PFW_ERR_INVALID, "null pointer");
+    typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+    static range_fn get_range = nullptr;
+    if (!get_range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess)
+            return set_err(PFW_ERR_CUDA, "cuMemGetAddressRange not available");
+        get_range = (range_fn)fn;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (unsigned long long)(uintptr_t)d_ptr) != 0)
+        return set_err(PFW_ERR_CUDA, "cuMemGetAddressRange failed for %p", d_ptr);
     cudaIpcMemHandle_t hd;
     CUDA_TRY(cudaIpcGetMemHandle(&hd, const_cast<void *>(d_ptr)));
     memcpy(out, &hd, sizeof hd);
+    *offset = (uint64_t)((uintptr_t)d_ptr - (uintptr_t)base);
     return PFW_OK;
 }
 
-int pfw_ipc_open(int device, const void *handle, void **out_ptr) {
-    if (!handle || !out_ptr) return set_err(PFW_ERR_INVALID, "null pointer");
+int pfw_ipc_open(int device, const void *handle, void **out_base) {
+    if (!handle || !out_base) return set_err(PFW_ERR_INVALID, "null pointer");
     DeviceGuard g(device);
     cudaIpcMemHandle_t hd;
     memcpy(&hd, handle, sizeof hd);
-    CUDA_TRY(cudaIpcOpenMemHandle(out_ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    CUDA_TRY(cudaIpcOpenMemHandle(out_base, hd, cudaIpcMemLazyEnablePeerAccess));
     return PFW_OK;
 }
 

@@ -164,8 +164,9 @@ class FusedFunctionParallel:
 
         def handle(t):
             buf = ctypes.create_string_buffer(hs)
-            _native.check(lib.pfw_ipc_get_handle(t.data_ptr(), buf), "pfw_ipc_get_handle")
-            return buf.raw
+            off = ctypes.c_uint64()
+            _native.check(lib.pfw_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)), "pfw_ipc_get_handle")
+            return buf.raw, off.value
 
         mine = (handle(self.first), handle(self.comps) if with_comps else None)
         world = self.info.world
@@ -185,10 +186,11 @@ class FusedFunctionParallel:
                 if hnd is None:
                     out.append(None)
                     continue
-                ptr = ctypes.c_void_p()
-                _native.check(lib.pfw_ipc_open(self.device, hnd, ctypes.byref(ptr)), "pfw_ipc_open")
-                self._opened.append(ptr.value)
-                out.append(ptr.value)
+                raw, off = hnd
+                base = ctypes.c_void_p()
+                _native.check(lib.pfw_ipc_open(self.device, raw, ctypes.byref(base)), "pfw_ipc_open")
+                self._opened.append(base.value)
+                out.append(base.value + off)
         P = ctypes.c_void_p
         self._peer_first = (P * world)(*firsts)
         self._peer_comps = (P * world)(*comps) if with_comps else None
