@@ -192,7 +192,7 @@ def main() -> int:
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-chunk", type=int, default=1 << 23, help="packets per H2D/scan/D2H chunk")
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 22, help="packets per H2D/scan/D2H chunk")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--first-pass", type=int, default=-1, help="rules in the first pass (0 = single pass)")
@@ -366,7 +366,7 @@ def main() -> int:
         e2e = {"value": pk_per_step * args.steps / float(tt.item()) / 1e6, "unit": "Mpps",
                "h2d_bytes_per_step": n * PKT_BYTES, "d2h_bytes_per_step": n * 5,
                "api": f"pfw_classify_host (C-ABI, pinned host buffers, {args.e2e_chunk}-packet chunks, "
-                      "2 streams)"}
+                      "copy-in / 2x compute / copy-out streams, 3 slots)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -105,6 +105,7 @@ int g_force_imad = 1;    // route the subtract through IMAD (FMA pipe)
 int g_first_pass = 1024; // rules in the first pass (0 = single pass); passes double
 constexpr int MAX_PASSES = 32;
 constexpr int MAX_PEERS = 64;
+constexpr int E2E_SLOTS = 3;
 
 }  // namespace
 
@@ -125,8 +126,8 @@ struct pfw_ruleset {
     // e2e workspace
     void *d_ws = nullptr;
     size_t ws_bytes = 0;
-    cudaStream_t streams[2] = {nullptr, nullptr};
-    cudaEvent_t ev_done = nullptr;
+    cudaStream_t streams[4] = {};  // e2e copy-in, compute x2 (alternating chunks), copy-out
+    cudaEvent_t events[3 * 3] = {};                          // e2e per-slot in / scan / out
     ScanWs ws;         // default (calls on the caller's stream)
     uint32_t **d_peers = nullptr;  // 2 * MAX_PEERS device pointer table (fused combine)
     ScanWs ws_e2e[2];  // pfw_classify_host slots
@@ -990,9 +991,10 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     if (h->d_peers) cudaFree(h->d_peers);
     free_ws(h->ws_e2e[0]);
     free_ws(h->ws_e2e[1]);
-    for (auto &s : h->streams)
-        if (s) cudaStreamDestroy(s);
-    if (h->ev_done) cudaEventDestroy(h->ev_done);
+    for (auto &st : h->streams)
+        if (st) cudaStreamDestroy(st);
+    for (auto &ev : h->events)
+        if (ev) cudaEventDestroy(ev);
     delete h;
     return PFW_OK;
 }
@@ -1140,6 +1142,13 @@ int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d
 
 int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *h_first,
                       uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
+    // Three-stage pipeline over E2E_SLOTS buffer slots:
+    //   copy-in stream   H2D chunk k into slot k%S     (waits: scan k-S done)
+    //   compute streams  scan chunk k on stream k%2    (waits: H2D k done); two
+    //                    streams let chunk k+1's first pass fill the SMs
+    //                    while chunk k's small late passes finish
+    //   copy-out stream  D2H results of chunk k        (waits: scan k done)
+    // so H2D of later chunks, the scans and D2H of earlier chunks all overlap.
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count");
     if (h_stats) h_stats[0] = h_stats[1] = 0;
@@ -1149,9 +1158,9 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
     if (chunk > n) chunk = n;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
-    // per-slot layout: packets (16B) + first (4B) + verdict (1B), 2 slots + stats
-    const size_t slot = (size_t)chunk * 21 + 256;
-    const size_t need = 2 * slot + 256;
+    constexpr int S = E2E_SLOTS;
+    const size_t slot = (((size_t)chunk * 21 + 255) / 256) * 256;  // packets 16B + first 4B + verdict 1B
+    const size_t need = S * slot + 256;
     if (h->ws_bytes < need) {
         if (h->d_ws) cudaFree(h->d_ws);
         h->d_ws = nullptr;
@@ -1159,35 +1168,45 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
         CUDA_TRY(cudaMalloc(&h->d_ws, need));
         h->ws_bytes = need;
     }
-    for (auto &s : h->streams)
-        if (!s) CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (auto &st : h->streams)
+        if (!st) CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto &ev : h->events)
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaStream_t s_in = h->streams[0], s_out = h->streams[3];
+    cudaEvent_t *ev_in = h->events, *ev_scan = h->events + S, *ev_out = h->events + 2 * S;
     char *ws = static_cast<char *>(h->d_ws);
-    uint64_t *d_stats = reinterpret_cast<uint64_t *>(ws + 2 * slot);
-    CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16, h->streams[0]));
-    cudaEvent_t ev_stats;
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_stats, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(ev_stats, h->streams[0]));
-    CUDA_TRY(cudaStreamWaitEvent(h->streams[1], ev_stats, 0));
+    uint64_t *d_stats = reinterpret_cast<uint64_t *>(ws + S * slot);
+    if (h_stats) {
+        CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16, s_in));
+        CUDA_TRY(cudaEventRecord(ev_in[0], s_in));  // ordered before every compute stream below
+    }
+    const int64_t nchunks = (n + chunk - 1) / chunk;
     int rc = PFW_OK;
-    for (int64_t c0 = 0, k = 0; c0 < n && rc == PFW_OK; c0 += chunk, k++) {
+    for (int64_t k = 0; k < nchunks && rc == PFW_OK; k++) {
+        const int64_t c0 = k * chunk;
         const int64_t m = (n - c0 < chunk) ? n - c0 : chunk;
-        cudaStream_t st = h->streams[k & 1];
-        char *base = ws + (k & 1) * slot;
+        const int sl = (int)(k % S);
+        cudaStream_t s_comp = h->streams[1 + (k & 1)];
+        char *base = ws + sl * slot;
         uint4 *dp = reinterpret_cast<uint4 *>(base);
         uint32_t *df = reinterpret_cast<uint32_t *>(base + (size_t)chunk * 16);
         uint8_t *dv = reinterpret_cast<uint8_t *>(base + (size_t)chunk * 20);
+        if (k >= S) CUDA_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
         CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
-                                 cudaMemcpyHostToDevice, st));
+                                 cudaMemcpyHostToDevice, s_in));
+        CUDA_TRY(cudaEventRecord(ev_in[sl], s_in));
+        CUDA_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
+        if (k >= S) CUDA_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
         rc = launch_scan(h, MODE_WRITE, 0, h->n, dp, m, df, nullptr, h_verdict ? dv : nullptr,
-                         h_stats ? d_stats : nullptr, st, &h->ws_e2e[k & 1]);
+                         h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1]);
         if (rc != PFW_OK) break;
-        CUDA_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, st));
-        if (h_verdict)
-            CUDA_TRY(cudaMemcpyAsync(h_verdict + c0, dv, m, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaEventRecord(ev_scan[sl], s_comp));
+        CUDA_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
+        CUDA_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, s_out));
+        if (h_verdict) CUDA_TRY(cudaMemcpyAsync(h_verdict + c0, dv, m, cudaMemcpyDeviceToHost, s_out));
+        CUDA_TRY(cudaEventRecord(ev_out[sl], s_out));
     }
-    CUDA_TRY(cudaStreamSynchronize(h->streams[0]));
-    CUDA_TRY(cudaStreamSynchronize(h->streams[1]));
-    cudaEventDestroy(ev_stats);
+    for (auto &st : h->streams) CUDA_TRY(cudaStreamSynchronize(st));
     if (rc != PFW_OK) return rc;
     if (h_stats) CUDA_TRY(cudaMemcpy(h_stats, d_stats, 16, cudaMemcpyDeviceToHost));
     return PFW_OK;
