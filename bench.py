@@ -192,6 +192,8 @@ def main() -> int:
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one step (all pass launches) in a CUDA graph and replay it")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 22, help="packets per H2D/scan/D2H chunk")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
@@ -290,6 +292,26 @@ def main() -> int:
         flush.fill_(1)
         step()
     barrier()
+    run_step = step
+    graph_launches = 0  # kernels per replay (replays bypass the library's launch counter)
+    if args.graph and fused is None and world == 1:
+        # the library launches on the caller's stream, so stream capture
+        # records every pass of the multi-pass scan into one graph
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            stream_saved = stream
+            stream = cap
+            before = _native.launch_count()
+            with torch.cuda.graph(g, stream=cap):
+                step()
+            graph_launches = _native.launch_count() - before
+            stream = stream_saved
+        torch.cuda.synchronize()
+        run_step = g.replay
+        run_step()
+        torch.cuda.synchronize()
     # algorithmic work of one step: sum of this rank's (per-task) comparisons
     local_comps = int(stats[0].item())
 
@@ -301,12 +323,12 @@ def main() -> int:
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            step()
+            run_step()
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
         barrier()
-    launches = _native.launch_count() - launches0
+    launches = _native.launch_count() - launches0 + graph_launches * args.steps
     total_ms = sum(times)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     tot = torch.tensor([float(n if w.model != "function" else 0), float(local_comps)],
