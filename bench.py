@@ -198,6 +198,9 @@ def main() -> int:
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--first-pass", type=int, default=-1, help="rules in the first pass (0 = single pass)")
+    ap.add_argument("--proto-split", action="store_true",
+                    help="scan protocol-split rule chains (opt-in algorithmic extension; the "
+                         "roofline then over-counts: it charges the reference's comparisons)")
     ap.add_argument("--fused", action="store_true",
                     help="function config: combine fused into the scan epilogue (NVLink atomics via "
                          "CUDA IPC, reduce-scatter result) instead of the NCCL all-reduce")
@@ -238,6 +241,8 @@ def main() -> int:
         _native.set_tuning("tile", args.tile)
     if args.first_pass >= 0:
         _native.set_tuning("first_pass", args.first_pass)
+    if args.proto_split:
+        _native.set_tuning("proto_split", 1)
     peaks = load_peaks()
     dev = torch.device(f"cuda:{local}")
     info = parallel.RankInfo(rank, world)
@@ -410,6 +415,7 @@ def main() -> int:
                                       + (" (fused NVLink-atomic combine)" if fused is not None else
                                          " (NCCL MIN all-reduce)" if w.model == "function" else ""),
                        "l2": "flushed between timed steps (256 MiB write)",
+                       "rule_layout": "protocol-split chains" if args.proto_split else "single ordered table",
                        "kernel": _native.version()},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -36,6 +36,7 @@
 #include <string>
 #include <vector>
 #include <atomic>
+#include <algorithm>
 
 #include "../../include/pfw.h"
 
@@ -106,6 +107,8 @@ int g_first_pass = 1024; // rules in the first pass (0 = single pass); passes do
 constexpr int MAX_PASSES = 32;
 constexpr int MAX_PEERS = 64;
 constexpr int E2E_SLOTS = 3;
+constexpr int MAX_CHAINS = 257;
+int g_proto_split = 0;   // opt-in: scan protocol-split rule chains
 
 }  // namespace
 
@@ -131,6 +134,21 @@ struct pfw_ruleset {
     ScanWs ws;         // default (calls on the caller's stream)
     uint32_t **d_peers = nullptr;  // 2 * MAX_PEERS device pointer table (fused combine)
     ScanWs ws_e2e[2];  // pfw_classify_host slots
+    // Protocol-split rule chains (opt-in, tuning "proto_split"): chain c holds,
+    // in rule order, the rules a packet of protocol proto_of[c] can match
+    // (proto == that value or ANY); the last chain holds only the ANY rules
+    // (packets whose protocol no rule names).  lut[p] = chain of protocol p.
+    struct Chain {
+        int64_t n = 0, rpad = 0;
+        uint32_t *d_rules = nullptr;  // NF * rpad, same encoding as d_rules
+        uint32_t *d_orig = nullptr;   // chain position -> original rule index
+        std::vector<uint32_t> orig;
+    };
+    std::vector<Chain> chains;
+    uint8_t *d_lut = nullptr;          // 256 entries
+    uint32_t *d_bucket = nullptr;      // packet ids grouped by chain (n)
+    unsigned *d_bcount = nullptr;      // [3 * MAX_CHAINS]: count, base, cursor
+    int64_t bucket_cap = 0;
 };
 
 namespace {
@@ -142,12 +160,17 @@ struct ScanParams {
     const uint32_t *rules;
     const uint8_t *accept;
     int64_t rpad;
-    int64_t lo, hi;            // rule window [lo, hi): masking + comparison counts
+    int64_t lo, hi;            // rule window [lo, hi) in table positions (masking, stages)
+    int64_t win_lo, win_hi;    // the same window in original rule indices (comparisons)
+    const uint32_t *orig;      // table position -> original rule index (null = identity)
     int64_t s_begin, s_end;    // this pass: stage starts s_begin, s_begin+STAGE, ... < s_end
     const uint4 *pkts;
     int64_t n;                 // packets in the batch (pass 0 count when in_ids == null)
     const uint32_t *in_ids;    // live packet ids of this pass (null = 0..n-1)
     const unsigned int *in_count;  // device count of in_ids (null = n)
+    const unsigned int *bucket_base;  // pass 0 of a chain scan: in_ids offset (device)
+    const uint32_t *in_ids0;          // pass-0 input of a launch (null = identity)
+    const unsigned int *in_count0;
     uint32_t *out_ids;         // survivors of this pass (null = final pass)
     unsigned int *out_count;
     uint32_t *first;
@@ -318,6 +341,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     constexpr int STAGE = 32 * KS;
     const bool final_pass = p.out_ids == nullptr;
     const int64_t count = p.in_count ? (int64_t)*p.in_count : p.n;
+    const uint32_t *in_ids = p.in_ids ? p.in_ids + (p.bucket_base ? *p.bucket_base : 0u) : nullptr;
     // Tile size for this pass: the full capacity when there is enough work,
     // otherwise small enough to give every CTA ~2 tiles (late passes carry
     // few survivors; a handful of huge tiles would idle most SMs).  Every
@@ -359,7 +383,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
         for (int i = tid; i < cnt; i += BLOCK) {
             // per-packet precompute, amortised over every stage of the pass:
             // the fp32 port/proto words (exact integers < 2^24)
-            const uint32_t id = p.in_ids ? __ldg(p.in_ids + base + i) : (uint32_t)(base + i);
+            const uint32_t id = in_ids ? __ldg(in_ids + base + i) : (uint32_t)(base + i);
             const uint4 v = __ldg(p.pkts + id);
             const uint32_t sp = v.z >> 16, dp = v.z & 0xFFFFu, pr = v.w & 0xFFu;
             s_pk[i] = make_uint4(v.x, v.y, __float_as_uint((float)((pr << 16) | sp)),
@@ -483,17 +507,18 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
 
         // epilogue: resolve matched packets (and, in the final pass, the
         // unmatched ones); survivors of a non-final pass go to the next pass
-        const uint32_t span = (uint32_t)(p.hi > p.lo ? p.hi - p.lo : 0);
+        const uint32_t span = (uint32_t)(p.win_hi > p.win_lo ? p.win_hi - p.win_lo : 0);
         for (int i0 = 0; i0 < cnt; i0 += BLOCK) {
             const int i = i0 + tid;
             bool survive = false;
             uint32_t id = 0;
             if (i < cnt) {
-                const uint32_t f = s_first[i];
+                uint32_t f = s_first[i];
                 id = s_id[i];
                 survive = !final_pass && f == PFW_NO_MATCH;
                 if (!survive) {
-                    const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.lo + 1) : span;
+                    if (p.orig && f != PFW_NO_MATCH) f = __ldg(p.orig + f);
+                    const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.win_lo + 1) : span;
                     if (MODE == MODE_ACC) {
                         if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
                         p.comps[id] += c;
@@ -545,6 +570,66 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
             if (st_sum) atomicAdd(&p.stats[0], st_sum);
             if (st_max) atomicMax(&p.stats[1], (unsigned long long)st_max);
         }
+    }
+}
+
+// ---------------------------------------------------- protocol bucketing
+// Packets grouped by rule chain (protocol): per-block shared-memory histograms
+// and one global atomic per chain per block, so single-protocol traffic does
+// not serialise on one counter.  counts/base/cursor live in bc[0..3*MAX_CHAINS).
+constexpr int BK_BLOCK = 256, BK_PER_THREAD = 16;
+
+__global__ void __launch_bounds__(BK_BLOCK) bucket_count_kernel(const uint4 *pkts, int64_t n,
+                                                                const uint8_t *lut, int nchains,
+                                                                unsigned *bc) {
+    __shared__ unsigned hist[MAX_CHAINS];
+    for (int c = threadIdx.x; c < nchains; c += BK_BLOCK) hist[c] = 0;
+    __syncthreads();
+    const int64_t b0 = (int64_t)blockIdx.x * BK_BLOCK * BK_PER_THREAD;
+    for (int k = 0; k < BK_PER_THREAD; k++) {
+        const int64_t i = b0 + (int64_t)k * BK_BLOCK + threadIdx.x;
+        if (i < n) atomicAdd(&hist[lut[__ldg(&pkts[i].w) & 0xFFu]], 1u);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nchains; c += BK_BLOCK)
+        if (hist[c]) atomicAdd(&bc[c], hist[c]);
+}
+
+__global__ void bucket_prefix_kernel(int nchains, unsigned *bc) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned acc = 0;
+        for (int c = 0; c < nchains; c++) {
+            bc[MAX_CHAINS + c] = acc;  // base
+            bc[2 * MAX_CHAINS + c] = 0;  // cursor
+            acc += bc[c];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(BK_BLOCK) bucket_scatter_kernel(const uint4 *pkts, int64_t n,
+                                                                  const uint8_t *lut, int nchains,
+                                                                  unsigned *bc, uint32_t *ids) {
+    __shared__ unsigned hist[MAX_CHAINS], gbase[MAX_CHAINS];
+    for (int c = threadIdx.x; c < nchains; c += BK_BLOCK) hist[c] = 0;
+    __syncthreads();
+    const int64_t b0 = (int64_t)blockIdx.x * BK_BLOCK * BK_PER_THREAD;
+    uint8_t ch[BK_PER_THREAD];
+#pragma unroll
+    for (int k = 0; k < BK_PER_THREAD; k++) {
+        const int64_t i = b0 + (int64_t)k * BK_BLOCK + threadIdx.x;
+        ch[k] = i < n ? lut[__ldg(&pkts[i].w) & 0xFFu] : 0;
+        if (i < n) atomicAdd(&hist[ch[k]], 1u);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nchains; c += BK_BLOCK) {
+        gbase[c] = hist[c] ? bc[MAX_CHAINS + c] + atomicAdd(&bc[2 * MAX_CHAINS + c], hist[c]) : 0;
+        hist[c] = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK_PER_THREAD; k++) {
+        const int64_t i = b0 + (int64_t)k * BK_BLOCK + threadIdx.x;
+        if (i < n) ids[gbase[ch[k]] + atomicAdd(&hist[ch[k]], 1u)] = (uint32_t)i;
     }
 }
 
@@ -695,11 +780,6 @@ uint64_t host_randbelow(uint64_t &x, uint64_t n) {
     }
 }
 
-bool stage_fits(int T, int KS, int dev) {
-    int maxsm = 0;
-    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return smem_bytes(T, KS) <= (size_t)maxsm;
-}
 
 int ensure_ws(ScanWs &ws, int64_t n) {
     if (!ws.ctr) CUDA_TRY(cudaMalloc(&ws.ctr, 2 * MAX_PASSES * sizeof(unsigned int)));
@@ -778,8 +858,9 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
         p.s_begin = b[k];
         p.s_end = b[k + 1];
         p.tile_counter = ws.ctr + 2 * k;
-        p.in_ids = k == 0 ? nullptr : ws.ids + (size_t)((k - 1) & 1) * ws.cap;
-        p.in_count = k == 0 ? nullptr : ws.ctr + 2 * (k - 1) + 1;
+        p.in_ids = k == 0 ? p0.in_ids0 : ws.ids + (size_t)((k - 1) & 1) * ws.cap;
+        p.in_count = k == 0 ? p0.in_count0 : ws.ctr + 2 * (k - 1) + 1;
+        p.bucket_base = k == 0 ? p0.bucket_base : nullptr;
         const bool last = k == npass - 1;
         p.out_ids = last ? nullptr : ws.ids + (size_t)(k & 1) * ws.cap;
         p.out_count = last ? nullptr : ws.ctr + 2 * k + 1;
@@ -799,6 +880,9 @@ int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t
         default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4 or 8)", g_ks);
     }
 }
+
+int launch_mode(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st);
+int launch_split(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st);
 
 int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                 uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
@@ -821,6 +905,9 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
     p.rpad = h->rpad;
     p.lo = lo;
     p.hi = hi;
+    p.win_lo = lo;
+    p.win_hi = hi;
+    p.orig = nullptr;
     p.pkts = reinterpret_cast<const uint4 *>(d_pkts);
     p.n = n;
     p.first = first;
@@ -838,6 +925,11 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
         p.scatter = peer->scatter;
     }
     ScanWs &w = ws ? *ws : h->ws;
+    if (g_proto_split && !h->chains.empty() && lo < hi) return launch_split(h, mode, p, w, st);
+    return launch_mode(h, mode, p, w, st);
+}
+
+int launch_mode(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st) {
     switch (mode) {
         case MODE_ACC:
             return g_force_imad ? launch_scan_ks<MODE_ACC, true>(h, p, w, st) : launch_scan_ks<MODE_ACC, false>(h, p, w, st);
@@ -846,6 +938,52 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
         default:
             return g_force_imad ? launch_scan_ks<MODE_WRITE, true>(h, p, w, st) : launch_scan_ks<MODE_WRITE, false>(h, p, w, st);
     }
+}
+
+// Protocol-split scan: group the packets by rule chain on the device, then
+// run the multi-pass scan of each chain over its bucket (empty buckets exit
+// immediately; counts stay on the device, no host sync).
+int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cudaStream_t st) {
+    const int nch = (int)h->chains.size();
+    const int64_t n = p0.n;
+    if (h->bucket_cap < n) {
+        if (h->d_bucket) cudaFree(h->d_bucket);
+        h->d_bucket = nullptr;
+        h->bucket_cap = 0;
+        CUDA_TRY(cudaMalloc(&h->d_bucket, (size_t)n * sizeof(uint32_t)));
+        h->bucket_cap = n;
+    }
+    if (!h->d_bcount) CUDA_TRY(cudaMalloc(&h->d_bcount, 3 * MAX_CHAINS * sizeof(unsigned)));
+    CUDA_TRY(cudaMemsetAsync(h->d_bcount, 0, MAX_CHAINS * sizeof(unsigned), st));
+    const unsigned nb = (unsigned)((n + BK_BLOCK * BK_PER_THREAD - 1) / (BK_BLOCK * BK_PER_THREAD));
+    bucket_count_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, n, h->d_lut, nch, h->d_bcount);
+    bucket_prefix_kernel<<<1, 32, 0, st>>>(nch, h->d_bcount);
+    bucket_scatter_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, n, h->d_lut, nch, h->d_bcount, h->d_bucket);
+    CUDA_TRY(cudaGetLastError());
+    g_launches += 3;
+    // bucket c's ids start at base[c]; its count is bc[c].  The base is only
+    // known on the device, so each chain scan reads its ids through a
+    // device-side pointer computed by a tiny kernel into the ws pointer slot.
+    for (int c = 0; c < nch; c++) {
+        const pfw_ruleset::Chain &ch = h->chains[(size_t)c];
+        ScanParams p = p0;
+        p.rules = ch.d_rules;
+        p.rpad = ch.rpad;
+        p.orig = ch.d_orig;
+        p.win_lo = p0.lo;
+        p.win_hi = p0.hi;
+        p.lo = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.lo) - ch.orig.begin());
+        p.hi = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.hi) - ch.orig.begin());
+        p.bucket_base = h->d_bcount + MAX_CHAINS + c;
+        p.in_ids0 = h->d_bucket;
+        p.in_count0 = h->d_bcount + c;
+        if (p.lo >= p.hi) {
+            p.lo = p.hi;
+        }
+        int rc = launch_mode(h, mode, p, w, st);
+        if (rc != PFW_OK) return rc;
+    }
+    return PFW_OK;
 }
 
 int grid_for(int64_t n) {
@@ -896,6 +1034,8 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "first_pass")) {
         if (value < 0 || value > (1 << 24)) return set_err(PFW_ERR_INVALID, "first_pass in [0, 2^24]");
         g_first_pass = (int)value;
+    } else if (!strcmp(key, "proto_split")) {
+        g_proto_split = value != 0;
     } else if (!strcmp(key, "force_imad")) {
         g_force_imad = value != 0;
     } else {
@@ -972,6 +1112,41 @@ int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32
     if (e == cudaSuccess) e = cudaMemcpy(h->d_rules, host.data(), host.size() * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_accept, acc.data(), acc.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess && n > 0) {
+        // protocol-split chains: one per concrete protocol named by a rule,
+        // plus the ANY-only chain for every other protocol
+        bool named[256] = {};
+        for (int64_t r = 0; r < n; r++) named[proto[r]] = true;
+        std::vector<int> protos;
+        for (int v = 1; v < 256; v++)
+            if (named[v]) protos.push_back(v);
+        uint8_t lut[256];
+        const int any_chain = (int)protos.size();
+        for (int v = 0; v < 256; v++) lut[v] = (uint8_t)any_chain;
+        for (size_t c = 0; c < protos.size(); c++) lut[protos[c]] = (uint8_t)c;
+        h->chains.resize(protos.size() + 1);
+        for (size_t c = 0; c <= protos.size() && e == cudaSuccess; c++) {
+            pfw_ruleset::Chain &ch = h->chains[c];
+            const int v = c < protos.size() ? protos[c] : -1;
+            for (int64_t r = 0; r < n; r++)
+                if (proto[r] == 0 || (int)proto[r] == v) ch.orig.push_back((uint32_t)r);
+            ch.n = (int64_t)ch.orig.size();
+            ch.rpad = ((ch.n + 31) / 32) * 32 + 8 * 32;
+            std::vector<uint32_t> tab((size_t)NF * ch.rpad);
+            std::vector<uint32_t> orig_pad((size_t)ch.rpad, 0);
+            for (int64_t k = 0; k < ch.rpad; k++) {
+                const int64_t r = k < ch.n ? (int64_t)ch.orig[(size_t)k] : n;  // n..: never-match pad row
+                for (int f = 0; f < NF; f++) tab[(size_t)f * ch.rpad + k] = host[(size_t)f * h->rpad + r];
+                orig_pad[(size_t)k] = k < ch.n ? ch.orig[(size_t)k] : 0u;
+            }
+            e = cudaMalloc(&ch.d_rules, tab.size() * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&ch.d_orig, orig_pad.size() * 4);
+            if (e == cudaSuccess) e = cudaMemcpy(ch.d_rules, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess) e = cudaMemcpy(ch.d_orig, orig_pad.data(), orig_pad.size() * 4, cudaMemcpyHostToDevice);
+        }
+        if (e == cudaSuccess) e = cudaMalloc(&h->d_lut, 256);
+        if (e == cudaSuccess) e = cudaMemcpy(h->d_lut, lut, 256, cudaMemcpyHostToDevice);
+    }
     if (e != cudaSuccess) {
         const int code = e == cudaErrorMemoryAllocation ? PFW_ERR_NOMEM : PFW_ERR_CUDA;
         pfw_ruleset_destroy(h);
@@ -989,6 +1164,13 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     if (h->d_ws) cudaFree(h->d_ws);
     free_ws(h->ws);
     if (h->d_peers) cudaFree(h->d_peers);
+    for (auto &ch : h->chains) {
+        if (ch.d_rules) cudaFree(ch.d_rules);
+        if (ch.d_orig) cudaFree(ch.d_orig);
+    }
+    if (h->d_lut) cudaFree(h->d_lut);
+    if (h->d_bucket) cudaFree(h->d_bucket);
+    if (h->d_bcount) cudaFree(h->d_bcount);
     free_ws(h->ws_e2e[0]);
     free_ws(h->ws_e2e[1]);
     for (auto &st : h->streams)

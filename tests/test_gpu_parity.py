@@ -36,7 +36,8 @@ def compiled(rules: dict) -> pfw.CompiledRuleset:
 @pytest.fixture(autouse=True)
 def _reset_tuning():
     yield
-    for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024)):
+    for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
+                 ("proto_split", 0)):
         _native.set_tuning(k, v)
 
 
@@ -413,3 +414,33 @@ def test_fused_function_parallel_single_rank_class():
     np.testing.assert_array_equal(first_to_host(first), g["function_1_first"])
     np.testing.assert_array_equal(comps.cpu().numpy(), g["function_1_comps"])
     fused.close()
+
+
+# ------------------------------------------------------ protocol-split chains
+
+@pytest.mark.parametrize("name,rn,tn", SCANS)
+def test_proto_split_scan_matches_reference_golden(name, rn, tn):
+    _native.set_tuning("proto_split", 1)
+    test_scan_matches_reference_golden(name, rn, tn)
+
+
+def test_proto_split_windows_engines_and_mixed_protocols():
+    _native.set_tuning("proto_split", 1)
+    test_scan_windows()
+    test_windows_every_alignment_vs_oracle()
+    for model in ("data", "function", "hybrid"):
+        test_engine_models_match_reference_golden(model)
+    test_function_parallel_100k_rules()
+    test_unnormalised_and_inverted_rules_never_match()
+    test_fused_min_combine_virtual_ranks(1)
+    # mixed-protocol traffic (TCP / UDP / ICMP / an unnamed protocol) against
+    # a ruleset with every protocol class
+    rules = oracle.gen_ruleset(3000, 17, wp=0.3)
+    rules["proto"][::97] = 47  # a protocol only a few rules name
+    parts = [oracle.gen_traffic_uniform(5000, 20 + k, proto=pr) for k, pr in enumerate((6, 17, 1, 47, 99))]
+    pk = {f: np.concatenate([pt[f] for pt in parts]) for f in PKT_FIELDS}
+    perm = np.random.default_rng(0).permutation(len(pk["proto"]))
+    pk = {f: v[perm] for f, v in pk.items()}
+    c = compiled(rules)
+    for lo, hi in ((0, 3000), (5, 2900), (1000, 1001)):
+        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
