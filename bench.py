@@ -410,7 +410,7 @@ def main() -> int:
             "data": "synthetic: generate_ruleset(RulesetGenParams(R, seed=1)) x generate_traffic("
                     "TrafficProfile(N, seed=2)), generated on the GPU bit-exactly",
             "config": {"workload": w.description, "rules": R, "packets": w.packets,
-                       "packets_per_gpu": n, "model": w.model,
+                       "packets_per_gpu": n, "execution_model": w.model,
                        "parallelism": f"{'rule' if w.model == 'function' else 'packet'}-sharded x{world}"
                                       + (" (fused NVLink-atomic combine)" if fused is not None else
                                          " (NCCL MIN all-reduce)" if w.model == "function" else ""),
