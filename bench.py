@@ -189,6 +189,10 @@ def main() -> int:
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="data", choices=("data", "grid", "function", "adversarial", "oracle"))
     ap.add_argument("--packets", type=int, default=0, help="override the workload's packet count")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="packet-sharded configs: weak = every rank scans its own full-size shard of "
+                         "an N-times larger global stream (default); strong = the workload's packets "
+                         "split over the ranks")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -251,13 +255,18 @@ def main() -> int:
     cols = workloads.rule_columns(w)
     compiled = CompiledRuleset.from_columns(cols, device=local)
     R = compiled.num_rules
+    weak = args.scaling == "weak" and w.model != "function"
+    total_packets = w.packets * world if weak else w.packets
     if w.model == "function":
         p_lo, p_hi = 0, w.packets                       # packets replicated
         r_lo, r_hi = parallel.rule_shard(R, info)       # rules sharded
     else:
-        p_lo, p_hi = parallel.packet_shard(w.packets, info)  # packets sharded
+        # packets sharded: contiguous partition_bounds shards of the global stream
+        p_lo, p_hi = parallel.packet_shard(total_packets, info)
         r_lo, r_hi = 0, R
-    pkts = workloads.packets(w, p_lo, p_hi - p_lo, local)
+    # the generator draws from the global stream of total_packets packets
+    wgen = workloads.Workload(w.name, w.rules, total_packets, w.model, w.description)
+    pkts = workloads.packets(wgen, p_lo, p_hi - p_lo, local)
     n = len(pkts)
     first = torch.empty(n, dtype=torch.int32, device=dev)
     comps = torch.empty(n, dtype=torch.int32, device=dev)
@@ -406,10 +415,11 @@ def main() -> int:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "Mpps", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
+            "dtype": "u32",
             "data": "synthetic: generate_ruleset(RulesetGenParams(R, seed=1)) x generate_traffic("
                     "TrafficProfile(N, seed=2)), generated on the GPU bit-exactly",
-            "config": {"workload": w.description, "rules": R, "packets": w.packets,
+            "config": {"workload": w.description, "rules": R, "packets": total_packets,
                        "packets_per_gpu": n, "execution_model": w.model,
                        "parallelism": f"{'rule' if w.model == 'function' else 'packet'}-sharded x{world}"
                                       + (" (fused NVLink-atomic combine)" if fused is not None else

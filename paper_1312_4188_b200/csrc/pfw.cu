@@ -876,8 +876,9 @@ int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t
     switch (g_ks) {
         case 2: return launch_scan_t<2, MODE, FMA>(h, p, ws, st);
         case 4: return launch_scan_t<4, MODE, FMA>(h, p, ws, st);
+        case 6: return launch_scan_t<6, MODE, FMA>(h, p, ws, st);
         case 8: return launch_scan_t<8, MODE, FMA>(h, p, ws, st);
-        default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4 or 8)", g_ks);
+        default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4, 6 or 8)", g_ks);
     }
 }
 
@@ -1023,7 +1024,8 @@ static uint32_t f2u(float f) {
 int pfw_set_tuning(const char *key, int64_t value) {
     if (!key) return set_err(PFW_ERR_INVALID, "null key");
     if (!strcmp(key, "ks")) {
-        if (value != 2 && value != 4 && value != 8) return set_err(PFW_ERR_INVALID, "ks must be 2, 4 or 8");
+        if (value != 2 && value != 4 && value != 6 && value != 8)
+            return set_err(PFW_ERR_INVALID, "ks must be 2, 4, 6 or 8");
         g_ks = (int)value;
     } else if (!strcmp(key, "tile")) {
         if (value < 256 || value > 8192 || value % 256) return set_err(PFW_ERR_INVALID, "tile must be a multiple of 256 in [256, 8192]");
