@@ -200,6 +200,7 @@ def main() -> int:
                     help="capture one step (all pass launches) in a CUDA graph and replay it")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 22, help="packets per H2D/scan/D2H chunk")
     ap.add_argument("--ks", type=int, default=0)
+    ap.add_argument("--sc", type=int, default=-1, help="warp-level short-circuit of the port tests (0/1)")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--first-pass", type=int, default=-1, help="rules in the first pass (0 = single pass)")
     ap.add_argument("--proto-split", action="store_true",
@@ -241,6 +242,8 @@ def main() -> int:
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     if args.ks:
         _native.set_tuning("ks", args.ks)
+    if args.sc >= 0:
+        _native.set_tuning("short_circuit", args.sc)
     if args.tile:
         _native.set_tuning("tile", args.tile)
     if args.first_pass >= 0:

@@ -109,6 +109,7 @@ constexpr int MAX_PEERS = 64;
 constexpr int E2E_SLOTS = 3;
 constexpr int MAX_CHAINS = 257;
 int g_proto_split = 0;   // opt-in: scan protocol-split rule chains
+int g_short_circuit = 0; // warp-level short-circuit of the port tests (SC variant; measured slower)
 
 }  // namespace
 
@@ -216,6 +217,40 @@ __device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src,
            (__float_as_uint(dB) <= r[F_B_W]);
 }
 
+// The two halves of the fast-path test, for warp-level short-circuit
+// evaluation (SC): the IP prefix tests first (they pass for ~1% of random
+// rule/packet pairs), the port/protocol tests only for rows where some lane
+// passed them -- model.py:224-230 evaluates the conjunction lazily too.
+template <bool FMA>
+__device__ __forceinline__ bool ip_test(const uint32_t (&r)[NF], uint32_t src, uint32_t dst, uint32_t one) {
+    uint32_t a, b;
+    if (FMA) {
+        a = sub_fma(src, one, r[F_SRC_NLO]);
+        b = sub_fma(dst, one, r[F_DST_NLO]);
+    } else {
+        a = src + r[F_SRC_NLO];
+        b = dst + r[F_DST_NLO];
+    }
+    return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]);
+}
+
+// warp-uniform "any" without the compiler's divergence check (the scan loop
+// is warp-uniform by construction: every lane runs every iteration)
+__device__ __forceinline__ bool warp_any(bool x) {
+    uint32_t r;
+    asm volatile(
+        "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nvote.sync.any.pred q, p, 0xffffffff;\nselp.u32 %0, 1, 0, q;\n}\n"
+        : "=r"(r) : "r"((uint32_t)x));
+    return r != 0;
+}
+
+__device__ __forceinline__ bool port_test(const uint32_t (&r)[NF], float A, float A2, float B) {
+    const float x = fmaf(A2, __uint_as_float(r[F_A_C2]), __uint_as_float(r[F_A_NLO]));
+    const float dA = fmaf(A, __uint_as_float(r[F_A_C1]), x);
+    const float dB = B + __uint_as_float(r[F_B_NLO]);
+    return (__float_as_uint(dA) <= r[F_A_W]) & (__float_as_uint(dB) <= r[F_B_W]);
+}
+
 // Slow-path re-evaluation (once per packet, after a stage hit).  Written with a
 // different instruction sequence so the compiler cannot CSE it with the fast
 // path and keep KS predicates / values alive across the vote.  Exact for the
@@ -321,7 +356,7 @@ __device__ __forceinline__ void issue_stage(const ScanParams &p, int64_t s, uint
     for (int f = 0; f < NF; f++) tma_bulk_g2s(buf + f * 32 * KS, p.rules + f * p.rpad + s, ROW, bar);
 }
 
-template <int KS, int MODE, bool FMA>
+template <int KS, int MODE, bool FMA, bool SC>
 __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int TMAX = p.tile;  // shared-memory capacity in packets
@@ -436,15 +471,44 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 const float a0 = __uint_as_float(v0.z), c0 = __uint_as_float(v0.w);
                 const float a1 = __uint_as_float(v1.z), c1 = __uint_as_float(v1.w);
                 bool lo0 = false, hi0 = false, lo1 = false, hi1 = false;
+                if (SC) {
+                    // rows in rule order; per row: IP tests, one vote, the
+                    // port/protocol tests only if some lane passed them, and the
+                    // ballot of the full result is the exact first match (no
+                    // stage-level OR, no re-evaluation).  A resolved packet
+                    // keeps only its cheap IP tests for the rest of the stage.
+                    bool done0 = false, done1 = false;
 #pragma unroll
-                for (int j = 0; j < KS / 2; j++) {
-                    lo0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
-                    lo1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
-                }
+                    for (int j = 0; j < KS; j++) {
+                        const bool i0 = ip_test<FMA>(r[j], v0.x, v0.y, one) & !done0;
+                        const bool i1 = ip_test<FMA>(r[j], v1.x, v1.y, one) & !done1;
+                        if (__any_sync(0xFFFFFFFFu, i0)) {
+                            const unsigned bm = __ballot_sync(0xFFFFFFFFu, i0 & port_test(r[j], a0, c0, b0));
+                            if (bm) {
+                                if (lane == 0) s_first[q0] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
+                                done0 = true;
+                            }
+                        }
+                        if (__any_sync(0xFFFFFFFFu, i1)) {
+                            const unsigned bm = __ballot_sync(0xFFFFFFFFu, i1 & port_test(r[j], a1, c1, b1));
+                            if (bm) {
+                                if (lane == 0) s_first[q1] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
+                                done1 = true;
+                            }
+                        }
+                    }
+                    continue;
+                } else {
 #pragma unroll
-                for (int j = KS / 2; j < KS; j++) {
-                    hi0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
-                    hi1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
+                    for (int j = 0; j < KS / 2; j++) {
+                        lo0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
+                        lo1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
+                    }
+#pragma unroll
+                    for (int j = KS / 2; j < KS; j++) {
+                        hi0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
+                        hi1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
+                    }
                 }
                 if (__any_sync(0xFFFFFFFFu, lo0 | hi0)) {
                     const unsigned k = stage_first<KS, FMA>(r, lo0, v0.x, v0.y, a0, c0, b0, one);
@@ -455,7 +519,23 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                     if (lane == 0) s_first[q1] = (uint32_t)(s + k);
                 }
             }
-            if (i < nlive) {
+            if (SC && i < nlive) {
+                const int q = live[i];
+                const uint4 v = s_pk[q];
+                const float bb = __uint_as_float(s_pr[q]);
+                const float a = __uint_as_float(v.z), c = __uint_as_float(v.w);
+#pragma unroll
+                for (int j = 0; j < KS; j++) {
+                    const bool ip = ip_test<FMA>(r[j], v.x, v.y, one);
+                    if (__any_sync(0xFFFFFFFFu, ip)) {
+                        const unsigned bm = __ballot_sync(0xFFFFFFFFu, ip & port_test(r[j], a, c, bb));
+                        if (bm) {
+                            if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
+                            break;
+                        }
+                    }
+                }
+            } else if (i < nlive) {
                 const int q = live[i];
                 const uint4 v = s_pk[q];
                 const float bb = __uint_as_float(s_pr[q]);
@@ -824,10 +904,10 @@ std::vector<int64_t> plan_passes(int64_t lo, int64_t hi, int stage) {
     return b;
 }
 
-template <int KS, int MODE, bool FMA>
+template <int KS, int MODE, bool FMA, bool SC>
 int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t st) {
     const size_t sm = smem_bytes(p0.tile, KS);
-    auto kern = scan_kernel<KS, MODE, FMA>;
+    auto kern = scan_kernel<KS, MODE, FMA, SC>;
     int maxsm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     if (sm > (size_t)maxsm)
@@ -871,15 +951,27 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
     return PFW_OK;
 }
 
-template <int MODE, bool FMA>
+template <int MODE, bool FMA, bool SC>
 int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t st) {
     switch (g_ks) {
-        case 2: return launch_scan_t<2, MODE, FMA>(h, p, ws, st);
-        case 4: return launch_scan_t<4, MODE, FMA>(h, p, ws, st);
-        case 6: return launch_scan_t<6, MODE, FMA>(h, p, ws, st);
-        case 8: return launch_scan_t<8, MODE, FMA>(h, p, ws, st);
+        case 2: return launch_scan_t<2, MODE, FMA, SC>(h, p, ws, st);
+        case 4: return launch_scan_t<4, MODE, FMA, SC>(h, p, ws, st);
+        case 6: return launch_scan_t<6, MODE, FMA, SC>(h, p, ws, st);
+        case 8: return launch_scan_t<8, MODE, FMA, SC>(h, p, ws, st);
         default: return set_err(PFW_ERR_INVALID, "unsupported ks=%d (2, 4, 6 or 8)", g_ks);
     }
+}
+
+template <int MODE, bool SC>
+int launch_scan_fma(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t st) {
+    return g_force_imad ? launch_scan_ks<MODE, true, SC>(h, p, ws, st)
+                        : launch_scan_ks<MODE, false, SC>(h, p, ws, st);
+}
+
+template <int MODE>
+int launch_scan_sc(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t st) {
+    return g_short_circuit ? launch_scan_fma<MODE, true>(h, p, ws, st)
+                           : launch_scan_fma<MODE, false>(h, p, ws, st);
 }
 
 int launch_mode(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st);
@@ -932,12 +1024,9 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
 
 int launch_mode(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st) {
     switch (mode) {
-        case MODE_ACC:
-            return g_force_imad ? launch_scan_ks<MODE_ACC, true>(h, p, w, st) : launch_scan_ks<MODE_ACC, false>(h, p, w, st);
-        case MODE_PEER:
-            return g_force_imad ? launch_scan_ks<MODE_PEER, true>(h, p, w, st) : launch_scan_ks<MODE_PEER, false>(h, p, w, st);
-        default:
-            return g_force_imad ? launch_scan_ks<MODE_WRITE, true>(h, p, w, st) : launch_scan_ks<MODE_WRITE, false>(h, p, w, st);
+        case MODE_ACC: return launch_scan_sc<MODE_ACC>(h, p, w, st);
+        case MODE_PEER: return launch_scan_sc<MODE_PEER>(h, p, w, st);
+        default: return launch_scan_sc<MODE_WRITE>(h, p, w, st);
     }
 }
 
@@ -1036,6 +1125,8 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "first_pass")) {
         if (value < 0 || value > (1 << 24)) return set_err(PFW_ERR_INVALID, "first_pass in [0, 2^24]");
         g_first_pass = (int)value;
+    } else if (!strcmp(key, "short_circuit")) {
+        g_short_circuit = value != 0;
     } else if (!strcmp(key, "proto_split")) {
         g_proto_split = value != 0;
     } else if (!strcmp(key, "force_imad")) {

@@ -37,7 +37,7 @@ def compiled(rules: dict) -> pfw.CompiledRuleset:
 def _reset_tuning():
     yield
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
-                 ("proto_split", 0)):
+                 ("proto_split", 0), ("short_circuit", 0)):
         _native.set_tuning(k, v)
 
 
@@ -287,9 +287,12 @@ def test_unnormalised_and_inverted_rules_never_match():
     assert (want[:500] == 2).all() and (want[500:] == 3).all()
 
 
+@pytest.mark.parametrize("sc", [0, 1])
 @pytest.mark.parametrize("ks,tile,imad,fp", [(2, 256, 1, 64), (4, 1024, 0, 0), (8, 4096, 1, 256),
-                                             (8, 6144, 0, 1024), (4, 2048, 1, 100), (8, 2048, 1, 32)])
-def test_tuning_variants_identical(ks, tile, imad, fp):
+                                             (8, 6144, 0, 1024), (4, 2048, 1, 100), (8, 2048, 1, 32),
+                                             (6, 2048, 1, 1024)])
+def test_tuning_variants_identical(ks, tile, imad, fp, sc):
+    _native.set_tuning("short_circuit", sc)
     _native.set_tuning("ks", ks)
     _native.set_tuning("tile", tile)
     _native.set_tuning("force_imad", imad)
@@ -444,3 +447,9 @@ def test_proto_split_windows_engines_and_mixed_protocols():
     c = compiled(rules)
     for lo, hi in ((0, 3000), (5, 2900), (1000, 1001)):
         np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+
+
+@pytest.mark.parametrize("name,rn,tn", SCANS)
+def test_short_circuit_scan_matches_reference_golden(name, rn, tn):
+    _native.set_tuning("short_circuit", 1)
+    test_scan_matches_reference_golden(name, rn, tn)
