@@ -19,20 +19,21 @@ NVCC_FLAGS = [
 ]
 
 
-def build_native(verbose: bool = False, force: bool = False) -> str:
-    """Compile csrc/pfw.cu -> libpfw.so unless the library is newer than its sources."""
+def build_native(verbose: bool = False, force: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile csrc/pfw.cu -> libpfw.so unless the library is newer than its sources.
+    ``defines`` (e.g. ["PFW_GROUP=4"]) build experiment variants into ``out``."""
     deps = [SRC, os.path.join(ROOT, "include", "pfw.h"), os.path.abspath(__file__)]
-    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
-        return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, "-o", tmp, SRC, "-lcudart"]
+    if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
+        return out
+    tmp = out + ".tmp"
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, SRC, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr}")
     if verbose:
         print(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -12,7 +12,7 @@ import os
 import threading
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libpfw.so")
+LIB_PATH = os.environ.get("PFW_LIB") or os.path.join(PKG, "libpfw.so")  # PFW_LIB: experiment builds
 
 NO_MATCH = 0x7FFFFFFF  # PFW_NO_MATCH
 PFW_OK, PFW_ERR_INVALID, PFW_ERR_CUDA, PFW_ERR_NOMEM, PFW_ERR_GENERATION = range(5)

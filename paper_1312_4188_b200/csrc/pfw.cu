@@ -90,7 +90,8 @@ constexpr int NF = 10;
 //     packet A  = (proto << 16) | sport   proto-major: concrete-proto rules
 //     packet A2 = (sport << 8)  | proto   proto-minor: ANY-proto rules
 //     packet B  = (dport << 8)  | proto   proto-minor: every rule
-//     dA = A*c1 + (A2*c2 - loA) with (c1, c2) = (1, 0) concrete, (0, 1) ANY;
+//     dA = (A - A2)*c1 + (A2 - loA) with c1 = 1 concrete, 0 ANY (A - A2 is
+//     precomputed per packet; F_A_C2 = 1 - c1 stays in the table, unused);
 //     dB = B - loB; a field matches iff 0 <= d <= w, tested as
 //     float_bits(d) <=u float_bits(w) (negative d has the sign bit set).
 enum { F_SRC_NLO = 0, F_SRC_W, F_DST_NLO, F_DST_W, F_A_C1, F_A_C2, F_A_NLO, F_A_W, F_B_NLO,
@@ -210,7 +211,9 @@ __device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src,
         a = src + r[F_SRC_NLO];
         b = dst + r[F_DST_NLO];
     }
-    const float x = fmaf(A2, __uint_as_float(r[F_A_C2]), __uint_as_float(r[F_A_NLO]));
+    // A holds D = A - A2 (packet precompute): dA = D*c1 + (A2 - loA) is
+    // A - loA for c1 = 1 and A2 - loA for c1 = 0, exactly (integers < 2^24)
+    const float x = A2 + __uint_as_float(r[F_A_NLO]);
     const float dA = fmaf(A, __uint_as_float(r[F_A_C1]), x);
     const float dB = B + __uint_as_float(r[F_B_NLO]);
     return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
@@ -245,7 +248,7 @@ __device__ __forceinline__ bool warp_any(bool x) {
 }
 
 __device__ __forceinline__ bool port_test(const uint32_t (&r)[NF], float A, float A2, float B) {
-    const float x = fmaf(A2, __uint_as_float(r[F_A_C2]), __uint_as_float(r[F_A_NLO]));
+    const float x = A2 + __uint_as_float(r[F_A_NLO]);
     const float dA = fmaf(A, __uint_as_float(r[F_A_C1]), x);
     const float dB = B + __uint_as_float(r[F_B_NLO]);
     return (__float_as_uint(dA) <= r[F_A_W]) & (__float_as_uint(dB) <= r[F_B_W]);
@@ -266,9 +269,8 @@ __device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t
         a = sub_fma(src, one, r[F_SRC_NLO]);
         b = sub_fma(dst, one, r[F_DST_NLO]);
     }
-    const float dA = __fadd_rn(__fadd_rn(__fmul_rn(A, __uint_as_float(r[F_A_C1])),
-                                         __fmul_rn(A2, __uint_as_float(r[F_A_C2]))),
-                               __uint_as_float(r[F_A_NLO]));
+    const float dA = __fadd_rn(__fmul_rn(A, __uint_as_float(r[F_A_C1])),
+                               __fsub_rn(A2, -__uint_as_float(r[F_A_NLO])));
     const float dB = __fsub_rn(B, -__uint_as_float(r[F_B_NLO]));
     return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
            (__float_as_uint(dB) <= r[F_B_W]);
@@ -296,6 +298,55 @@ __device__ __forceinline__ unsigned stage_first(const uint32_t (&r)[KS][NF], boo
     return rows_first<KS, KS / 2, KS, FMA>(r, src, dst, A, A2, B, one);
 }
 
+// One warp, P live packets of the tile (warp-uniform), one stage of KS rows in
+// registers: the fast path ORs each packet's row results into two half-stage
+// accumulators; a packet whose stage hit locates its first match with the
+// slow path and records it.  P independent packets = P-fold ILP.
+template <int P, int KS, bool FMA, bool HALF>
+__device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const int (&q)[P],
+                                           const uint4 *s_pk, const uint32_t *s_pr, uint32_t *s_first,
+                                           int64_t s, uint32_t one, int lane) {
+    uint4 v[P];
+    float a[P], c[P], b[P];
+#pragma unroll
+    for (int k = 0; k < P; k++) {
+        v[k] = s_pk[q[k]];
+        b[k] = __uint_as_float(s_pr[q[k]]);
+        a[k] = __uint_as_float(v[k].z);
+        c[k] = __uint_as_float(v[k].w);
+    }
+    // HALF: two half-stage accumulators per packet (the slow path then
+    // re-checks <= KS/2 rows); with HALF off one accumulator per packet keeps
+    // the live predicates within the 7 predicate registers for larger P.
+    bool lo[P], hi[P];
+#pragma unroll
+    for (int k = 0; k < P; k++) lo[k] = hi[k] = false;
+#pragma unroll
+    for (int j = 0; j < KS; j++)
+#pragma unroll
+        for (int k = 0; k < P; k++) {
+            const bool m = rule_test<FMA>(r[j], v[k].x, v[k].y, a[k], c[k], b[k], one);
+            if (HALF && j >= KS / 2) hi[k] |= m; else lo[k] |= m;
+        }
+#pragma unroll
+    for (int k = 0; k < P; k++) {
+        if (__any_sync(0xFFFFFFFFu, lo[k] | hi[k])) {
+            const unsigned f =
+                HALF ? stage_first<KS, FMA>(r, lo[k], v[k].x, v[k].y, a[k], c[k], b[k], one)
+                     : rows_first<KS, 0, KS, FMA>(r, v[k].x, v[k].y, a[k], c[k], b[k], one);
+            if (lane == 0) s_first[q[k]] = (uint32_t)(s + f);
+        }
+    }
+}
+
+#ifndef PFW_GROUP_HALF
+#define PFW_GROUP_HALF 0
+#endif
+constexpr bool GROUP_HALF = PFW_GROUP_HALF;
+#ifndef PFW_GROUP
+#define PFW_GROUP 3
+#endif
+constexpr int GROUP = PFW_GROUP;  // packets per warp iteration (ILP)
 constexpr int BLOCK = 256;
 constexpr int NWARPS = BLOCK / 32;
 
@@ -421,8 +472,8 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
             const uint32_t id = in_ids ? __ldg(in_ids + base + i) : (uint32_t)(base + i);
             const uint4 v = __ldg(p.pkts + id);
             const uint32_t sp = v.z >> 16, dp = v.z & 0xFFFFu, pr = v.w & 0xFFu;
-            s_pk[i] = make_uint4(v.x, v.y, __float_as_uint((float)((pr << 16) | sp)),
-                                 __float_as_uint((float)((sp << 8) | pr)));
+            const float fa = (float)((pr << 16) | sp), fa2 = (float)((sp << 8) | pr);
+            s_pk[i] = make_uint4(v.x, v.y, __float_as_uint(fa - fa2), __float_as_uint(fa2));
             s_pr[i] = __float_as_uint((float)((dp << 8) | pr));
             s_id[i] = id;
             s_first[i] = PFW_NO_MATCH;
@@ -458,96 +509,53 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                     r[j][F_B_W] = NEVER_B_W;
                 }
             }
-            // Two live packets per iteration: independent chains for ILP and
-            // half the loop overhead.  Packets are warp-uniform, so every
-            // branch below is warp-uniform too.  Rows are OR-ed into two
-            // half-stage accumulators (same PLOP3 count as one) so the slow
-            // path knows which half holds the first match.
+            // Live packets are split across the warps (warp-uniform, so every
+            // branch below is warp-uniform too).
             int i = warp;
-            for (; i + NWARPS < nlive; i += 2 * NWARPS) {
-                const int q0 = live[i], q1 = live[i + NWARPS];
-                const uint4 v0 = s_pk[q0], v1 = s_pk[q1];
-                const float b0 = __uint_as_float(s_pr[q0]), b1 = __uint_as_float(s_pr[q1]);
-                const float a0 = __uint_as_float(v0.z), c0 = __uint_as_float(v0.w);
-                const float a1 = __uint_as_float(v1.z), c1 = __uint_as_float(v1.w);
-                bool lo0 = false, hi0 = false, lo1 = false, hi1 = false;
-                if (SC) {
-                    // rows in rule order; per row: IP tests, one vote, the
-                    // port/protocol tests only if some lane passed them, and the
-                    // ballot of the full result is the exact first match (no
-                    // stage-level OR, no re-evaluation).  A resolved packet
-                    // keeps only its cheap IP tests for the rest of the stage.
-                    bool done0 = false, done1 = false;
+            if (!SC) {
+                // groups of GROUP packets: independent chains for ILP, loop
+                // overhead shared by the group
+                for (; i + (GROUP - 1) * NWARPS < nlive; i += GROUP * NWARPS) {
+                    int qq[GROUP];
+#pragma unroll
+                    for (int k = 0; k < GROUP; k++) qq[k] = live[i + k * NWARPS];
+                    scan_group<GROUP, KS, FMA, GROUP_HALF>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                }
+                if (GROUP > 3 && i + NWARPS < nlive) {
+                    const int qq[2] = {live[i], live[i + NWARPS]};
+                    scan_group<2, KS, FMA, true>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    i += 2 * NWARPS;
+                }
+                if (i + NWARPS < nlive) {
+                    const int qq[2] = {live[i], live[i + NWARPS]};
+                    scan_group<2, KS, FMA, true>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    i += 2 * NWARPS;
+                }
+                if (i < nlive) {
+                    const int qq[1] = {live[i]};
+                    scan_group<1, KS, FMA, true>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                }
+            } else {
+                // short-circuit variant (off by default): rows in rule order; per
+                // row the IP tests, one vote, the port/protocol tests only if some
+                // lane passed them, and the ballot of the full result is the
+                // exact first match (no stage-level OR, no re-evaluation)
+                for (; i < nlive; i += NWARPS) {
+                    const int q = live[i];
+                    const uint4 v = s_pk[q];
+                    const float bb = __uint_as_float(s_pr[q]);
+                    const float a = __uint_as_float(v.z), c = __uint_as_float(v.w);
 #pragma unroll
                     for (int j = 0; j < KS; j++) {
-                        const bool i0 = ip_test<FMA>(r[j], v0.x, v0.y, one) & !done0;
-                        const bool i1 = ip_test<FMA>(r[j], v1.x, v1.y, one) & !done1;
-                        if (__any_sync(0xFFFFFFFFu, i0)) {
-                            const unsigned bm = __ballot_sync(0xFFFFFFFFu, i0 & port_test(r[j], a0, c0, b0));
+                        const bool ip = ip_test<FMA>(r[j], v.x, v.y, one);
+                        if (__any_sync(0xFFFFFFFFu, ip)) {
+                            const unsigned bm = __ballot_sync(0xFFFFFFFFu, ip & port_test(r[j], a, c, bb));
                             if (bm) {
-                                if (lane == 0) s_first[q0] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
-                                done0 = true;
-                            }
-                        }
-                        if (__any_sync(0xFFFFFFFFu, i1)) {
-                            const unsigned bm = __ballot_sync(0xFFFFFFFFu, i1 & port_test(r[j], a1, c1, b1));
-                            if (bm) {
-                                if (lane == 0) s_first[q1] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
-                                done1 = true;
+                                if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
+                                break;
                             }
                         }
                     }
-                    continue;
-                } else {
-#pragma unroll
-                    for (int j = 0; j < KS / 2; j++) {
-                        lo0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
-                        lo1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
-                    }
-#pragma unroll
-                    for (int j = KS / 2; j < KS; j++) {
-                        hi0 |= rule_test<FMA>(r[j], v0.x, v0.y, a0, c0, b0, one);
-                        hi1 |= rule_test<FMA>(r[j], v1.x, v1.y, a1, c1, b1, one);
-                    }
-                }
-                if (__any_sync(0xFFFFFFFFu, lo0 | hi0)) {
-                    const unsigned k = stage_first<KS, FMA>(r, lo0, v0.x, v0.y, a0, c0, b0, one);
-                    if (lane == 0) s_first[q0] = (uint32_t)(s + k);
-                }
-                if (__any_sync(0xFFFFFFFFu, lo1 | hi1)) {
-                    const unsigned k = stage_first<KS, FMA>(r, lo1, v1.x, v1.y, a1, c1, b1, one);
-                    if (lane == 0) s_first[q1] = (uint32_t)(s + k);
-                }
-            }
-            if (SC && i < nlive) {
-                const int q = live[i];
-                const uint4 v = s_pk[q];
-                const float bb = __uint_as_float(s_pr[q]);
-                const float a = __uint_as_float(v.z), c = __uint_as_float(v.w);
-#pragma unroll
-                for (int j = 0; j < KS; j++) {
-                    const bool ip = ip_test<FMA>(r[j], v.x, v.y, one);
-                    if (__any_sync(0xFFFFFFFFu, ip)) {
-                        const unsigned bm = __ballot_sync(0xFFFFFFFFu, ip & port_test(r[j], a, c, bb));
-                        if (bm) {
-                            if (lane == 0) s_first[q] = (uint32_t)(s + j * 32 + __ffs(bm) - 1);
-                            break;
-                        }
-                    }
-                }
-            } else if (i < nlive) {
-                const int q = live[i];
-                const uint4 v = s_pk[q];
-                const float bb = __uint_as_float(s_pr[q]);
-                const float a = __uint_as_float(v.z), c = __uint_as_float(v.w);
-                bool lo = false, hi = false;
-#pragma unroll
-                for (int j = 0; j < KS / 2; j++) lo |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
-#pragma unroll
-                for (int j = KS / 2; j < KS; j++) hi |= rule_test<FMA>(r[j], v.x, v.y, a, c, bb, one);
-                if (__any_sync(0xFFFFFFFFu, lo | hi)) {
-                    const unsigned k = stage_first<KS, FMA>(r, lo, v.x, v.y, a, c, bb, one);
-                    if (lane == 0) s_first[q] = (uint32_t)(s + k);
                 }
             }
             // live counter alternates between two slots so that resetting one
