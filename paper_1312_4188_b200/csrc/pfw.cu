@@ -328,6 +328,11 @@ __device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const in
             const bool m = rule_test<FMA>(r[j], v[k].x, v[k].y, a[k], c[k], b[k], one);
             if (HALF && j >= KS / 2) hi[k] |= m; else lo[k] |= m;
         }
+    // one vote for the whole group; per-packet votes only when it hit
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < P; k++) any |= lo[k] | hi[k];
+    if (!__any_sync(0xFFFFFFFFu, any)) return;
 #pragma unroll
     for (int k = 0; k < P; k++) {
         if (__any_sync(0xFFFFFFFFu, lo[k] | hi[k])) {
