@@ -167,6 +167,24 @@ int pfw_generate_traffic_at(int device, uint64_t seed, int64_t first_packet, int
                             int sport_lo, int sport_hi, int dport_lo, int dport_hi, void *d_out,
                             void *stream);
 
+/* Native readers / writers of the formats feeding the path (hostio.cpp).
+ * They accept the canonical grammar strictly and return PFW_ERR_INVALID with
+ * pfw_io_last_error() = "line N: ..." at the first line they cannot accept;
+ * callers then re-read with the reference-compatible parser (exact errors).
+ *   pfw_parse_rules    ruleset text (model.py:7-20, 233-331) -> the ten
+ *                      CompiledRuleset columns (classifier.py:120-134)
+ *   pfw_parse_traffic  traffic CSV (traffic.py:259-297) -> ids + 16-byte records
+ *   pfw_format_results "id,VERDICT,index|-" lines (cli.py:62-65) */
+const char *pfw_io_last_error(void);
+int pfw_parse_rules(const char *buf, int64_t len, int64_t cap, uint8_t *proto, uint32_t *src_base,
+                    uint32_t *src_mask, uint16_t *sport_lo, uint16_t *sport_hi, uint32_t *dst_base,
+                    uint32_t *dst_mask, uint16_t *dport_lo, uint16_t *dport_hi, uint8_t *accept,
+                    int64_t *n_out);
+int pfw_parse_traffic(const char *buf, int64_t len, int64_t cap, int64_t *ids, void *h_records,
+                      int64_t *n_out);
+int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t *verdict, int64_t n,
+                       char *out, int64_t cap, int64_t *written);
+
 /* Launch-count / tuning introspection (bench + tests). */
 int64_t pfw_launch_count(void);
 int pfw_set_tuning(const char *key, int64_t value);

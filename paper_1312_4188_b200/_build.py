@@ -7,6 +7,7 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "pfw.cu")
+SRC_HOST = os.path.join(PKG, "csrc", "hostio.cpp")
 LIB = os.path.join(PKG, "libpfw.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -22,11 +23,11 @@ NVCC_FLAGS = [
 def build_native(verbose: bool = False, force: bool = False, out: str = LIB, defines=()) -> str:
     """Compile csrc/pfw.cu -> libpfw.so unless the library is newer than its sources.
     ``defines`` (e.g. ["PFW_GROUP=4"]) build experiment variants into ``out``."""
-    deps = [SRC, os.path.join(ROOT, "include", "pfw.h"), os.path.abspath(__file__)]
+    deps = [SRC, SRC_HOST, os.path.join(ROOT, "include", "pfw.h"), os.path.abspath(__file__)]
     if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out
     tmp = out + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, SRC, "-lcudart"]
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, SRC, SRC_HOST, "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr}")

@@ -59,6 +59,10 @@ _SIGS = {
                                     _I32, _I32, _P, _P]),
     "pfw_generate_traffic_at": (_I32, [_I32, _U64, _I64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,
                                        _I32, _I32, _P, _P]),
+    "pfw_io_last_error": (ctypes.c_char_p, []),
+    "pfw_parse_rules": (_I32, [_P, _I64, _I64] + [_P] * 10 + [ctypes.POINTER(_I64)]),
+    "pfw_parse_traffic": (_I32, [_P, _I64, _I64, _P, _P, ctypes.POINTER(_I64)]),
+    "pfw_format_results": (_I32, [_P, _P, _P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
     "pfw_launch_count": (_I64, []),
     "pfw_set_tuning": (_I32, [ctypes.c_char_p, _I64]),
 }

@@ -237,16 +237,6 @@ __device__ __forceinline__ bool ip_test(const uint32_t (&r)[NF], uint32_t src, u
     return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]);
 }
 
-// warp-uniform "any" without the compiler's divergence check (the scan loop
-// is warp-uniform by construction: every lane runs every iteration)
-__device__ __forceinline__ bool warp_any(bool x) {
-    uint32_t r;
-    asm volatile(
-        "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nvote.sync.any.pred q, p, 0xffffffff;\nselp.u32 %0, 1, 0, q;\n}\n"
-        : "=r"(r) : "r"((uint32_t)x));
-    return r != 0;
-}
-
 __device__ __forceinline__ bool port_test(const uint32_t (&r)[NF], float A, float A2, float B) {
     const float x = A2 + __uint_as_float(r[F_A_NLO]);
     const float dA = fmaf(A, __uint_as_float(r[F_A_C1]), x);
