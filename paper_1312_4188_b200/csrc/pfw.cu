@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
     uint16_t *s_liveB = s_liveA + TMAX;
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(s_liveB + TMAX) + 15) & ~uintptr_t(15));
-    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile, [3]=out base
+    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t one = p.one;
