@@ -42,6 +42,20 @@
 
 #define PFW_VERSION "0.1.0"
 
+// -DPFW_CHECKS builds device-side bounds assertions into every derived index
+// (compute-sanitizer is not available on the GPU pool): a violated check
+// traps the kernel, which the parity suite then reports as a CUDA error.
+#ifdef PFW_CHECKS
+#define PFW_CHECK(cond) \
+    do {                \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define PFW_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace {
 
 // ------------------------------------------------------------------ errors
@@ -175,6 +189,7 @@ struct ScanParams {
     const unsigned int *in_count0;
     uint32_t *out_ids;         // survivors of this pass (null = final pass)
     unsigned int *out_count;
+    int64_t out_cap;           // capacity of out_ids (checks)
     uint32_t *first;
     uint32_t *comps;
     uint8_t *verdict;
@@ -329,6 +344,7 @@ __device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const in
             const unsigned f =
                 HALF ? stage_first<KS, FMA>(r, lo[k], v[k].x, v[k].y, a[k], c[k], b[k], one)
                      : rows_first<KS, 0, KS, FMA>(r, v[k].x, v[k].y, a[k], c[k], b[k], one);
+            PFW_CHECK(f < (unsigned)KS * 32u && q[k] >= 0);
             if (lane == 0) s_first[q[k]] = (uint32_t)(s + f);
         }
     }
@@ -465,6 +481,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
             // per-packet precompute, amortised over every stage of the pass:
             // the fp32 port/proto words (exact integers < 2^24)
             const uint32_t id = in_ids ? __ldg(in_ids + base + i) : (uint32_t)(base + i);
+            PFW_CHECK(id < (uint64_t)p.n && i < T && T <= TMAX);
             const uint4 v = __ldg(p.pkts + id);
             const uint32_t sp = v.z >> 16, dp = v.z & 0xFFFFu, pr = v.w & 0xFFu;
             const float fa = (float)((pr << 16) | sp), fa2 = (float)((sp << 8) | pr);
@@ -493,6 +510,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
 
             // stage rules -> registers (lane l: rules s + 32j + l)
             const uint32_t *sr = s_rules + buf * NF * STAGE;
+            PFW_CHECK(s >= 0 && s + STAGE <= p.rpad && nlive <= T);
             uint32_t r[KS][NF];
 #pragma unroll
             for (int j = 0; j < KS; j++) {
@@ -600,7 +618,9 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 id = s_id[i];
                 survive = !final_pass && f == PFW_NO_MATCH;
                 if (!survive) {
+                    PFW_CHECK(f == PFW_NO_MATCH || (f >= p.lo && f < p.hi));
                     if (p.orig && f != PFW_NO_MATCH) f = __ldg(p.orig + f);
+                    PFW_CHECK(f == PFW_NO_MATCH || (f >= p.win_lo && f < p.win_hi));
                     const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.win_lo + 1) : span;
                     if (MODE == MODE_ACC) {
                         if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
@@ -616,6 +636,7 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                             const uint64_t big = (q + 1) * r;
                             const uint64_t o = id < big ? id / (q + 1) : r + (id - big) / q;
                             const uint64_t off = id - (o < r ? o * (q + 1) : big + (o - r) * q);
+                            PFW_CHECK(o < (uint64_t)p.npeers && off < (o < r ? q + 1 : q));
                             if (f != PFW_NO_MATCH) atomicMin(p.peer_first[o] + off, f);
                             if (p.peer_comps) atomicAdd(p.peer_comps[o] + off, c);
                         } else {
@@ -638,7 +659,10 @@ __global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
                 unsigned off = 0;
                 if (lane == 0) off = atomicAdd(p.out_count, (unsigned)__popc(b));
                 off = __shfl_sync(0xFFFFFFFFu, off, 0);
-                if (survive) p.out_ids[off + __popc(b & ((1u << lane) - 1u))] = id;
+                if (survive) {
+                    PFW_CHECK(off + __popc(b & ((1u << lane) - 1u)) < (uint64_t)p.out_cap);
+                    p.out_ids[off + __popc(b & ((1u << lane) - 1u))] = id;
+                }
             }
         }
         __syncthreads();
@@ -712,7 +736,11 @@ __global__ void __launch_bounds__(BK_BLOCK) bucket_scatter_kernel(const uint4 *p
 #pragma unroll
     for (int k = 0; k < BK_PER_THREAD; k++) {
         const int64_t i = b0 + (int64_t)k * BK_BLOCK + threadIdx.x;
-        if (i < n) ids[gbase[ch[k]] + atomicAdd(&hist[ch[k]], 1u)] = (uint32_t)i;
+        if (i < n) {
+            const unsigned pos = gbase[ch[k]] + atomicAdd(&hist[ch[k]], 1u);
+            PFW_CHECK(pos < (uint64_t)n && ch[k] < nchains);
+            ids[pos] = (uint32_t)i;
+        }
     }
 }
 
@@ -947,6 +975,7 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
         const bool last = k == npass - 1;
         p.out_ids = last ? nullptr : ws.ids + (size_t)(k & 1) * ws.cap;
         p.out_count = last ? nullptr : ws.ctr + 2 * k + 1;
+        p.out_cap = last ? 0 : ws.cap;
         kern<<<(unsigned)grid, BLOCK, sm, st>>>(p);
         CUDA_TRY(cudaGetLastError());
         g_launches++;
