@@ -418,8 +418,13 @@ __device__ __forceinline__ void issue_stage(const ScanParams &p, int64_t s, uint
     for (int f = 0; f < NF; f++) tma_bulk_g2s(buf + f * 32 * KS, p.rules + f * p.rpad + s, ROW, bar);
 }
 
+// 8-row stages need ~120 registers (2 CTAs = 16 warps per SM); short stages
+// fit 3 CTAs per SM (24 warps) for more latency hiding.
+template <int KS>
+constexpr int min_ctas() { return KS <= 4 ? 3 : 2; }
+
 template <int KS, int MODE, bool FMA, bool SC>
-__global__ void __launch_bounds__(BLOCK, 2) scan_kernel(ScanParams p) {
+__global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int TMAX = p.tile;  // shared-memory capacity in packets
     uint4 *s_pk = reinterpret_cast<uint4 *>(smem_raw);
