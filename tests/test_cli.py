@@ -102,3 +102,25 @@ def test_estimator_predict_matches_golden():
     np.testing.assert_array_equal(labels == "ACCEPT", g["verdict"])
     res = clf.match(X[:100])
     assert [r.matched_index if r.matched_index is not None else -1 for r in res] == g["first"][:100].tolist()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_verify_detects_divergence(tmp_path, capsys, monkeypatch):
+    """Mutation fixture: corrupt one model's results -> exit 3."""
+    from paper_1312_4188_b200 import engines
+    rules = write_rules(tmp_path, ["DROP tcp * * * 22", "ACCEPT tcp 10.0.0.0/8 * * *"])
+    traffic = write_traffic(tmp_path, ["0,tcp,10.1.2.3,5555,8.8.8.8,22", "1,tcp,10.1.2.3,5555,8.8.8.8,80"])
+    real = engines.Engine.run_arrays
+
+    def mutated(self, ruleset, packets):
+        res = real(self, ruleset, packets)
+        if self.config.model is engines.ExecutionModel.HYBRID and self.config.nodes == 2:
+            first = res.first.copy()
+            first[1] = -1
+            return engines.EngineResult(first, res.comparisons, res.verdict_accept, res.stats)
+        return res
+
+    monkeypatch.setattr(engines.Engine, "run_arrays", mutated)
+    assert cli.main(["verify", "--rules", rules, "--traffic", traffic]) == cli.EXIT_DIVERGENCE
+    assert "divergence: packet 1 model hybrid nodes 2" in capsys.readouterr().err
