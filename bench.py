@@ -380,16 +380,22 @@ def main() -> int:
     # --- end to end through the C-ABI with host buffers (pfw_classify_host)
     e2e = None
     if not args.no_e2e and w.model != "function":
-        host_pk = pkts.data.cpu().pin_memory()
+        # host input in the reference's own layout: the five PacketArrays columns
+        # (classifier.py:62-95, 13 B/packet), pinned; nothing is packed on the host
+        hc = pkts.columns()
+        dt = {np.dtype(np.uint8): torch.uint8, np.dtype(np.uint16): torch.int16,
+              np.dtype(np.uint32): torch.int32}
+        host_cols = [torch.from_numpy(hc[f].view(dt[hc[f].dtype])).pin_memory()
+                     for f in ("proto", "src_ip", "src_port", "dst_ip", "dst_port")]
         h_first = torch.empty(n, dtype=torch.int32).pin_memory()
         h_verd = torch.empty(n, dtype=torch.uint8).pin_memory()
         h_stats = torch.zeros(2, dtype=torch.int64)
         lib = _native.lib()
 
         def e2e_step():
-            _native.check(lib.pfw_classify_host(compiled.handle, host_pk.data_ptr(), n, h_first.data_ptr(),
-                                                h_verd.data_ptr(), h_stats.data_ptr(), args.e2e_chunk),
-                          "pfw_classify_host")
+            _native.check(lib.pfw_classify_host_columns(
+                compiled.handle, *[t.data_ptr() for t in host_cols], n, h_first.data_ptr(),
+                h_verd.data_ptr(), h_stats.data_ptr(), args.e2e_chunk), "pfw_classify_host_columns")
         for _ in range(max(1, args.warmup)):
             e2e_step()
         # parity of the e2e path with the device-resident path (bit-exact)
@@ -405,9 +411,10 @@ def main() -> int:
         tt = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
         parallel.all_reduce(tt, dist.ReduceOp.MAX)
         e2e = {"value": pk_per_step * args.steps / float(tt.item()) / 1e6, "unit": "Mpps",
-               "h2d_bytes_per_step": n * PKT_BYTES, "d2h_bytes_per_step": n * 5,
-               "api": f"pfw_classify_host (C-ABI, pinned host buffers, {args.e2e_chunk}-packet chunks, "
-                      "copy-in / 2x compute / copy-out streams, 3 slots)"}
+               "h2d_bytes_per_step": n * 13, "d2h_bytes_per_step": n * 5,
+               "api": f"pfw_classify_host_columns (C-ABI, the reference's PacketArrays columns in "
+                      f"pinned host memory, {args.e2e_chunk}-packet chunks, copy-in / 2x compute / "
+                      "copy-out streams, 3 slots)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

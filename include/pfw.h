@@ -92,6 +92,14 @@ int pfw_scan_range(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, 
                    uint32_t *d_first, uint32_t *d_comps, uint8_t *d_verdict,
                    uint64_t *d_stats, void *stream);
 
+/* Same scan reading the reference's own column layout (PacketArrays,
+ * classifier.py:62-95: proto u8, src_ip u32, src_port u16, dst_ip u32,
+ * dst_port u16 -- 13 bytes per packet) directly, no packing step. */
+int pfw_scan_range_columns(pfw_ruleset_t h, int64_t lo, int64_t hi, const uint8_t *d_proto,
+                           const uint32_t *d_src_ip, const uint16_t *d_src_port, const uint32_t *d_dst_ip,
+                           const uint16_t *d_dst_port, int64_t n, uint32_t *d_first, uint32_t *d_comps,
+                           uint8_t *d_verdict, uint64_t *d_stats, void *stream);
+
 /* One partition of the function-parallel / hybrid models.  Replaces a
  * _scan_partitions task + its share of _combine_rows (engines.py:349-369):
  *   d_first[i]  = min(d_first[i], partition-local first match)
@@ -147,6 +155,13 @@ int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d
  * h_verdict and h_stats ([sum, max] comparisons) are nullable. */
 int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *h_first,
                       uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk);
+
+/* pfw_classify_host for the reference's column layout (PacketArrays):
+ * copies 13 bytes per packet (five column copies per chunk), no host packing. */
+int pfw_classify_host_columns(pfw_ruleset_t h, const uint8_t *h_proto, const uint32_t *h_src_ip,
+                              const uint16_t *h_src_port, const uint32_t *h_dst_ip,
+                              const uint16_t *h_dst_port, int64_t n, uint32_t *h_first,
+                              uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk);
 
 /* Bit-exact UNIFORM traffic generation on the device.  Replaces
  * generate_traffic(TrafficProfile(...)) with match_mode UNIFORM

@@ -45,6 +45,7 @@ _SIGS = {
     "pfw_ruleset_device": (_I32, [_P]),
     "pfw_pack_packets_host": (_I32, [_I64, _P, _P, _P, _P, _P, _P]),
     "pfw_scan_range": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P]),
+    "pfw_scan_range_columns": (_I32, [_P, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "pfw_scan_partition_accumulate": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
     "pfw_accumulator_init": (_I32, [_I64, _P, _P, _P]),
     "pfw_scan_fused_min": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _I32, _I32, _P, _P]),
@@ -55,6 +56,7 @@ _SIGS = {
     "pfw_verdicts": (_I32, [_P, _P, _I64, _P, _P]),
     "pfw_combine_min": (_I32, [_P, _I64, _I64, _P, _P]),
     "pfw_classify_host": (_I32, [_P, _P, _I64, _P, _P, _P, _I64]),
+    "pfw_classify_host_columns": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I64]),
     "pfw_generate_traffic": (_I32, [_I32, _U64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,
                                     _I32, _I32, _P, _P]),
     "pfw_generate_traffic_at": (_I32, [_I32, _U64, _I64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,

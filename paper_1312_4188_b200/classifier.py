@@ -285,6 +285,40 @@ class CompiledRuleset:
               "pfw_scan_range")
         return first
 
+    def scan_range_columns_device(self, cols: dict, lo: int, hi: int, *, first=None, comps=None,
+                                  verdict=None, stats=None, stream: int | None = None):
+        """scan_range over the reference's own column layout on the device:
+        ``cols`` maps proto / src_ip / src_port / dst_ip / dst_port to CUDA
+        tensors (uint8, int32/uint32, int16/uint16 bit patterns) -- no packing."""
+        torch = _torch()
+        n = int(cols["proto"].numel())
+        if first is None:
+            first = torch.empty(n, dtype=torch.int32, device=cols["proto"].device)
+        lo, hi = int(lo), int(hi)
+        if lo > hi:
+            lo = hi
+        st = _stream(self.device) if stream is None else stream
+        check(_native.lib().pfw_scan_range_columns(
+            self._h, lo, hi, _ptr(cols["proto"]), _ptr(cols["src_ip"]), _ptr(cols["src_port"]),
+            _ptr(cols["dst_ip"]), _ptr(cols["dst_port"]), n, _ptr(first), _ptr(comps), _ptr(verdict),
+            _ptr(stats), st), "pfw_scan_range_columns")
+        return first
+
+    def classify_host_columns(self, cols: dict, chunk: int = 1 << 22):
+        """End-to-end over HOST columns (numpy; pinned memory overlaps the copies):
+        returns (first int64 with -1 for default deny, verdict bool, [sum, max] comps)."""
+        n = len(cols["proto"])
+        arrs = [np.ascontiguousarray(cols[f], dtype=d) for f, d in zip(PACKET_COLUMNS, _PACKET_DTYPES)]
+        first = np.empty(n, dtype=np.uint32)
+        verdict = np.empty(n, dtype=np.uint8)
+        stats = np.zeros(2, dtype=np.uint64)
+        check(_native.lib().pfw_classify_host_columns(self._h, *[a.ctypes.data for a in arrs], n,
+                                                      first.ctypes.data, verdict.ctypes.data,
+                                                      stats.ctypes.data, chunk), "pfw_classify_host_columns")
+        f = first.astype(np.int64)
+        f[f == NO_MATCH] = -1
+        return f, verdict.astype(np.bool_), stats.astype(np.int64)
+
     def scan_partition_accumulate(self, pkts: PacketArrays, lo: int, hi: int, first, comps, stats=None,
                                   stream: int | None = None) -> None:
         """Function-parallel / hybrid partition task folded into running min / sums."""

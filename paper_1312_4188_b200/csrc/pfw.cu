@@ -172,6 +172,16 @@ namespace {
 
 // ================================================================ kernels
 
+// The reference's own packet layout (PacketArrays, classifier.py:62-95): five
+// SoA columns, 13 bytes per packet.  Scans read either these or 16-byte records.
+struct PacketCols {
+    const uint8_t *proto;
+    const uint32_t *src;
+    const uint16_t *sport;
+    const uint32_t *dst;
+    const uint16_t *dport;
+};
+
 struct ScanParams {
     const uint32_t *rules;
     const uint8_t *accept;
@@ -180,7 +190,8 @@ struct ScanParams {
     int64_t win_lo, win_hi;    // the same window in original rule indices (comparisons)
     const uint32_t *orig;      // table position -> original rule index (null = identity)
     int64_t s_begin, s_end;    // this pass: stage starts s_begin, s_begin+STAGE, ... < s_end
-    const uint4 *pkts;
+    const uint4 *pkts;         // 16-byte records, or null: read the columns in `cols`
+    PacketCols cols;
     int64_t n;                 // packets in the batch (pass 0 count when in_ids == null)
     const uint32_t *in_ids;    // live packet ids of this pass (null = 0..n-1)
     const unsigned int *in_count;  // device count of in_ids (null = n)
@@ -487,7 +498,15 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
             // the fp32 port/proto words (exact integers < 2^24)
             const uint32_t id = in_ids ? __ldg(in_ids + base + i) : (uint32_t)(base + i);
             PFW_CHECK(id < (uint64_t)p.n && i < T && T <= TMAX);
-            const uint4 v = __ldg(p.pkts + id);
+            uint4 v;
+            if (p.pkts) {
+                v = __ldg(p.pkts + id);
+            } else {
+                v.x = __ldg(p.cols.src + id);
+                v.y = __ldg(p.cols.dst + id);
+                v.z = ((uint32_t)__ldg(p.cols.sport + id) << 16) | (uint32_t)__ldg(p.cols.dport + id);
+                v.w = __ldg(p.cols.proto + id);
+            }
             const uint32_t sp = v.z >> 16, dp = v.z & 0xFFFFu, pr = v.w & 0xFFu;
             const float fa = (float)((pr << 16) | sp), fa2 = (float)((sp << 8) | pr);
             s_pk[i] = make_uint4(v.x, v.y, __float_as_uint(fa - fa2), __float_as_uint(fa2));
@@ -691,8 +710,12 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
 // not serialise on one counter.  counts/base/cursor live in bc[0..3*MAX_CHAINS).
 constexpr int BK_BLOCK = 256, BK_PER_THREAD = 16;
 
-__global__ void __launch_bounds__(BK_BLOCK) bucket_count_kernel(const uint4 *pkts, int64_t n,
-                                                                const uint8_t *lut, int nchains,
+__device__ __forceinline__ uint32_t pkt_proto(const uint4 *pkts, const uint8_t *proto_col, int64_t i) {
+    return proto_col ? (uint32_t)__ldg(proto_col + i) : __ldg(&pkts[i].w) & 0xFFu;
+}
+
+__global__ void __launch_bounds__(BK_BLOCK) bucket_count_kernel(const uint4 *pkts, const uint8_t *proto_col,
+                                                                int64_t n, const uint8_t *lut, int nchains,
                                                                 unsigned *bc) {
     __shared__ unsigned hist[MAX_CHAINS];
     for (int c = threadIdx.x; c < nchains; c += BK_BLOCK) hist[c] = 0;
@@ -700,7 +723,7 @@ __global__ void __launch_bounds__(BK_BLOCK) bucket_count_kernel(const uint4 *pkt
     const int64_t b0 = (int64_t)blockIdx.x * BK_BLOCK * BK_PER_THREAD;
     for (int k = 0; k < BK_PER_THREAD; k++) {
         const int64_t i = b0 + (int64_t)k * BK_BLOCK + threadIdx.x;
-        if (i < n) atomicAdd(&hist[lut[__ldg(&pkts[i].w) & 0xFFu]], 1u);
+        if (i < n) atomicAdd(&hist[lut[pkt_proto(pkts, proto_col, i)]], 1u);
     }
     __syncthreads();
     for (int c = threadIdx.x; c < nchains; c += BK_BLOCK)
@@ -718,8 +741,8 @@ __global__ void bucket_prefix_kernel(int nchains, unsigned *bc) {
     }
 }
 
-__global__ void __launch_bounds__(BK_BLOCK) bucket_scatter_kernel(const uint4 *pkts, int64_t n,
-                                                                  const uint8_t *lut, int nchains,
+__global__ void __launch_bounds__(BK_BLOCK) bucket_scatter_kernel(const uint4 *pkts, const uint8_t *proto_col,
+                                                                  int64_t n, const uint8_t *lut, int nchains,
                                                                   unsigned *bc, uint32_t *ids) {
     __shared__ unsigned hist[MAX_CHAINS], gbase[MAX_CHAINS];
     for (int c = threadIdx.x; c < nchains; c += BK_BLOCK) hist[c] = 0;
@@ -729,7 +752,7 @@ __global__ void __launch_bounds__(BK_BLOCK) bucket_scatter_kernel(const uint4 *p
 #pragma unroll
     for (int k = 0; k < BK_PER_THREAD; k++) {
         const int64_t i = b0 + (int64_t)k * BK_BLOCK + threadIdx.x;
-        ch[k] = i < n ? lut[__ldg(&pkts[i].w) & 0xFFu] : 0;
+        ch[k] = i < n ? lut[pkt_proto(pkts, proto_col, i)] : 0;
         if (i < n) atomicAdd(&hist[ch[k]], 1u);
     }
     __syncthreads();
@@ -1016,7 +1039,8 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaS
 
 int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                 uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
-                cudaStream_t st, ScanWs *ws = nullptr, const ScanParams *peer = nullptr) {
+                cudaStream_t st, ScanWs *ws = nullptr, const ScanParams *peer = nullptr,
+                const PacketCols *cols = nullptr) {
     const bool acc = mode == MODE_ACC;
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count %lld", (long long)n);
@@ -1026,7 +1050,9 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
     if (hi > h->n) return set_err(PFW_ERR_INVALID, "rule window end %lld beyond ruleset of %lld",
                                   (long long)hi, (long long)h->n);
     if (n == 0) return PFW_OK;
-    if (!d_pkts || (!first && mode != MODE_PEER)) return set_err(PFW_ERR_INVALID, "null packet or output pointer");
+    const bool have_cols = cols && cols->proto && cols->src && cols->sport && cols->dst && cols->dport;
+    if ((!d_pkts && !have_cols) || (!first && mode != MODE_PEER))
+        return set_err(PFW_ERR_INVALID, "null packet or output pointer");
     if (acc && !comps) return set_err(PFW_ERR_INVALID, "accumulate needs a comps buffer");
     if (lo > hi) lo = hi;  // empty window: scan_range returns all -1
     ScanParams p{};
@@ -1038,7 +1064,8 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
     p.win_lo = lo;
     p.win_hi = hi;
     p.orig = nullptr;
-    p.pkts = reinterpret_cast<const uint4 *>(d_pkts);
+    p.pkts = have_cols ? nullptr : reinterpret_cast<const uint4 *>(d_pkts);
+    if (have_cols) p.cols = *cols;
     p.n = n;
     p.first = first;
     p.comps = comps;
@@ -1083,9 +1110,10 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cuda
     if (!h->d_bcount) CUDA_TRY(cudaMalloc(&h->d_bcount, 3 * MAX_CHAINS * sizeof(unsigned)));
     CUDA_TRY(cudaMemsetAsync(h->d_bcount, 0, MAX_CHAINS * sizeof(unsigned), st));
     const unsigned nb = (unsigned)((n + BK_BLOCK * BK_PER_THREAD - 1) / (BK_BLOCK * BK_PER_THREAD));
-    bucket_count_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, n, h->d_lut, nch, h->d_bcount);
+    bucket_count_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, h->d_bcount);
     bucket_prefix_kernel<<<1, 32, 0, st>>>(nch, h->d_bcount);
-    bucket_scatter_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, n, h->d_lut, nch, h->d_bcount, h->d_bucket);
+    bucket_scatter_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, h->d_bcount,
+                                                  h->d_bucket);
     CUDA_TRY(cudaGetLastError());
     g_launches += 3;
     // bucket c's ids start at base[c]; its count is bc[c].  The base is only
@@ -1338,6 +1366,15 @@ int pfw_scan_range(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, 
                        (cudaStream_t)stream);
 }
 
+int pfw_scan_range_columns(pfw_ruleset_t h, int64_t lo, int64_t hi, const uint8_t *d_proto,
+                           const uint32_t *d_src_ip, const uint16_t *d_src_port, const uint32_t *d_dst_ip,
+                           const uint16_t *d_dst_port, int64_t n, uint32_t *d_first, uint32_t *d_comps,
+                           uint8_t *d_verdict, uint64_t *d_stats, void *stream) {
+    const PacketCols c{d_proto, d_src_ip, d_src_port, d_dst_ip, d_dst_port};
+    return launch_scan(h, MODE_WRITE, lo, hi, nullptr, n, d_first, d_comps, d_verdict, d_stats,
+                       (cudaStream_t)stream, nullptr, nullptr, &c);
+}
+
 int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts,
                                   int64_t n, uint32_t *d_first, uint32_t *d_comps,
                                   uint64_t *d_stats, void *stream) {
@@ -1452,8 +1489,8 @@ int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d
     return PFW_OK;
 }
 
-int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *h_first,
-                      uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
+static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketCols *hc, int64_t n,
+                              uint32_t *h_first, uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
     // Three-stage pipeline over E2E_SLOTS buffer slots:
     //   copy-in stream   H2D chunk k into slot k%S     (waits: scan k-S done)
     //   compute streams  scan chunk k on stream k%2    (waits: H2D k done); two
@@ -1465,13 +1502,14 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count");
     if (h_stats) h_stats[0] = h_stats[1] = 0;
     if (n == 0) return PFW_OK;
-    if (!h_pkts || !h_first) return set_err(PFW_ERR_INVALID, "null host buffer");
+    if ((!h_pkts && !hc) || !h_first) return set_err(PFW_ERR_INVALID, "null host buffer");
     if (chunk <= 0) chunk = 1 << 22;
     if (chunk > n) chunk = n;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
     constexpr int S = E2E_SLOTS;
-    const size_t slot = (((size_t)chunk * 21 + 255) / 256) * 256;  // packets 16B + first 4B + verdict 1B
+    // slot: packets (16B records, or 13B of columns) + first 4B + verdict 1B
+    const size_t slot = (((size_t)chunk * 21 + 255) / 256) * 256;
     const size_t need = S * slot + 256;
     if (h->ws_bytes < need) {
         if (h->d_ws) cudaFree(h->d_ws);
@@ -1503,14 +1541,28 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
         uint4 *dp = reinterpret_cast<uint4 *>(base);
         uint32_t *df = reinterpret_cast<uint32_t *>(base + (size_t)chunk * 16);
         uint8_t *dv = reinterpret_cast<uint8_t *>(base + (size_t)chunk * 20);
+        // column layout inside the 16B/packet region: src | dst | sport | dport | proto
+        PacketCols dc{reinterpret_cast<const uint8_t *>(base + (size_t)chunk * 12),
+                      reinterpret_cast<const uint32_t *>(base),
+                      reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 8),
+                      reinterpret_cast<const uint32_t *>(base + (size_t)chunk * 4),
+                      reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 10)};
         if (k >= S) CUDA_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
-        CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
-                                 cudaMemcpyHostToDevice, s_in));
+        if (hc) {
+            CUDA_TRY(cudaMemcpyAsync((void *)dc.src, hc->src + c0, m * 4, cudaMemcpyHostToDevice, s_in));
+            CUDA_TRY(cudaMemcpyAsync((void *)dc.dst, hc->dst + c0, m * 4, cudaMemcpyHostToDevice, s_in));
+            CUDA_TRY(cudaMemcpyAsync((void *)dc.sport, hc->sport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
+            CUDA_TRY(cudaMemcpyAsync((void *)dc.dport, hc->dport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
+            CUDA_TRY(cudaMemcpyAsync((void *)dc.proto, hc->proto + c0, m, cudaMemcpyHostToDevice, s_in));
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
+                                     cudaMemcpyHostToDevice, s_in));
+        }
         CUDA_TRY(cudaEventRecord(ev_in[sl], s_in));
         CUDA_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
         if (k >= S) CUDA_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
-        rc = launch_scan(h, MODE_WRITE, 0, h->n, dp, m, df, nullptr, h_verdict ? dv : nullptr,
-                         h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1]);
+        rc = launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
+                         h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr);
         if (rc != PFW_OK) break;
         CUDA_TRY(cudaEventRecord(ev_scan[sl], s_comp));
         CUDA_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
@@ -1522,6 +1574,22 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
     if (rc != PFW_OK) return rc;
     if (h_stats) CUDA_TRY(cudaMemcpy(h_stats, d_stats, 16, cudaMemcpyDeviceToHost));
     return PFW_OK;
+}
+
+
+int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *h_first,
+                      uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
+    return classify_host_impl(h, h_pkts, nullptr, n, h_first, h_verdict, h_stats, chunk);
+}
+
+int pfw_classify_host_columns(pfw_ruleset_t h, const uint8_t *h_proto, const uint32_t *h_src_ip,
+                              const uint16_t *h_src_port, const uint32_t *h_dst_ip,
+                              const uint16_t *h_dst_port, int64_t n, uint32_t *h_first,
+                              uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
+    if (n > 0 && (!h_proto || !h_src_ip || !h_src_port || !h_dst_ip || !h_dst_port))
+        return set_err(PFW_ERR_INVALID, "null packet column");
+    const PacketCols hc{h_proto, h_src_ip, h_src_port, h_dst_ip, h_dst_port};
+    return classify_host_impl(h, nullptr, &hc, n, h_first, h_verdict, h_stats, chunk);
 }
 
 int pfw_generate_traffic(int device, uint64_t seed, int64_t n, int proto, uint32_t src_base,

@@ -453,3 +453,25 @@ def test_proto_split_windows_engines_and_mixed_protocols():
 def test_short_circuit_scan_matches_reference_golden(name, rn, tn):
     _native.set_tuning("short_circuit", 1)
     test_scan_matches_reference_golden(name, rn, tn)
+
+
+# --------------------------------------------------- reference column layout
+
+def test_scan_range_columns_device_and_host():
+    rules = golden_rules("r2048_s21_w15")
+    pk = golden_traffic("t10000_s41")
+    c = compiled(rules)
+    dev = {f: torch.from_numpy(np.ascontiguousarray(pk[f]).view(
+        {np.uint8: np.uint8, np.uint16: np.int16, np.uint32: np.int32}[pk[f].dtype.type])).to("cuda:0")
+        for f in PKT_FIELDS}
+    for split in (0, 1):
+        _native.set_tuning("proto_split", split)
+        for lo, hi in ((0, 2048), (100, 1500)):
+            first = c.scan_range_columns_device(dev, lo, hi)
+            np.testing.assert_array_equal(first_to_host(first), oracle.scan_range(rules, pk, lo, hi))
+    f, v, st = c.classify_host_columns(pk, chunk=3001)
+    want = oracle.scan_range(rules, pk, 0, 2048)
+    np.testing.assert_array_equal(f, want)
+    np.testing.assert_array_equal(v, np.where(want >= 0, rules["action_accept"][np.maximum(want, 0)], False))
+    comps = oracle.sequential_comparisons(want, 2048)
+    assert st.tolist() == [int(comps.sum()), int(comps.max())]
