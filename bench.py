@@ -383,8 +383,7 @@ def main() -> int:
         # host input in the reference's own layout: the five PacketArrays columns
         # (classifier.py:62-95, 13 B/packet), pinned; nothing is packed on the host
         hc = pkts.columns()
-        dt = {np.dtype(np.uint8): torch.uint8, np.dtype(np.uint16): torch.int16,
-              np.dtype(np.uint32): torch.int32}
+        dt = {np.dtype(np.uint8): np.uint8, np.dtype(np.uint16): np.int16, np.dtype(np.uint32): np.int32}
         host_cols = [torch.from_numpy(hc[f].view(dt[hc[f].dtype])).pin_memory()
                      for f in ("proto", "src_ip", "src_port", "dst_ip", "dst_port")]
         h_first = torch.empty(n, dtype=torch.int32).pin_memory()
