@@ -455,15 +455,18 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
     const bool final_pass = p.out_ids == nullptr;
     const int64_t count = p.in_count ? (int64_t)*p.in_count : p.n;
     const uint32_t *in_ids = p.in_ids ? p.in_ids + (p.bucket_base ? *p.bucket_base : 0u) : nullptr;
-    // Tile size for this pass: the full capacity when there is enough work,
-    // otherwise small enough to give every CTA ~2 tiles (late passes carry
-    // few survivors; a handful of huge tiles would idle most SMs).  Every
-    // CTA derives the same T from the same count.
+    // Tile size for this pass: the full capacity when there is enough work;
+    // otherwise sized so the tile count is a whole number of waves of the
+    // persistent grid (small batches and late passes carry few packets: a
+    // 1.3-wave tail would idle most SMs).  Every CTA derives the same T.
     int T = TMAX;
     {
-        const int64_t want = (count + 2 * (int64_t)gridDim.x - 1) / (2 * (int64_t)gridDim.x);
-        if (want < T) T = (int)(want < 256 ? 256 : ((want + 31) & ~int64_t(31)));
-        if (T > TMAX) T = TMAX;
+        const int64_t g = (int64_t)gridDim.x;
+        const int64_t k = (count + g * TMAX - 1) / (g * TMAX);  // waves at the full tile size
+        if (k >= 1) {
+            const int64_t want = ((count + g * k - 1) / (g * k) + 31) & ~int64_t(31);
+            if (want < T) T = (int)(want < 64 ? 64 : want);
+        }
     }
     const int64_t ntiles = (count + T - 1) / T;
 
