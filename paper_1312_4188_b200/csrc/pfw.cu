@@ -189,6 +189,7 @@ struct ScanParams {
     int64_t lo, hi;            // rule window [lo, hi) in table positions (masking, stages)
     int64_t win_lo, win_hi;    // the same window in original rule indices (comparisons)
     const uint32_t *orig;      // table position -> original rule index (null = identity)
+    int chain;                 // table is a protocol-split chain (protocol-free encoding)
     int64_t s_begin, s_end;    // this pass: stage starts s_begin, s_begin+STAGE, ... < s_end
     const uint4 *pkts;         // 16-byte records, or null: read the columns in `cols`
     PacketCols cols;
@@ -226,7 +227,7 @@ __device__ __forceinline__ uint32_t sub_fma(uint32_t x, uint32_t one, uint32_t n
 
 // Fast-path test.  FMA: IP subtractions as IMAD with a runtime 1 (FMA-heavy
 // pipe) instead of IADD3 (ALU pipe, the bottleneck).
-template <bool FMA>
+template <bool FMA, bool CH = false>
 __device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src, uint32_t dst, float A,
                                           float A2, float B, uint32_t one) {
     uint32_t a, b;
@@ -238,9 +239,11 @@ __device__ __forceinline__ bool rule_test(const uint32_t (&r)[NF], uint32_t src,
         b = dst + r[F_DST_NLO];
     }
     // A holds D = A - A2 (packet precompute): dA = D*c1 + (A2 - loA) is
-    // A - loA for c1 = 1 and A2 - loA for c1 = 0, exactly (integers < 2^24)
+    // A - loA for c1 = 1 and A2 - loA for c1 = 0, exactly (integers < 2^24).
+    // CH (protocol-split chain tables): every rule is encoded protocol-free
+    // (c1 = 0), so dA = A2 - loA is one FADD.
     const float x = A2 + __uint_as_float(r[F_A_NLO]);
-    const float dA = fmaf(A, __uint_as_float(r[F_A_C1]), x);
+    const float dA = CH ? x : fmaf(A, __uint_as_float(r[F_A_C1]), x);
     const float dB = B + __uint_as_float(r[F_B_NLO]);
     return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
            (__float_as_uint(dB) <= r[F_B_W]);
@@ -274,7 +277,7 @@ __device__ __forceinline__ bool port_test(const uint32_t (&r)[NF], float A, floa
 // different instruction sequence so the compiler cannot CSE it with the fast
 // path and keep KS predicates / values alive across the vote.  Exact for the
 // same reasons: all float operands are integers < 2^24 and c1, c2 are 0 or 1.
-template <bool FMA>
+template <bool FMA, bool CH = false>
 __device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t src, uint32_t dst,
                                                float A, float A2, float B, uint32_t one) {
     uint32_t a, b;
@@ -285,8 +288,9 @@ __device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t
         a = sub_fma(src, one, r[F_SRC_NLO]);
         b = sub_fma(dst, one, r[F_DST_NLO]);
     }
-    const float dA = __fadd_rn(__fmul_rn(A, __uint_as_float(r[F_A_C1])),
-                               __fsub_rn(A2, -__uint_as_float(r[F_A_NLO])));
+    const float dA = CH ? __fsub_rn(A2, -__uint_as_float(r[F_A_NLO]))
+                        : __fadd_rn(__fmul_rn(A, __uint_as_float(r[F_A_C1])),
+                                    __fsub_rn(A2, -__uint_as_float(r[F_A_NLO])));
     const float dB = __fsub_rn(B, -__uint_as_float(r[F_B_NLO]));
     return (a <= r[F_SRC_W]) & (b <= r[F_DST_W]) & (__float_as_uint(dA) <= r[F_A_W]) &
            (__float_as_uint(dB) <= r[F_B_W]);
@@ -294,12 +298,12 @@ __device__ __forceinline__ bool rule_test_slow(const uint32_t (&r)[NF], uint32_t
 
 // Stage-local first match among rows [J0, J1) for one packet (some lane hit
 // there): rows in rule order, one ballot each, stop at the first non-empty.
-template <int KS, int J0, int J1, bool FMA>
+template <int KS, int J0, int J1, bool FMA, bool CH>
 __device__ __forceinline__ unsigned rows_first(const uint32_t (&r)[KS][NF], uint32_t src, uint32_t dst,
                                                float A, float A2, float B, uint32_t one) {
 #pragma unroll
     for (int j = J0; j < J1; j++) {
-        const unsigned b = __ballot_sync(0xFFFFFFFFu, rule_test_slow<FMA>(r[j], src, dst, A, A2, B, one));
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, rule_test_slow<FMA, CH>(r[j], src, dst, A, A2, B, one));
         if (b) return (unsigned)(j * 32 + __ffs(b) - 1);
     }
     return 0xFFFFFFFFu;  // unreachable when the caller's vote hit
@@ -307,18 +311,18 @@ __device__ __forceinline__ unsigned rows_first(const uint32_t (&r)[KS][NF], uint
 
 // Slow path: the stage hit; the half-stage accumulators say which half holds
 // the first match, so at most KS/2 rows are re-evaluated.
-template <int KS, bool FMA>
+template <int KS, bool FMA, bool CH>
 __device__ __forceinline__ unsigned stage_first(const uint32_t (&r)[KS][NF], bool accA, uint32_t src,
                                                 uint32_t dst, float A, float A2, float B, uint32_t one) {
-    if (__any_sync(0xFFFFFFFFu, accA)) return rows_first<KS, 0, KS / 2, FMA>(r, src, dst, A, A2, B, one);
-    return rows_first<KS, KS / 2, KS, FMA>(r, src, dst, A, A2, B, one);
+    if (__any_sync(0xFFFFFFFFu, accA)) return rows_first<KS, 0, KS / 2, FMA, CH>(r, src, dst, A, A2, B, one);
+    return rows_first<KS, KS / 2, KS, FMA, CH>(r, src, dst, A, A2, B, one);
 }
 
 // One warp, P live packets of the tile (warp-uniform), one stage of KS rows in
 // registers: the fast path ORs each packet's row results into two half-stage
 // accumulators; a packet whose stage hit locates its first match with the
 // slow path and records it.  P independent packets = P-fold ILP.
-template <int P, int KS, bool FMA, bool HALF>
+template <int P, int KS, bool FMA, bool HALF, bool CH>
 __device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const int (&q)[P],
                                            const uint4 *s_pk, const uint32_t *s_pr, uint32_t *s_first,
                                            int64_t s, uint32_t one, int lane) {
@@ -341,7 +345,7 @@ __device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const in
     for (int j = 0; j < KS; j++)
 #pragma unroll
         for (int k = 0; k < P; k++) {
-            const bool m = rule_test<FMA>(r[j], v[k].x, v[k].y, a[k], c[k], b[k], one);
+            const bool m = rule_test<FMA, CH>(r[j], v[k].x, v[k].y, a[k], c[k], b[k], one);
             if (HALF && j >= KS / 2) hi[k] |= m; else lo[k] |= m;
         }
     // one vote for the whole group; per-packet votes only when it hit
@@ -353,8 +357,8 @@ __device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const in
     for (int k = 0; k < P; k++) {
         if (__any_sync(0xFFFFFFFFu, lo[k] | hi[k])) {
             const unsigned f =
-                HALF ? stage_first<KS, FMA>(r, lo[k], v[k].x, v[k].y, a[k], c[k], b[k], one)
-                     : rows_first<KS, 0, KS, FMA>(r, v[k].x, v[k].y, a[k], c[k], b[k], one);
+                HALF ? stage_first<KS, FMA, CH>(r, lo[k], v[k].x, v[k].y, a[k], c[k], b[k], one)
+                     : rows_first<KS, 0, KS, FMA, CH>(r, v[k].x, v[k].y, a[k], c[k], b[k], one);
             PFW_CHECK(f < (unsigned)KS * 32u && q[k] >= 0);
             if (lane == 0) s_first[q[k]] = (uint32_t)(s + f);
         }
@@ -434,7 +438,7 @@ __device__ __forceinline__ void issue_stage(const ScanParams &p, int64_t s, uint
 template <int KS>
 constexpr int min_ctas() { return KS <= 4 ? 3 : 2; }
 
-template <int KS, int MODE, bool FMA, bool SC>
+template <int KS, int MODE, bool FMA, bool SC, bool CH>
 __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int TMAX = p.tile;  // shared-memory capacity in packets
@@ -559,21 +563,21 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
                     int qq[GROUP];
 #pragma unroll
                     for (int k = 0; k < GROUP; k++) qq[k] = live[i + k * NWARPS];
-                    scan_group<GROUP, KS, FMA, GROUP_HALF>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    scan_group<GROUP, KS, FMA, GROUP_HALF, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
                 }
                 if (GROUP > 3 && i + NWARPS < nlive) {
                     const int qq[2] = {live[i], live[i + NWARPS]};
-                    scan_group<2, KS, FMA, true>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    scan_group<2, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
                     i += 2 * NWARPS;
                 }
                 if (i + NWARPS < nlive) {
                     const int qq[2] = {live[i], live[i + NWARPS]};
-                    scan_group<2, KS, FMA, true>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    scan_group<2, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
                     i += 2 * NWARPS;
                 }
                 if (i < nlive) {
                     const int qq[1] = {live[i]};
-                    scan_group<1, KS, FMA, true>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    scan_group<1, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
                 }
             } else {
                 // short-circuit variant (off by default): rows in rule order; per
@@ -966,10 +970,10 @@ std::vector<int64_t> plan_passes(int64_t lo, int64_t hi, int stage) {
     return b;
 }
 
-template <int KS, int MODE, bool FMA, bool SC>
+template <int KS, int MODE, bool FMA, bool SC, bool CH = false>
 int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t st) {
     const size_t sm = smem_bytes(p0.tile, KS);
-    auto kern = scan_kernel<KS, MODE, FMA, SC>;
+    auto kern = scan_kernel<KS, MODE, FMA, SC, CH>;
     int maxsm = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
     if (sm > (size_t)maxsm)
@@ -1016,6 +1020,8 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
 
 template <int MODE, bool FMA, bool SC>
 int launch_scan_ks(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t st) {
+    // protocol-split chain tables: the protocol-free variant (default KS / FMA / no SC)
+    if (p.chain && g_ks == 8 && FMA && !SC) return launch_scan_t<8, MODE, true, false, true>(h, p, ws, st);
     switch (g_ks) {
         case 2: return launch_scan_t<2, MODE, FMA, SC>(h, p, ws, st);
         case 4: return launch_scan_t<4, MODE, FMA, SC>(h, p, ws, st);
@@ -1128,6 +1134,7 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cuda
         p.rules = ch.d_rules;
         p.rpad = ch.rpad;
         p.orig = ch.d_orig;
+        p.chain = 1;
         p.win_lo = p0.lo;
         p.win_hi = p0.hi;
         p.lo = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.lo) - ch.orig.begin());
@@ -1299,6 +1306,18 @@ int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32
                 const int64_t r = k < ch.n ? (int64_t)ch.orig[(size_t)k] : n;  // n..: never-match pad row
                 for (int f = 0; f < NF; f++) tab[(size_t)f * ch.rpad + k] = host[(size_t)f * h->rpad + r];
                 orig_pad[(size_t)k] = k < ch.n ? ch.orig[(size_t)k] : 0u;
+                // every packet scanned against this chain has protocol v, and
+                // every rule in it is ANY or v: the protocol test is implied, so
+                // concrete rules take the protocol-free sport form (A2 word)
+                const bool live = k < ch.n && tab[(size_t)F_B_NLO * ch.rpad + k] != NEVER_B_NLO;
+                if (live && proto[r] != 0) {
+                    const uint32_t slo = sport_lo[r], shi = sport_hi[r];
+                    const uint32_t loA = slo << 8, widA = ((shi << 8) | 0xFFu) - loA;
+                    tab[(size_t)F_A_C1 * ch.rpad + k] = f2u(0.f);
+                    tab[(size_t)F_A_C2 * ch.rpad + k] = f2u(1.f);
+                    tab[(size_t)F_A_NLO * ch.rpad + k] = f2u(-(float)loA);
+                    tab[(size_t)F_A_W * ch.rpad + k] = f2u((float)widA);
+                }
             }
             e = cudaMalloc(&ch.d_rules, tab.size() * 4);
             if (e == cudaSuccess) e = cudaMalloc(&ch.d_orig, orig_pad.size() * 4);
