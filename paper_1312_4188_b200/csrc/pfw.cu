@@ -318,6 +318,11 @@ __device__ __forceinline__ unsigned stage_first(const uint32_t (&r)[KS][NF], boo
     return rows_first<KS, KS / 2, KS, FMA, CH>(r, src, dst, A, A2, B, one);
 }
 
+// protocol of tile slot i from the shared-memory packet words (B = dport<<8 | proto)
+__device__ __forceinline__ uint32_t s_pk_proto(const uint4 *, const uint32_t *s_pr, int i) {
+    return ((uint32_t)__uint_as_float(s_pr[i])) & 0xFFu;
+}
+
 // One warp, P live packets of the tile (warp-uniform), one stage of KS rows in
 // registers: the fast path ORs each packet's row results into two half-stage
 // accumulators; a packet whose stage hit locates its first match with the
@@ -362,6 +367,45 @@ __device__ __forceinline__ void scan_group(const uint32_t (&r)[KS][NF], const in
             PFW_CHECK(f < (unsigned)KS * 32u && q[k] >= 0);
             if (lane == 0) s_first[q[k]] = (uint32_t)(s + f);
         }
+    }
+}
+
+#ifndef PFW_GROUP_HALF
+#define PFW_GROUP_HALF 0
+#endif
+#ifndef PFW_GROUP
+#define PFW_GROUP 3
+#endif
+
+// One stage over this warp's share of the live list: groups of GROUP packets
+// (independent chains for ILP, loop overhead shared by the group).  CH: the
+// sport/proto test is the one-FADD protocol-free/-fixed form.
+template <int KS, bool FMA, bool CH>
+__device__ __forceinline__ void scan_live(const uint32_t (&r)[KS][NF], const uint16_t *live, int nlive,
+                                          int warp, const uint4 *s_pk, const uint32_t *s_pr,
+                                          uint32_t *s_first, int64_t s, uint32_t one, int lane) {
+    constexpr int NW = 8;  // warps per CTA (BLOCK / 32)
+    constexpr int G = PFW_GROUP;
+    int i = warp;
+    for (; i + (G - 1) * NW < nlive; i += G * NW) {
+        int qq[G];
+#pragma unroll
+        for (int k = 0; k < G; k++) qq[k] = live[i + k * NW];
+        scan_group<G, KS, FMA, (PFW_GROUP_HALF != 0), CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+    }
+    if (G > 3 && i + NW < nlive) {
+        const int qq[2] = {live[i], live[i + NW]};
+        scan_group<2, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+        i += 2 * NW;
+    }
+    if (i + NW < nlive) {
+        const int qq[2] = {live[i], live[i + NW]};
+        scan_group<2, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+        i += 2 * NW;
+    }
+    if (i < nlive) {
+        const int qq[1] = {live[i]};
+        scan_group<1, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
     }
 }
 
@@ -451,7 +495,7 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
     uint16_t *s_liveB = s_liveA + TMAX;
     uint64_t *s_bar = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(s_liveB + TMAX) + 15) & ~uintptr_t(15));
-    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2]=live counts, [1]=tile
+    int *s_misc = reinterpret_cast<int *>(s_bar + 2);  // [0],[2] live counts, [1] tile, [3],[4] proto min/max
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t one = p.one;
@@ -522,7 +566,38 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
             s_first[i] = PFW_NO_MATCH;
             s_liveA[i] = (uint16_t)i;
         }
+        // is the tile protocol-uniform?  (warp min/max, one smem atomic per warp)
+        if (!CH && !SC) {
+            if (tid == 0) {
+                s_misc[3] = 255;
+                s_misc[4] = 0;
+            }
+            __syncthreads();
+            unsigned pmin = 255u, pmax = 0u;
+            for (int i = tid; i < cnt; i += BLOCK) {
+                const uint32_t pr = s_pk_proto(s_pk, s_pr, i);
+                pmin = min(pmin, pr);
+                pmax = max(pmax, pr);
+            }
+            pmin = __reduce_min_sync(0xFFFFFFFFu, pmin);
+            pmax = __reduce_max_sync(0xFFFFFFFFu, pmax);
+            if (lane == 0) {
+                atomicMin(&s_misc[3], (int)pmin);
+                atomicMax(&s_misc[4], (int)pmax);
+            }
+        }
         __syncthreads();
+        // (the short-circuit variant keeps the generic encoding)
+        const bool tile_uniform = !CH && !SC && s_misc[3] == s_misc[4];
+        const uint32_t tile_proto = (uint32_t)s_misc[3];
+        if (tile_uniform) {
+            // A2 slot <- the protocol-major word A = D + A2 (exact integers)
+            for (int i = tid; i < cnt; i += BLOCK) {
+                const uint4 v = s_pk[i];
+                s_pk[i].w = __float_as_uint(__uint_as_float(v.z) + __uint_as_float(v.w));
+            }
+            __syncthreads();
+        }
 
         int nlive = any_rules ? cnt : 0;
         uint16_t *live = s_liveA, *live2 = s_liveB;
@@ -557,27 +632,23 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
             // branch below is warp-uniform too).
             int i = warp;
             if (!SC) {
-                // groups of GROUP packets: independent chains for ILP, loop
-                // overhead shared by the group
-                for (; i + (GROUP - 1) * NWARPS < nlive; i += GROUP * NWARPS) {
-                    int qq[GROUP];
+                if (CH || !tile_uniform) {
+                    scan_live<KS, FMA, CH>(r, live, nlive, warp, s_pk, s_pr, s_first, s, one, lane);
+                } else {
+                    // every packet of the tile has protocol tile_proto: rewrite the
+                    // ANY rules' sport test into the protocol-major form for that
+                    // protocol (concrete rules already have it), so every rule --
+                    // still tested against every packet -- needs one FADD
 #pragma unroll
-                    for (int k = 0; k < GROUP; k++) qq[k] = live[i + k * NWARPS];
-                    scan_group<GROUP, KS, FMA, GROUP_HALF, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
-                }
-                if (GROUP > 3 && i + NWARPS < nlive) {
-                    const int qq[2] = {live[i], live[i + NWARPS]};
-                    scan_group<2, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
-                    i += 2 * NWARPS;
-                }
-                if (i + NWARPS < nlive) {
-                    const int qq[2] = {live[i], live[i + NWARPS]};
-                    scan_group<2, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
-                    i += 2 * NWARPS;
-                }
-                if (i < nlive) {
-                    const int qq[1] = {live[i]};
-                    scan_group<1, KS, FMA, true, CH>(r, qq, s_pk, s_pr, s_first, s, one, lane);
+                    for (int j = 0; j < KS; j++) {
+                        if (r[j][F_A_C1] == 0u) {  // c1 = +0.0f: ANY rule, A2 encoding
+                            const uint32_t slo = ((uint32_t)(-__uint_as_float(r[j][F_A_NLO]))) >> 8;
+                            const uint32_t shi = (((uint32_t)__uint_as_float(r[j][F_A_W])) + (slo << 8)) >> 8;
+                            r[j][F_A_NLO] = __float_as_uint(-(float)((tile_proto << 16) | slo));
+                            r[j][F_A_W] = __float_as_uint((float)(shi - slo));
+                        }
+                    }
+                    scan_live<KS, FMA, true>(r, live, nlive, warp, s_pk, s_pr, s_first, s, one, lane);
                 }
             } else {
                 // short-circuit variant (off by default): rows in rule order; per

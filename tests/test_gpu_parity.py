@@ -475,3 +475,30 @@ def test_scan_range_columns_device_and_host():
     np.testing.assert_array_equal(v, np.where(want >= 0, rules["action_accept"][np.maximum(want, 0)], False))
     comps = oracle.sequential_comparisons(want, 2048)
     assert st.tolist() == [int(comps.sum()), int(comps.max())]
+
+
+# --------------------------------------------- protocol-uniform tile fast path
+
+@pytest.mark.parametrize("proto", [1, 6, 17, 47, 0, 255])
+def test_protocol_uniform_tiles(proto):
+    """Every packet of a tile has the same protocol -> ANY rules are rewritten
+    into the protocol-major form for it at stage load (no rule skipped)."""
+    rules = oracle.gen_ruleset(1500, 23, wp=0.35)
+    rules["proto"][::13] = 47
+    rules["proto"][::29] = 255
+    pk = oracle.gen_traffic_uniform(6000, 24, proto=max(proto, 1))
+    pk["proto"][:] = proto
+    c = compiled(rules)
+    for lo, hi in ((0, 1500), (77, 1400)):
+        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+
+
+def test_mixed_and_uniform_tiles_in_one_batch():
+    _native.set_tuning("tile", 256)
+    rules = oracle.gen_ruleset(900, 25, wp=0.35)
+    pk = oracle.gen_traffic_uniform(256 * 12, 26)
+    pk["proto"][256 * 3:256 * 4] = 17          # a whole UDP tile
+    pk["proto"][256 * 6 + 5] = 1               # one ICMP packet in a TCP tile
+    pk["proto"][256 * 9:256 * 10:2] = 17       # an interleaved tile
+    np.testing.assert_array_equal(compiled(rules).scan_range(dev_pkts(pk), 0, 900),
+                                  oracle.scan_range(rules, pk, 0, 900))
