@@ -203,6 +203,7 @@ def main() -> int:
     ap.add_argument("--e2e-chunk", type=int, default=1 << 22, help="packets per H2D/scan/D2H chunk")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--sc", type=int, default=-1, help="warp-level short-circuit of the port tests (0/1)")
+    ap.add_argument("--bucket", type=int, default=-1, help="group large batches by protocol (0/1)")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--first-pass", type=int, default=-1, help="rules in the first pass (0 = single pass)")
     ap.add_argument("--proto-split", action="store_true",
@@ -246,6 +247,8 @@ def main() -> int:
         _native.set_tuning("ks", args.ks)
     if args.sc >= 0:
         _native.set_tuning("short_circuit", args.sc)
+    if args.bucket >= 0:
+        _native.set_tuning("bucket", args.bucket)
     if args.tile:
         _native.set_tuning("tile", args.tile)
     if args.first_pass >= 0:

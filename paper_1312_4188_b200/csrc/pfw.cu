@@ -125,6 +125,8 @@ constexpr int E2E_SLOTS = 3;
 constexpr int MAX_CHAINS = 257;
 int g_proto_split = 0;   // opt-in: scan protocol-split rule chains
 int g_short_circuit = 0; // warp-level short-circuit of the port tests (SC variant; measured slower)
+int g_bucket = 1;        // group large batches by protocol (protocol-uniform tiles)
+int64_t g_bucket_min = 1 << 20;  // ... from this many packets on
 
 }  // namespace
 
@@ -197,6 +199,8 @@ struct ScanParams {
     const uint32_t *in_ids;    // live packet ids of this pass (null = 0..n-1)
     const unsigned int *in_count;  // device count of in_ids (null = n)
     const unsigned int *bucket_base;  // pass 0 of a chain scan: in_ids offset (device)
+    const int *bk_single;             // pass 0 of a bucketed scan: only non-empty bucket, or -1
+    int bk_index;                     // this launch's bucket
     const uint32_t *in_ids0;          // pass-0 input of a launch (null = identity)
     const unsigned int *in_count0;
     uint32_t *out_ids;         // survivors of this pass (null = final pass)
@@ -501,8 +505,14 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
     const uint32_t one = p.one;
     constexpr int STAGE = 32 * KS;
     const bool final_pass = p.out_ids == nullptr;
-    const int64_t count = p.in_count ? (int64_t)*p.in_count : p.n;
+    int64_t count = p.in_count ? (int64_t)*p.in_count : p.n;
     const uint32_t *in_ids = p.in_ids ? p.in_ids + (p.bucket_base ? *p.bucket_base : 0u) : nullptr;
+    if (p.bk_single && *p.bk_single >= 0) {
+        // single-protocol batch: the bucket list was not written; the only
+        // non-empty bucket is the whole batch in order
+        in_ids = nullptr;
+        count = (*p.bk_single == p.bk_index) ? p.n : 0;
+    }
     // Tile size for this pass: the full capacity when there is enough work;
     // otherwise sized so the tile count is a whole number of waves of the
     // persistent grid (small batches and late passes carry few packets: a
@@ -808,20 +818,28 @@ __global__ void __launch_bounds__(BK_BLOCK) bucket_count_kernel(const uint4 *pkt
         if (hist[c]) atomicAdd(&bc[c], hist[c]);
 }
 
-__global__ void bucket_prefix_kernel(int nchains, unsigned *bc) {
+__global__ void bucket_prefix_kernel(int nchains, unsigned *bc, int *single) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         unsigned acc = 0;
+        int nonempty = 0, last = -1;
         for (int c = 0; c < nchains; c++) {
             bc[MAX_CHAINS + c] = acc;  // base
             bc[2 * MAX_CHAINS + c] = 0;  // cursor
             acc += bc[c];
+            if (bc[c]) {
+                nonempty++;
+                last = c;
+            }
         }
+        if (single) *single = nonempty == 1 ? last : -1;
     }
 }
 
 __global__ void __launch_bounds__(BK_BLOCK) bucket_scatter_kernel(const uint4 *pkts, const uint8_t *proto_col,
                                                                   int64_t n, const uint8_t *lut, int nchains,
-                                                                  unsigned *bc, uint32_t *ids) {
+                                                                  unsigned *bc, uint32_t *ids,
+                                                                  const int *single) {
+    if (single && *single >= 0) return;  // one bucket: scans read the batch in order
     __shared__ unsigned hist[MAX_CHAINS], gbase[MAX_CHAINS];
     for (int c = threadIdx.x; c < nchains; c += BK_BLOCK) hist[c] = 0;
     __syncthreads();
@@ -1078,6 +1096,7 @@ int launch_scan_t(pfw_ruleset *h, const ScanParams &p0, ScanWs &ws, cudaStream_t
         p.in_ids = k == 0 ? p0.in_ids0 : ws.ids + (size_t)((k - 1) & 1) * ws.cap;
         p.in_count = k == 0 ? p0.in_count0 : ws.ctr + 2 * (k - 1) + 1;
         p.bucket_base = k == 0 ? p0.bucket_base : nullptr;
+        p.bk_single = k == 0 ? p0.bk_single : nullptr;
         const bool last = k == npass - 1;
         p.out_ids = last ? nullptr : ws.ids + (size_t)(k & 1) * ws.cap;
         p.out_count = last ? nullptr : ws.ctr + 2 * k + 1;
@@ -1115,7 +1134,7 @@ int launch_scan_sc(pfw_ruleset *h, const ScanParams &p, ScanWs &ws, cudaStream_t
 }
 
 int launch_mode(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st);
-int launch_split(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st);
+int launch_split(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaStream_t st, bool chains);
 
 int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                 uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
@@ -1162,7 +1181,12 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
         p.scatter = peer->scatter;
     }
     ScanWs &w = ws ? *ws : h->ws;
-    if (g_proto_split && !h->chains.empty() && lo < hi) return launch_split(h, mode, p, w, st);
+    if (g_proto_split && !h->chains.empty() && lo < hi) return launch_split(h, mode, p, w, st, true);
+    // large batches are grouped by protocol first so that tiles are
+    // protocol-uniform (the one-FADD sport test); single-protocol batches skip
+    // the scatter on the device
+    if (g_bucket && !h->chains.empty() && lo < hi && n >= g_bucket_min && !g_short_circuit)
+        return launch_split(h, mode, p, w, st, false);
     return launch_mode(h, mode, p, w, st);
 }
 
@@ -1177,7 +1201,8 @@ int launch_mode(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaSt
 // Protocol-split scan: group the packets by rule chain on the device, then
 // run the multi-pass scan of each chain over its bucket (empty buckets exit
 // immediately; counts stay on the device, no host sync).
-int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cudaStream_t st) {
+int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cudaStream_t st,
+                 bool chains) {
     const int nch = (int)h->chains.size();
     const int64_t n = p0.n;
     if (h->bucket_cap < n) {
@@ -1187,35 +1212,38 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cuda
         CUDA_TRY(cudaMalloc(&h->d_bucket, (size_t)n * sizeof(uint32_t)));
         h->bucket_cap = n;
     }
-    if (!h->d_bcount) CUDA_TRY(cudaMalloc(&h->d_bcount, 3 * MAX_CHAINS * sizeof(unsigned)));
+    if (!h->d_bcount) CUDA_TRY(cudaMalloc(&h->d_bcount, (3 * MAX_CHAINS + 1) * sizeof(unsigned)));
+    int *d_single = reinterpret_cast<int *>(h->d_bcount + 3 * MAX_CHAINS);
     CUDA_TRY(cudaMemsetAsync(h->d_bcount, 0, MAX_CHAINS * sizeof(unsigned), st));
     const unsigned nb = (unsigned)((n + BK_BLOCK * BK_PER_THREAD - 1) / (BK_BLOCK * BK_PER_THREAD));
     bucket_count_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, h->d_bcount);
-    bucket_prefix_kernel<<<1, 32, 0, st>>>(nch, h->d_bcount);
+    bucket_prefix_kernel<<<1, 32, 0, st>>>(nch, h->d_bcount, d_single);
     bucket_scatter_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, h->d_bcount,
-                                                  h->d_bucket);
+                                                  h->d_bucket, d_single);
     CUDA_TRY(cudaGetLastError());
     g_launches += 3;
     // bucket c's ids start at base[c]; its count is bc[c].  The base is only
     // known on the device, so each chain scan reads its ids through a
     // device-side pointer computed by a tiny kernel into the ws pointer slot.
     for (int c = 0; c < nch; c++) {
-        const pfw_ruleset::Chain &ch = h->chains[(size_t)c];
         ScanParams p = p0;
-        p.rules = ch.d_rules;
-        p.rpad = ch.rpad;
-        p.orig = ch.d_orig;
-        p.chain = 1;
-        p.win_lo = p0.lo;
-        p.win_hi = p0.hi;
-        p.lo = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.lo) - ch.orig.begin());
-        p.hi = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.hi) - ch.orig.begin());
         p.bucket_base = h->d_bcount + MAX_CHAINS + c;
         p.in_ids0 = h->d_bucket;
         p.in_count0 = h->d_bcount + c;
-        if (p.lo >= p.hi) {
-            p.lo = p.hi;
-        }
+        p.bk_single = d_single;
+        p.bk_index = c;
+        if (chains) {  // protocol-split: this bucket scans its chain table
+            const pfw_ruleset::Chain &ch = h->chains[(size_t)c];
+            p.rules = ch.d_rules;
+            p.rpad = ch.rpad;
+            p.orig = ch.d_orig;
+            p.chain = 1;
+            p.win_lo = p0.lo;
+            p.win_hi = p0.hi;
+            p.lo = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.lo) - ch.orig.begin());
+            p.hi = (int64_t)(std::lower_bound(ch.orig.begin(), ch.orig.end(), (uint32_t)p0.hi) - ch.orig.begin());
+            if (p.lo >= p.hi) p.lo = p.hi;
+        }  // else: protocol bucketing only -- the full table, protocol-uniform tiles
         int rc = launch_mode(h, mode, p, w, st);
         if (rc != PFW_OK) return rc;
     }
@@ -1273,6 +1301,11 @@ int pfw_set_tuning(const char *key, int64_t value) {
         g_first_pass = (int)value;
     } else if (!strcmp(key, "short_circuit")) {
         g_short_circuit = value != 0;
+    } else if (!strcmp(key, "bucket")) {
+        g_bucket = value != 0;
+    } else if (!strcmp(key, "bucket_min")) {
+        if (value < 0) return set_err(PFW_ERR_INVALID, "bucket_min must be >= 0");
+        g_bucket_min = value;
     } else if (!strcmp(key, "proto_split")) {
         g_proto_split = value != 0;
     } else if (!strcmp(key, "force_imad")) {

@@ -37,7 +37,7 @@ def compiled(rules: dict) -> pfw.CompiledRuleset:
 def _reset_tuning():
     yield
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
-                 ("proto_split", 0), ("short_circuit", 0)):
+                 ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20)):
         _native.set_tuning(k, v)
 
 
@@ -502,3 +502,35 @@ def test_mixed_and_uniform_tiles_in_one_batch():
     pk["proto"][256 * 9:256 * 10:2] = 17       # an interleaved tile
     np.testing.assert_array_equal(compiled(rules).scan_range(dev_pkts(pk), 0, 900),
                                   oracle.scan_range(rules, pk, 0, 900))
+
+
+@pytest.mark.parametrize("bucket_min", [0, 1 << 20])
+def test_protocol_bucketing_mixed_traffic(bucket_min):
+    """Mixed-protocol batches are grouped by protocol on the device so tiles are
+    protocol-uniform; results identical, with or without the grouping."""
+    _native.set_tuning("bucket_min", bucket_min)
+    rules = oracle.gen_ruleset(2500, 31, wp=0.3)
+    rules["proto"][::17] = 47
+    n = 1_200_000 if bucket_min else 40_000
+    parts = [oracle.gen_traffic_uniform(n // 5, 40 + k, proto=pr) for k, pr in enumerate((6, 17, 1, 47, 99))]
+    pk = {f: np.concatenate([pt[f] for pt in parts]) for f in PKT_FIELDS}
+    perm = np.random.default_rng(1).permutation(len(pk["proto"]))
+    pk = {f: v[perm] for f, v in pk.items()}
+    c = compiled(rules)
+    p = dev_pkts(pk)
+    want = oracle.scan_range(rules, pk, 0, 2500)
+    np.testing.assert_array_equal(c.scan_range(p, 0, 2500), want)
+    _native.set_tuning("bucket", 0)
+    np.testing.assert_array_equal(c.scan_range(p, 0, 2500), want)
+    _native.set_tuning("bucket", 1)
+    # function-parallel accumulate through the bucketed path
+    res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=3)).run_arrays(c, p)
+    first, comps, total, mx = oracle.engine_run(rules, pk, "function", 3)
+    np.testing.assert_array_equal(res.first, first)
+    np.testing.assert_array_equal(res.comparisons, comps)
+
+
+@pytest.mark.parametrize("name,rn,tn", SCANS)
+def test_bucketed_scan_matches_reference_golden(name, rn, tn):
+    _native.set_tuning("bucket_min", 0)
+    test_scan_matches_reference_golden(name, rn, tn)
