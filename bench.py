@@ -201,6 +201,9 @@ def main() -> int:
     ap.add_argument("--graph", action="store_true",
                     help="capture one step (all pass launches) in a CUDA graph and replay it")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 22, help="packets per H2D/scan/D2H chunk")
+    ap.add_argument("--algo", type=int, default=-1,
+                    help="0 auto (match sets when built), 1 rule-by-rule scan, 2 match sets")
+    ap.add_argument("--ms-words", type=int, default=0, help="match-set scan: words per lane per step (1, 2, 4)")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--sc", type=int, default=-1, help="warp-level short-circuit of the port tests (0/1)")
     ap.add_argument("--bucket", type=int, default=-1, help="group large batches by protocol (0/1)")
@@ -243,6 +246,10 @@ def main() -> int:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if args.algo >= 0:
+        _native.set_tuning("algo", args.algo)
+    if args.ms_words:
+        _native.set_tuning("ms_words", args.ms_words)
     if args.ks:
         _native.set_tuning("ks", args.ks)
     if args.sc >= 0:

@@ -59,10 +59,12 @@ int pfw_device_count(void);
 /* Ruleset packing + upload.  Replaces CompiledRuleset.__init__
  * (classifier.py:120-134): takes exactly its ten SoA columns (proto u8 with
  * ANY = 0, CIDR base/mask u32, inclusive port lo/hi u16, action_accept u8)
- * and uploads the device form (range-test SoA) once. Rules
- * whose base has host bits outside the mask, or whose port range is inverted,
- * can never match under the reference predicate (model.py:222-230) and are
- * packed as never-matching.  n_rules may be 0. */
+ * and uploads the device forms once: the range-test SoA of the rule-by-rule
+ * scan and, within the memory budget, the per-field match sets (interval
+ * bitmaps).  Rules whose base has host bits outside the mask, or
+ * whose port range is inverted, can never match under the reference
+ * predicate (model.py:222-230) and are packed as never-matching.  n_rules may
+ * be 0. */
 int pfw_ruleset_create(int device, int64_t n_rules, const uint8_t *proto,
                        const uint32_t *src_base, const uint32_t *src_mask,
                        const uint16_t *sport_lo, const uint16_t *sport_hi,
@@ -72,6 +74,9 @@ int pfw_ruleset_create(int device, int64_t n_rules, const uint8_t *proto,
 int pfw_ruleset_destroy(pfw_ruleset_t h);
 int64_t pfw_ruleset_size(pfw_ruleset_t h);
 int pfw_ruleset_device(pfw_ruleset_t h);
+/* Device bytes of the ruleset's match sets; 0 when they were not built (the
+ * ruleset then scans rule by rule). */
+int64_t pfw_ruleset_matchset_bytes(pfw_ruleset_t h);
 
 /* Host packet packing.  Replaces PacketArrays.from_packets
  * (classifier.py:75-83) for column input: writes n 16-byte records. */
@@ -200,7 +205,12 @@ int pfw_parse_traffic(const char *buf, int64_t len, int64_t cap, int64_t *ids, v
 int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t *verdict, int64_t n,
                        char *out, int64_t cap, int64_t *written);
 
-/* Launch-count / tuning introspection (bench + tests). */
+/* Launch-count / tuning introspection (bench + tests).  Tuning keys include
+ * "algo" (0 auto: match sets when built, 1 rule-by-rule scan, 2 match sets),
+ * "matchset" (build match sets at ruleset creation, default 1),
+ * "matchset_budget_mb" (0 = a quarter of free device memory), "ms_words",
+ * and the rule-scan options "ks", "tile", "first_pass", "bucket",
+ * "bucket_min", "proto_split", "short_circuit", "force_imad", "ctas_per_sm". */
 int64_t pfw_launch_count(void);
 int pfw_set_tuning(const char *key, int64_t value);
 

@@ -8,6 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "pfw.cu")
 SRC_HOST = os.path.join(PKG, "csrc", "hostio.cpp")
+HEADERS = [os.path.join(PKG, "csrc", "matchset.cuh")]
 LIB = os.path.join(PKG, "libpfw.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -23,7 +24,7 @@ NVCC_FLAGS = [
 def build_native(verbose: bool = False, force: bool = False, out: str = LIB, defines=()) -> str:
     """Compile csrc/pfw.cu -> libpfw.so unless the library is newer than its sources.
     ``defines`` (e.g. ["PFW_GROUP=4"]) build experiment variants into ``out``."""
-    deps = [SRC, SRC_HOST, os.path.join(ROOT, "include", "pfw.h"), os.path.abspath(__file__)]
+    deps = [SRC, SRC_HOST, *HEADERS, os.path.join(ROOT, "include", "pfw.h"), os.path.abspath(__file__)]
     if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(d) for d in deps):
         return out
     tmp = out + ".tmp"

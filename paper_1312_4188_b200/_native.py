@@ -42,6 +42,7 @@ _SIGS = {
     "pfw_ruleset_create": (_I32, [_I32, _I64] + [_P] * 10 + [ctypes.POINTER(_P)]),
     "pfw_ruleset_destroy": (_I32, [_P]),
     "pfw_ruleset_size": (_I64, [_P]),
+    "pfw_ruleset_matchset_bytes": (_I64, [_P]),
     "pfw_ruleset_device": (_I32, [_P]),
     "pfw_pack_packets_host": (_I32, [_I64, _P, _P, _P, _P, _P, _P]),
     "pfw_scan_range": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P]),

@@ -1,0 +1,498 @@
+// matchset.cuh -- the first-match scan over per-field match sets (included by
+// pfw.cu inside its anonymous namespace).
+//
+// Each rule field accepts one interval of its value domain: a CIDR block
+// [base, base | ~mask] (model.py:108-121), an inclusive port range [lo, hi]
+// (model.py:144-145), a protocol value or all of them (model.py:222-230).
+// The end points of all rules' intervals cut a field's domain into elementary
+// intervals; inside one, every rule's field test has the same outcome.  Row i
+// of a field's bitmap holds bit r = "rule r's test on this field holds on
+// interval i" (rule r at word r/32, bit r%32).  A packet's first match in the
+// window [lo, hi) (classifier.py:146-162) is the lowest set bit of the AND of
+// its four rows -- src, dst, (protocol class, sport), dport; the protocol is
+// folded into the sport rows, one block of rows per protocol class -- so the
+// scan reads 128-byte lines of 1024 rules per warp step instead of testing
+// rule by rule.  Results are the rule-by-rule scan's, bit for bit: the rows
+// are built by the reference predicate itself, evaluated on each interval's
+// first value.
+//
+// Layout in HBM (struct MatchSet): per field, rows x wp words (wp = rules/32
+// rounded up to a whole step of 128 words, 512 bytes); IP value -> interval through the
+// sorted boundaries and a 65536-entry table of boundary ranges per /16 block;
+// port value -> interval through a direct 65536-entry table; protocol ->
+// class through a 256-entry table.  The lookup tables (~1.5 MB) and the rows'
+// leading lines (where most first matches are) stay resident in L2.
+
+constexpr int MS_BLOCK = 256;
+enum { MSD_SRC = 0, MSD_DST = 1, MSD_SPORT = 2, MSD_DPORT = 3 };
+
+int g_matchset = 1;            // build match sets at ruleset creation
+int g_algo = 0;                // 0 auto (match sets when built), 1 rule-by-rule scan, 2 match sets
+int64_t g_ms_budget_mb = 0;    // device-memory budget for the tables (0 = a quarter of free memory)
+int g_ms_words = 2;            // words per lane per step: 1024 * g_ms_words rules per step (1, 2, 4)
+
+struct MsBuildArgs {
+    const uint32_t *base, *mask;  // IP fields
+    const uint16_t *lo, *hi;      // port fields
+    const uint8_t *proto;         // rule protocols (sport field)
+    const uint32_t *vals;         // first value of each elementary interval
+    const int *cls_proto;         // sport field: protocol of class c (-1: a protocol no rule names)
+    int64_t n, wp, rows, ivl;     // rules, words per row, rows, intervals per class (sport)
+    uint32_t *bits;
+};
+
+// One warp per (32-word group, row): lane = rule inside each word, one ballot
+// per word, lane k keeps word k, one coalesced 128-byte store.  Consecutive
+// warps share a word group, so the rule columns are L1 hits.
+template <int D>
+__global__ void __launch_bounds__(MS_BLOCK) ms_build_kernel(MsBuildArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    const int64_t groups = a.wp / 32;
+    for (int64_t t = gw; t < groups * a.rows; t += nw) {
+        const int64_t g = t / a.rows, row = t - g * a.rows;
+        uint32_t v;
+        int pcl = -1;
+        if (D == MSD_SPORT) {
+            const int64_t c = row / a.ivl;
+            v = __ldg(a.vals + (row - c * a.ivl));
+            pcl = __ldg(a.cls_proto + c);
+        } else {
+            v = __ldg(a.vals + row);
+        }
+        uint32_t mine = 0;
+#pragma unroll 4
+        for (int k = 0; k < 32; k++) {
+            const int64_t r = (g * 32 + k) * 32 + lane;
+            bool m = false;
+            if (r < a.n) {
+                if (D == MSD_SRC || D == MSD_DST) {
+                    m = (v & __ldg(a.mask + r)) == __ldg(a.base + r);         // model.py:119-121
+                } else {
+                    m = (uint32_t)__ldg(a.lo + r) <= v && v <= (uint32_t)__ldg(a.hi + r);  // model.py:144-145
+                    if (D == MSD_SPORT) {
+                        const int rp = __ldg(a.proto + r);                     // model.py:224-225
+                        m = m && (rp == 0 || rp == pcl);
+                    }
+                }
+            }
+            const uint32_t b = __ballot_sync(0xFFFFFFFFu, m);
+            if (lane == k) mine = b;
+        }
+        a.bits[row * a.wp + g * 32 + lane] = mine;
+    }
+}
+
+struct MsView {
+    const uint32_t *bits[4];
+    const uint32_t *ipb[2];   // src / dst boundaries
+    const uint2 *ipc[2];      // per /16 block: [first, end) boundary index
+    const uint32_t *port[2];  // sport / dport -> interval
+    const uint8_t *cls;       // protocol -> class
+    int64_t wp;
+    uint32_t sp_rows;
+};
+
+// interval of an IP: index of the last boundary <= ip (boundary 0 is 0)
+__device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint2 *c, uint32_t ip) {
+    const uint2 k = __ldg(c + (ip >> 16));
+    uint32_t lo = k.x, hi = k.y;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(b + mid) <= ip) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo - 1;
+}
+
+template <int V>
+struct MsWords;
+template <>
+struct MsWords<1> {
+    uint32_t w[1];
+    __device__ __forceinline__ void load(const uint32_t *q) { w[0] = __ldg(q); }
+};
+template <>
+struct MsWords<2> {
+    uint32_t w[2];
+    __device__ __forceinline__ void load(const uint32_t *q) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(q));
+        w[0] = v.x;
+        w[1] = v.y;
+    }
+};
+template <>
+struct MsWords<4> {
+    uint32_t w[4];
+    __device__ __forceinline__ void load(const uint32_t *q) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(q));
+        w[0] = v.x;
+        w[1] = v.y;
+        w[2] = v.z;
+        w[3] = v.w;
+    }
+};
+
+// Warps own batches of 32 packets (grid-stride).  Lane l looks up packet l's
+// four rows; then the warp walks the batch one packet at a time: per step
+// every lane reads V consecutive words of each of the packet's four rows
+// (32*V words = 1024*V rules per step, one vector load per row), ANDs them,
+// and one ballot finds the first lane holding a non-zero word.  The window
+// masks apply only on the first and last step.
+// WIN: the window is not the whole table, so the first / last step mask
+// words outside it (a whole-table scan needs no masks: bits past the last
+// rule are zero and rows are whole steps long).
+template <int MODE, int V, bool WIN>
+__global__ void __launch_bounds__(MS_BLOCK) ms_scan_kernel(ScanParams p, MsView t) {
+    constexpr uint32_t STEP = 32u * V;  // words per step
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    const int64_t n = p.n;
+    const uint32_t span = (uint32_t)(p.win_hi > p.win_lo ? p.win_hi - p.win_lo : 0);
+    const bool empty = p.lo >= p.hi;
+    const uint32_t wlo = (uint32_t)(p.lo >> 5), whi = empty ? 0u : (uint32_t)((p.hi - 1) >> 5);
+    const uint32_t cbeg = wlo & ~(STEP - 1u);                 // step-aligned start
+    const int nsteps = empty ? 0 : (int)((whi - cbeg) / STEP) + 1;
+    // this lane's masks on the first and the last step
+    uint32_t mfirst[V], mlast[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        const uint32_t w0 = cbeg + (uint32_t)lane * V + v;
+        const uint32_t wl = cbeg + (uint32_t)(nsteps - 1) * STEP + (uint32_t)lane * V + v;
+        mfirst[v] = w0 < wlo ? 0u : (w0 == wlo ? (0xFFFFFFFFu << (p.lo & 31)) : 0xFFFFFFFFu);
+        mlast[v] = wl > whi ? 0u : (wl == whi ? (0xFFFFFFFFu >> (31 - ((p.hi - 1) & 31))) : 0xFFFFFFFFu);
+    }
+    unsigned long long st_sum = 0;
+    unsigned st_max = 0;
+
+    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
+        const int64_t i = b0 + lane;
+        const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
+        // row offsets (words) of this lane's packet, at the first step
+        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+        if (i < n) {
+            uint4 v;
+            if (p.pkts) {
+                v = __ldg(p.pkts + i);
+            } else {
+                v.x = __ldg(p.cols.src + i);
+                v.y = __ldg(p.cols.dst + i);
+                v.z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
+                v.w = __ldg(p.cols.proto + i);
+            }
+            const uint32_t wp = (uint32_t)t.wp, at = cbeg;
+            o0 = ms_ip_row(t.ipb[0], t.ipc[0], v.x) * wp + at;
+            o1 = ms_ip_row(t.ipb[1], t.ipc[1], v.y) * wp + at;
+            o2 = ((uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16))) * wp + at;
+            o3 = __ldg(t.port[1] + (v.z & 0xFFFFu)) * wp + at;
+        }
+        uint32_t res = PFW_NO_MATCH;
+        // + this lane's V words of each step
+        const uint32_t *const t0 = t.bits[0] + lane * V, *const t1 = t.bits[1] + lane * V;
+        const uint32_t *const t2 = t.bits[2] + lane * V, *const t3 = t.bits[3] + lane * V;
+        for (int j = 0; j < nv; j++) {
+            const uint32_t *r0 = t0 + __shfl_sync(0xFFFFFFFFu, o0, j);
+            const uint32_t *r1 = t1 + __shfl_sync(0xFFFFFFFFu, o1, j);
+            const uint32_t *r2 = t2 + __shfl_sync(0xFFFFFFFFu, o2, j);
+            const uint32_t *r3 = t3 + __shfl_sync(0xFFFFFFFFu, o3, j);
+            for (int s = 0; s < nsteps; s++) {
+                const uint32_t so = (uint32_t)s * STEP;
+                MsWords<V> a, b, c, d;
+                a.load(r0);
+                b.load(r1);
+                c.load(r2);
+                d.load(r3);
+                r0 += STEP;
+                r1 += STEP;
+                r2 += STEP;
+                r3 += STEP;
+                uint32_t x[V], any = 0u;
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    x[v] = a.w[v] & b.w[v] & c.w[v] & d.w[v];
+                    if (WIN) {
+                        if (s == 0) x[v] &= mfirst[v];
+                        if (s == nsteps - 1) x[v] &= mlast[v];
+                    }
+                    any |= x[v];
+                }
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
+                if (bal) {
+                    // lowest set bit: first lane with a non-zero word, its
+                    // first non-zero word, that word's lowest bit
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int v = V - 1; v >= 0; v--)
+                        if (x[v]) cand = (cbeg + so + (uint32_t)lane * V + v) * 32u + (uint32_t)(__ffs(x[v]) - 1);
+                    cand = __shfl_sync(0xFFFFFFFFu, cand, __ffs(bal) - 1);
+                    if (lane == j) res = cand;
+                    break;
+                }
+            }
+        }
+        if (i < n) {
+            PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
+            emit_result<MODE>(p, (uint32_t)i, res, span, st_sum, st_max);
+        }
+    }
+    if (p.stats) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            st_sum += __shfl_xor_sync(0xFFFFFFFFu, st_sum, o);
+            st_max = max(st_max, __shfl_xor_sync(0xFFFFFFFFu, st_max, o));
+        }
+        if (lane == 0) {
+            if (st_sum) atomicAdd(&p.stats[0], st_sum);
+            if (st_max) atomicMax(&p.stats[1], (unsigned long long)st_max);
+        }
+    }
+}
+
+void ms_free(MatchSet *m) {
+    if (!m) return;
+    for (auto *b : m->d_bits)
+        if (b) cudaFree(b);
+    for (auto *b : m->d_ipb)
+        if (b) cudaFree(b);
+    for (auto *c : m->d_ipc)
+        if (c) cudaFree(c);
+    for (auto *q : m->d_port)
+        if (q) cudaFree(q);
+    if (m->d_cls) cudaFree(m->d_cls);
+    delete m;
+}
+
+// Elementary-interval boundaries of an IP field: 0 and, per rule that can
+// match at all, base and the first address past its block.
+std::vector<uint32_t> ms_ip_bounds(int64_t n, const uint32_t *base, const uint32_t *mask) {
+    std::vector<uint32_t> b;
+    b.reserve((size_t)(2 * n + 1));
+    b.push_back(0u);
+    for (int64_t r = 0; r < n; r++) {
+        if (base[r] & ~mask[r]) continue;  // never matches: constant on every interval
+        b.push_back(base[r]);
+        const uint64_t e = (uint64_t)(base[r] | ~mask[r]) + 1;
+        if (e < (1ull << 32)) b.push_back((uint32_t)e);
+    }
+    std::sort(b.begin(), b.end());
+    b.erase(std::unique(b.begin(), b.end()), b.end());
+    return b;
+}
+
+std::vector<uint32_t> ms_port_bounds(int64_t n, const uint16_t *lo, const uint16_t *hi) {
+    std::vector<uint32_t> b;
+    b.reserve((size_t)(2 * n + 1));
+    b.push_back(0u);
+    for (int64_t r = 0; r < n; r++) {
+        if (lo[r] > hi[r]) continue;
+        b.push_back(lo[r]);
+        if ((uint32_t)hi[r] + 1 < 65536u) b.push_back((uint32_t)hi[r] + 1);
+    }
+    std::sort(b.begin(), b.end());
+    b.erase(std::unique(b.begin(), b.end()), b.end());
+    return b;
+}
+
+template <typename T>
+cudaError_t ms_upload(T **d, const T *h, size_t count) {
+    cudaError_t e = cudaMalloc(d, count * sizeof(T) + 16);
+    if (e == cudaSuccess && count) e = cudaMemcpy(*d, h, count * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+// Build the match sets of ruleset h (host columns as given to
+// pfw_ruleset_create).  Tables that would exceed the memory budget are not
+// built: the ruleset then scans rule by rule.
+int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, const uint32_t *src_mask,
+              const uint16_t *sport_lo, const uint16_t *sport_hi, const uint32_t *dst_base,
+              const uint32_t *dst_mask, const uint16_t *dport_lo, const uint16_t *dport_hi) {
+    const int64_t n = h->n;
+    if (n == 0 || !g_matchset) return PFW_OK;
+    const std::vector<uint32_t> bs = ms_ip_bounds(n, src_base, src_mask);
+    const std::vector<uint32_t> bd = ms_ip_bounds(n, dst_base, dst_mask);
+    const std::vector<uint32_t> bsp = ms_port_bounds(n, sport_lo, sport_hi);
+    const std::vector<uint32_t> bdp = ms_port_bounds(n, dport_lo, dport_hi);
+    // protocol classes: one per protocol a rule names, plus one for the rest
+    // (their packets match only ANY rules)
+    std::vector<int> cls_proto;
+    uint8_t cls[256];
+    {
+        bool named[256] = {};
+        for (int64_t r = 0; r < n; r++) named[proto[r]] = true;
+        for (int v = 1; v < 256; v++)
+            if (named[v]) cls_proto.push_back(v);
+        const int other = (int)cls_proto.size();
+        for (int v = 0; v < 256; v++) cls[v] = (uint8_t)other;
+        for (int c = 0; c < other; c++) cls[cls_proto[(size_t)c]] = (uint8_t)c;
+        cls_proto.push_back(-1);
+    }
+    MatchSet *m = new MatchSet();
+    m->wp = (((n + 31) / 32 + 127) / 128) * 128;  // whole 4-word-per-lane steps
+    m->sp_rows = (int64_t)bsp.size();
+    m->rows[MSD_SRC] = (int64_t)bs.size();
+    m->rows[MSD_DST] = (int64_t)bd.size();
+    m->rows[MSD_SPORT] = (int64_t)cls_proto.size() * m->sp_rows;
+    m->rows[MSD_DPORT] = (int64_t)bdp.size();
+    size_t bytes = 0;
+    for (int d = 0; d < 4; d++) bytes += (size_t)m->rows[d] * (size_t)m->wp * 4;
+    bytes += (bs.size() + bd.size()) * 4 + 2 * 65536 * (8 + 4) + 256;
+    m->bytes = bytes;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    const size_t budget = g_ms_budget_mb > 0 ? (size_t)g_ms_budget_mb << 20 : free_b / 4;
+    bool fits = bytes <= budget;
+    for (int d = 0; d < 4; d++)  // word offsets are 32-bit in the scan
+        fits = fits && (uint64_t)m->rows[d] * (uint64_t)m->wp + 4 * 32 < (1ull << 32);
+    if (!fits) {
+        delete m;
+        return PFW_OK;  // too large for the budget: rule-by-rule scan
+    }
+    // lookup tables
+    std::vector<uint2> ipc[2];
+    const std::vector<uint32_t> *ipb[2] = {&bs, &bd};
+    for (int d = 0; d < 2; d++) {
+        const std::vector<uint32_t> &b = *ipb[d];
+        std::vector<uint32_t> c(65537);
+        size_t k = 0;
+        for (uint32_t blk = 0; blk < 65536; blk++) {
+            while (k < b.size() && b[k] < (blk << 16)) k++;
+            c[blk] = (uint32_t)k;
+        }
+        c[65536] = (uint32_t)b.size();
+        ipc[d].resize(65536);
+        for (uint32_t blk = 0; blk < 65536; blk++) ipc[d][blk] = make_uint2(c[blk], c[blk + 1]);
+    }
+    std::vector<uint32_t> ptab[2];
+    const std::vector<uint32_t> *pb[2] = {&bsp, &bdp};
+    for (int d = 0; d < 2; d++) {
+        ptab[d].resize(65536);
+        size_t k = 0;
+        for (uint32_t v = 0; v < 65536; v++) {
+            while (k + 1 < pb[d]->size() && (*pb[d])[k + 1] <= v) k++;
+            ptab[d][v] = (uint32_t)k;
+        }
+    }
+    // device copies of the rule columns (build only)
+    uint32_t *d_sb = nullptr, *d_sm = nullptr, *d_db = nullptr, *d_dm = nullptr, *d_vals[4] = {};
+    uint16_t *d_slo = nullptr, *d_shi = nullptr, *d_dlo = nullptr, *d_dhi = nullptr;
+    uint8_t *d_pr = nullptr;
+    int *d_clsp = nullptr;
+    cudaError_t e = cudaSuccess;
+    // + one 4-word-per-lane step of padding: the last step of a row may read
+    // past its end (masked), also on the last row
+    for (int d = 0; d < 4 && e == cudaSuccess; d++)
+        e = cudaMalloc(&m->d_bits[d], ((size_t)m->rows[d] * (size_t)m->wp + 4 * 32) * 4);
+    for (int d = 0; d < 4 && e == cudaSuccess; d++)
+        e = cudaMemsetAsync(m->d_bits[d] + (size_t)m->rows[d] * (size_t)m->wp, 0, 4 * 32 * 4);
+    if (e == cudaSuccess) e = ms_upload(&m->d_ipb[0], bs.data(), bs.size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_ipb[1], bd.data(), bd.size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_ipc[0], ipc[0].data(), ipc[0].size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_ipc[1], ipc[1].data(), ipc[1].size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_port[0], ptab[0].data(), ptab[0].size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_port[1], ptab[1].data(), ptab[1].size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_cls, cls, 256);
+    if (e == cudaSuccess) e = ms_upload(&d_sb, src_base, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_sm, src_mask, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_db, dst_base, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_dm, dst_mask, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_slo, sport_lo, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_shi, sport_hi, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_dlo, dport_lo, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_dhi, dport_hi, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_pr, proto, (size_t)n);
+    if (e == cudaSuccess) e = ms_upload(&d_clsp, cls_proto.data(), cls_proto.size());
+    if (e == cudaSuccess) e = ms_upload(&d_vals[0], bs.data(), bs.size());
+    if (e == cudaSuccess) e = ms_upload(&d_vals[1], bd.data(), bd.size());
+    if (e == cudaSuccess) e = ms_upload(&d_vals[2], bsp.data(), bsp.size());
+    if (e == cudaSuccess) e = ms_upload(&d_vals[3], bdp.data(), bdp.size());
+    if (e == cudaSuccess) {
+        MsBuildArgs a{};
+        a.n = n;
+        a.wp = m->wp;
+        a.proto = d_pr;
+        a.cls_proto = d_clsp;
+        a.ivl = m->sp_rows;
+        const unsigned grid = (unsigned)(h->sms * 8);
+        for (int d = 0; d < 4; d++) {
+            a.rows = m->rows[d];
+            a.vals = d_vals[d];
+            a.bits = m->d_bits[d];
+            a.base = d == MSD_SRC ? d_sb : d_db;
+            a.mask = d == MSD_SRC ? d_sm : d_dm;
+            a.lo = d == MSD_SPORT ? d_slo : d_dlo;
+            a.hi = d == MSD_SPORT ? d_shi : d_dhi;
+            switch (d) {
+                case MSD_SRC: ms_build_kernel<MSD_SRC><<<grid, MS_BLOCK>>>(a); break;
+                case MSD_DST: ms_build_kernel<MSD_DST><<<grid, MS_BLOCK>>>(a); break;
+                case MSD_SPORT: ms_build_kernel<MSD_SPORT><<<grid, MS_BLOCK>>>(a); break;
+                default: ms_build_kernel<MSD_DPORT><<<grid, MS_BLOCK>>>(a); break;
+            }
+            g_launches++;
+        }
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    for (void *q : {(void *)d_sb, (void *)d_sm, (void *)d_db, (void *)d_dm, (void *)d_slo, (void *)d_shi,
+                    (void *)d_dlo, (void *)d_dhi, (void *)d_pr, (void *)d_clsp, (void *)d_vals[0],
+                    (void *)d_vals[1], (void *)d_vals[2], (void *)d_vals[3]})
+        if (q) cudaFree(q);
+    if (e != cudaSuccess) {
+        ms_free(m);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            return PFW_OK;  // could not place the tables: rule-by-rule scan
+        }
+        return set_err(PFW_ERR_CUDA, "match-set build failed: %s", cudaGetErrorString(e));
+    }
+    h->ms = m;
+    return PFW_OK;
+}
+
+template <int MODE>
+int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
+    const MatchSet *m = h->ms;
+    MsView t{};
+    for (int d = 0; d < 4; d++) t.bits[d] = m->d_bits[d];
+    t.ipb[0] = m->d_ipb[0];
+    t.ipb[1] = m->d_ipb[1];
+    t.ipc[0] = m->d_ipc[0];
+    t.ipc[1] = m->d_ipc[1];
+    t.port[0] = m->d_port[0];
+    t.port[1] = m->d_port[1];
+    t.cls = m->d_cls;
+    t.wp = m->wp;
+    t.sp_rows = (uint32_t)m->sp_rows;
+    void (*kern)(ScanParams, MsView);
+    const bool win = !(p.lo == 0 && p.hi == h->n);
+    switch (g_ms_words * 2 + (win ? 1 : 0)) {
+        case 2: kern = ms_scan_kernel<MODE, 1, false>; break;
+        case 3: kern = ms_scan_kernel<MODE, 1, true>; break;
+        case 8: kern = ms_scan_kernel<MODE, 4, false>; break;
+        case 9: kern = ms_scan_kernel<MODE, 4, true>; break;
+        case 5: kern = ms_scan_kernel<MODE, 2, true>; break;
+        default: kern = ms_scan_kernel<MODE, 2, false>; break;
+    }
+    int occ = g_ctas_per_sm;
+    if (occ <= 0) {
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MS_BLOCK, 0));
+        if (occ < 1) occ = 1;
+    }
+    int64_t grid = (int64_t)h->sms * occ;
+    const int64_t need = (p.n + MS_BLOCK - 1) / MS_BLOCK;  // one 32-packet batch per warp
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t);
+    CUDA_TRY(cudaGetLastError());
+    g_launches++;
+    return PFW_OK;
+}
+
+int launch_ms(pfw_ruleset *h, int mode, const ScanParams &p, cudaStream_t st) {
+    switch (mode) {
+        case MODE_ACC: return launch_ms_k<MODE_ACC>(h, p, st);
+        case MODE_PEER: return launch_ms_k<MODE_PEER>(h, p, st);
+        default: return launch_ms_k<MODE_WRITE>(h, p, st);
+    }
+}

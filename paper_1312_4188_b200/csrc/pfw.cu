@@ -137,6 +137,20 @@ struct ScanWs {
     int64_t cap = 0;
 };
 
+// Per-field match sets (matchset.cuh): field value -> elementary interval ->
+// bitmap row of the rules whose test on that field holds there.
+struct MatchSet {
+    int64_t wp = 0;             // 32-bit words per bitmap row (whole 128-byte lines)
+    int64_t rows[4] = {};       // rows of src, dst, (protocol class, sport), dport
+    uint32_t *d_bits[4] = {};   // rows[d] * wp words each
+    uint32_t *d_ipb[2] = {};    // src / dst interval boundaries (sorted, [0] = 0)
+    uint2 *d_ipc[2] = {};       // per /16 block: [first, end) index into the boundaries
+    uint32_t *d_port[2] = {};   // sport / dport -> interval (65536 entries each)
+    uint8_t *d_cls = nullptr;   // protocol -> class (256 entries)
+    int64_t sp_rows = 0;        // sport intervals = rows per protocol class
+    size_t bytes = 0;           // device bytes of all of the above
+};
+
 struct pfw_ruleset {
     int device;
     int64_t n;       // rules
@@ -167,6 +181,7 @@ struct pfw_ruleset {
     uint32_t *d_bucket = nullptr;      // packet ids grouped by chain (n)
     unsigned *d_bcount = nullptr;      // [3 * MAX_CHAINS]: count, base, cursor
     int64_t bucket_cap = 0;
+    MatchSet *ms = nullptr;            // match sets (null: not built / over budget)
 };
 
 namespace {
@@ -222,6 +237,46 @@ struct ScanParams {
 };
 
 enum { MODE_WRITE = 0, MODE_ACC = 1, MODE_PEER = 2 };
+
+// Result epilogue shared by the scan kernels: packet `id` first matches
+// original rule f (or PFW_NO_MATCH) inside the window; writes first /
+// comparisons / verdict (MODE_WRITE), accumulates a function-parallel
+// partition (MODE_ACC), or combines straight into the ranks' buffers
+// (MODE_PEER); span = window length (comparisons of an unmatched packet).
+template <int MODE>
+__device__ __forceinline__ void emit_result(const ScanParams &p, uint32_t id, uint32_t f, uint32_t span,
+                                            unsigned long long &st_sum, unsigned &st_max) {
+    const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.win_lo + 1) : span;
+    if (MODE == MODE_ACC) {
+        if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
+        p.comps[id] += c;
+    } else if (MODE == MODE_PEER) {
+        // the engines.py:202-212 min-combine and :366-367 sum, issued straight
+        // from the scan epilogue into the ranks' buffers (NVLink atomics),
+        // overlapping the transfer with the remaining tiles' compute
+        if (p.scatter) {
+            const uint64_t q = (uint64_t)p.n / (uint64_t)p.npeers;
+            const uint64_t r = (uint64_t)p.n % (uint64_t)p.npeers;
+            const uint64_t big = (q + 1) * r;
+            const uint64_t o = id < big ? id / (q + 1) : r + (id - big) / q;
+            const uint64_t off = id - (o < r ? o * (q + 1) : big + (o - r) * q);
+            PFW_CHECK(o < (uint64_t)p.npeers && off < (o < r ? q + 1 : q));
+            if (f != PFW_NO_MATCH) atomicMin(p.peer_first[o] + off, f);
+            if (p.peer_comps) atomicAdd(p.peer_comps[o] + off, c);
+        } else {
+            for (int t = 0; t < p.npeers; t++) {
+                if (f != PFW_NO_MATCH) atomicMin(p.peer_first[t] + id, f);
+                if (p.peer_comps) atomicAdd(p.peer_comps[t] + id, c);
+            }
+        }
+    } else {
+        p.first[id] = f;
+        if (p.comps) p.comps[id] = c;
+        if (p.verdict) p.verdict[id] = (f != PFW_NO_MATCH) ? p.accept[f] : (uint8_t)0;
+    }
+    st_sum += c;
+    st_max = max(st_max, c);
+}
 
 __device__ __forceinline__ uint32_t sub_fma(uint32_t x, uint32_t one, uint32_t nlo) {
     uint32_t d;
@@ -733,37 +788,7 @@ __global__ void __launch_bounds__(BLOCK, min_ctas<KS>()) scan_kernel(ScanParams 
                     PFW_CHECK(f == PFW_NO_MATCH || (f >= p.lo && f < p.hi));
                     if (p.orig && f != PFW_NO_MATCH) f = __ldg(p.orig + f);
                     PFW_CHECK(f == PFW_NO_MATCH || (f >= p.win_lo && f < p.win_hi));
-                    const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.win_lo + 1) : span;
-                    if (MODE == MODE_ACC) {
-                        if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
-                        p.comps[id] += c;
-                    } else if (MODE == MODE_PEER) {
-                        // the engines.py:202-212 min-combine and :366-367 sum,
-                        // issued straight from the scan epilogue into the
-                        // ranks' buffers (NVLink atomics), overlapping the
-                        // transfer with the remaining tiles' compute
-                        if (p.scatter) {
-                            const uint64_t q = (uint64_t)p.n / (uint64_t)p.npeers;
-                            const uint64_t r = (uint64_t)p.n % (uint64_t)p.npeers;
-                            const uint64_t big = (q + 1) * r;
-                            const uint64_t o = id < big ? id / (q + 1) : r + (id - big) / q;
-                            const uint64_t off = id - (o < r ? o * (q + 1) : big + (o - r) * q);
-                            PFW_CHECK(o < (uint64_t)p.npeers && off < (o < r ? q + 1 : q));
-                            if (f != PFW_NO_MATCH) atomicMin(p.peer_first[o] + off, f);
-                            if (p.peer_comps) atomicAdd(p.peer_comps[o] + off, c);
-                        } else {
-                            for (int t = 0; t < p.npeers; t++) {
-                                if (f != PFW_NO_MATCH) atomicMin(p.peer_first[t] + id, f);
-                                if (p.peer_comps) atomicAdd(p.peer_comps[t] + id, c);
-                            }
-                        }
-                    } else {
-                        p.first[id] = f;
-                        if (p.comps) p.comps[id] = c;
-                        if (p.verdict) p.verdict[id] = (f != PFW_NO_MATCH) ? p.accept[f] : (uint8_t)0;
-                    }
-                    st_sum += c;
-                    st_max = max(st_max, c);
+                    emit_result<MODE>(p, id, f, span, st_sum, st_max);
                 }
             }
             const unsigned b = __ballot_sync(0xFFFFFFFFu, survive);
@@ -1016,6 +1041,8 @@ uint64_t host_randbelow(uint64_t &x, uint64_t n) {
 }
 
 
+#include "matchset.cuh"
+
 int ensure_ws(ScanWs &ws, int64_t n) {
     if (!ws.ctr) CUDA_TRY(cudaMalloc(&ws.ctr, 2 * MAX_PASSES * sizeof(unsigned int)));
     if (ws.cap < n) {
@@ -1181,6 +1208,11 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
         p.scatter = peer->scatter;
     }
     ScanWs &w = ws ? *ws : h->ws;
+    // match sets (matchset.cuh) unless the rule-by-rule scan is asked for
+    // (algo 1, or one of its own options: protocol-split chains, short circuit)
+    if (g_algo == 2 && !h->ms) return set_err(PFW_ERR_INVALID, "algo=2: this ruleset has no match sets");
+    if (h->ms && (g_algo == 2 || (g_algo == 0 && !g_proto_split && !g_short_circuit)))
+        return launch_ms(h, mode, p, st);
     if (g_proto_split && !h->chains.empty() && lo < hi) return launch_split(h, mode, p, w, st, true);
     // large batches are grouped by protocol first so that tiles are
     // protocol-uniform (the one-FADD sport test); single-protocol batches skip
@@ -1310,6 +1342,17 @@ int pfw_set_tuning(const char *key, int64_t value) {
         g_proto_split = value != 0;
     } else if (!strcmp(key, "force_imad")) {
         g_force_imad = value != 0;
+    } else if (!strcmp(key, "algo")) {
+        if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "algo: 0 auto, 1 rule scan, 2 match sets");
+        g_algo = (int)value;
+    } else if (!strcmp(key, "matchset")) {
+        g_matchset = value != 0;
+    } else if (!strcmp(key, "matchset_budget_mb")) {
+        if (value < 0) return set_err(PFW_ERR_INVALID, "matchset_budget_mb must be >= 0");
+        g_ms_budget_mb = value;
+    } else if (!strcmp(key, "ms_words")) {
+        if (value != 1 && value != 2 && value != 4) return set_err(PFW_ERR_INVALID, "ms_words: 1, 2 or 4");
+        g_ms_words = (int)value;
     } else {
         return set_err(PFW_ERR_INVALID, "unknown tuning key '%s'", key);
     }
@@ -1431,6 +1474,14 @@ int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32
         if (e == cudaSuccess) e = cudaMalloc(&h->d_lut, 256);
         if (e == cudaSuccess) e = cudaMemcpy(h->d_lut, lut, 256, cudaMemcpyHostToDevice);
     }
+    if (e == cudaSuccess) {
+        const int rc = ms_create(h, proto, src_base, src_mask, sport_lo, sport_hi, dst_base, dst_mask, dport_lo,
+                                 dport_hi);
+        if (rc != PFW_OK) {
+            pfw_ruleset_destroy(h);
+            return rc;
+        }
+    }
     if (e != cudaSuccess) {
         const int code = e == cudaErrorMemoryAllocation ? PFW_ERR_NOMEM : PFW_ERR_CUDA;
         pfw_ruleset_destroy(h);
@@ -1453,6 +1504,7 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
         if (ch.d_orig) cudaFree(ch.d_orig);
     }
     if (h->d_lut) cudaFree(h->d_lut);
+    ms_free(h->ms);
     if (h->d_bucket) cudaFree(h->d_bucket);
     if (h->d_bcount) cudaFree(h->d_bcount);
     free_ws(h->ws_e2e[0]);
@@ -1467,6 +1519,7 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
 
 int64_t pfw_ruleset_size(pfw_ruleset_t h) { return h ? h->n : -1; }
 int pfw_ruleset_device(pfw_ruleset_t h) { return h ? h->device : -1; }
+int64_t pfw_ruleset_matchset_bytes(pfw_ruleset_t h) { return h && h->ms ? (int64_t)h->ms->bytes : 0; }
 
 int pfw_pack_packets_host(int64_t n, const uint8_t *proto, const uint32_t *src_ip,
                           const uint16_t *src_port, const uint32_t *dst_ip,

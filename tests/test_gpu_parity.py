@@ -37,7 +37,8 @@ def compiled(rules: dict) -> pfw.CompiledRuleset:
 def _reset_tuning():
     yield
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
-                 ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20)):
+                 ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
+                 ("algo", 0), ("ms_words", 2), ("matchset", 1), ("matchset_budget_mb", 0)):
         _native.set_tuning(k, v)
 
 
@@ -292,6 +293,7 @@ def test_unnormalised_and_inverted_rules_never_match():
                                              (8, 6144, 0, 1024), (4, 2048, 1, 100), (8, 2048, 1, 32),
                                              (6, 2048, 1, 1024)])
 def test_tuning_variants_identical(ks, tile, imad, fp, sc):
+    _native.set_tuning("algo", 1)
     _native.set_tuning("short_circuit", sc)
     _native.set_tuning("ks", ks)
     _native.set_tuning("tile", tile)
@@ -313,6 +315,7 @@ def test_tuning_variants_identical(ks, tile, imad, fp, sc):
 
 
 def test_tile_too_large_is_rejected_loudly():
+    _native.set_tuning("algo", 1)
     _native.set_tuning("tile", 8192)
     c = compiled(golden_rules("r64_s30_w40"))
     with pytest.raises(ValueError, match="shared memory"):
@@ -423,11 +426,13 @@ def test_fused_function_parallel_single_rank_class():
 
 @pytest.mark.parametrize("name,rn,tn", SCANS)
 def test_proto_split_scan_matches_reference_golden(name, rn, tn):
+    _native.set_tuning("algo", 1)
     _native.set_tuning("proto_split", 1)
     test_scan_matches_reference_golden(name, rn, tn)
 
 
 def test_proto_split_windows_engines_and_mixed_protocols():
+    _native.set_tuning("algo", 1)
     _native.set_tuning("proto_split", 1)
     test_scan_windows()
     test_windows_every_alignment_vs_oracle()
@@ -451,6 +456,7 @@ def test_proto_split_windows_engines_and_mixed_protocols():
 
 @pytest.mark.parametrize("name,rn,tn", SCANS)
 def test_short_circuit_scan_matches_reference_golden(name, rn, tn):
+    _native.set_tuning("algo", 1)
     _native.set_tuning("short_circuit", 1)
     test_scan_matches_reference_golden(name, rn, tn)
 
@@ -464,7 +470,8 @@ def test_scan_range_columns_device_and_host():
     dev = {f: torch.from_numpy(np.ascontiguousarray(pk[f]).view(
         {np.uint8: np.uint8, np.uint16: np.int16, np.uint32: np.int32}[pk[f].dtype.type])).to("cuda:0")
         for f in PKT_FIELDS}
-    for split in (0, 1):
+    for algo, split in ((0, 0), (1, 0), (1, 1)):
+        _native.set_tuning("algo", algo)
         _native.set_tuning("proto_split", split)
         for lo, hi in ((0, 2048), (100, 1500)):
             first = c.scan_range_columns_device(dev, lo, hi)
@@ -483,6 +490,7 @@ def test_scan_range_columns_device_and_host():
 def test_protocol_uniform_tiles(proto):
     """Every packet of a tile has the same protocol -> ANY rules are rewritten
     into the protocol-major form for it at stage load (no rule skipped)."""
+    _native.set_tuning("algo", 1)
     rules = oracle.gen_ruleset(1500, 23, wp=0.35)
     rules["proto"][::13] = 47
     rules["proto"][::29] = 255
@@ -494,6 +502,7 @@ def test_protocol_uniform_tiles(proto):
 
 
 def test_mixed_and_uniform_tiles_in_one_batch():
+    _native.set_tuning("algo", 1)
     _native.set_tuning("tile", 256)
     rules = oracle.gen_ruleset(900, 25, wp=0.35)
     pk = oracle.gen_traffic_uniform(256 * 12, 26)
@@ -508,6 +517,7 @@ def test_mixed_and_uniform_tiles_in_one_batch():
 def test_protocol_bucketing_mixed_traffic(bucket_min):
     """Mixed-protocol batches are grouped by protocol on the device so tiles are
     protocol-uniform; results identical, with or without the grouping."""
+    _native.set_tuning("algo", 1)
     _native.set_tuning("bucket_min", bucket_min)
     rules = oracle.gen_ruleset(2500, 31, wp=0.3)
     rules["proto"][::17] = 47
@@ -532,5 +542,101 @@ def test_protocol_bucketing_mixed_traffic(bucket_min):
 
 @pytest.mark.parametrize("name,rn,tn", SCANS)
 def test_bucketed_scan_matches_reference_golden(name, rn, tn):
+    _native.set_tuning("algo", 1)
     _native.set_tuning("bucket_min", 0)
     test_scan_matches_reference_golden(name, rn, tn)
+
+
+# ------------------------------------------------- rule-by-rule vs match sets
+
+@pytest.mark.parametrize("name,rn,tn", SCANS)
+def test_rule_scan_matches_reference_golden(name, rn, tn):
+    """The same goldens through the rule-by-rule scan (the default path is the
+    match-set scan whenever the ruleset's match sets were built)."""
+    _native.set_tuning("algo", 1)
+    test_scan_matches_reference_golden(name, rn, tn)
+
+
+def test_rule_scan_windows_engines_and_samples():
+    _native.set_tuning("algo", 1)
+    test_scan_windows()
+    test_windows_every_alignment_vs_oracle()
+    for model in ("data", "function", "hybrid"):
+        test_engine_models_match_reference_golden(model)
+    test_function_parallel_100k_rules()
+    test_adversarial_recipe_sample()
+    test_ragged_sizes_and_empty()
+    test_unnormalised_and_inverted_rules_never_match()
+    test_fused_min_combine_virtual_ranks(1)
+    test_fused_min_combine_virtual_ranks(0)
+
+
+def test_match_sets_built_for_every_config_ruleset():
+    for rn in ("r1000_s1", "r4096_s1", "r10000_s1", "r100000_s1"):
+        c = compiled(golden_rules(rn))
+        assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
+
+
+@pytest.mark.parametrize("words", [1, 2, 4])
+def test_match_set_words_per_step(words):
+    _native.set_tuning("algo", 2)
+    _native.set_tuning("ms_words", words)
+    test_scan_matches_reference_golden("r2048_t1000", "r2048_s21_w15", "t1000_s22")
+    test_scan_matches_reference_golden("r1000_t3000icmp", "r1000_s1", "t3000_s11_icmp")
+    test_windows_every_alignment_vs_oracle()
+    test_engine_models_match_reference_golden("hybrid")
+    test_ragged_sizes_and_empty()
+
+
+def test_match_set_budget_falls_back_to_rule_scan():
+    _native.set_tuning("matchset_budget_mb", 1)        # 10K rules need ~117 MB
+    c = compiled(golden_rules("r10000_s1"))
+    assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) == 0
+    g = golden("scan_r10000_s1_t20000.npz")
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=20_000, seed=2), device=0)
+    np.testing.assert_array_equal(c.scan_range(p, 0, c.num_rules), g["first"])   # rule-by-rule scan
+    _native.set_tuning("algo", 2)
+    with pytest.raises(ValueError, match="no match sets"):
+        c.scan_range(p, 0, c.num_rules)
+    _native.set_tuning("matchset_budget_mb", 0)
+    _native.set_tuning("matchset", 0)
+    assert _native.lib().pfw_ruleset_matchset_bytes(compiled(golden_rules("r64_s30_w40")).handle) == 0
+
+
+def test_match_set_interval_edges():
+    """Interval boundaries at the ends of the value domains: /0, /32, host
+    255.255.255.255, port 0 / 65535, single-port ranges, adjacent blocks,
+    protocols no rule names, packet protocol 0."""
+    rng = np.random.default_rng(77)
+    R = 700
+    rules = oracle.gen_ruleset(R, 78, wp=0.25)
+    edge_ips = np.array([0, 1, 0xFFFFFFFF, 0xFFFFFFFE, 0x80000000, 0x7FFFFFFF, 0x0A000000, 0x0A0000FF,
+                         0x0A000100, 0xC0A80001], dtype=np.uint32)
+    for k in range(0, R, 7):
+        plen = int(rng.choice([0, 1, 8, 16, 24, 31, 32]))
+        mask = np.uint32(0) if plen == 0 else np.uint32((0xFFFFFFFF << (32 - plen)) & 0xFFFFFFFF)
+        ip = np.uint32(rng.choice(edge_ips))
+        f = "src" if k % 2 else "dst"
+        rules[f + "_base"][k] = ip & mask
+        rules[f + "_mask"][k] = mask
+        lo = int(rng.choice([0, 1, 80, 1023, 65534, 65535]))
+        hi = int(rng.choice([lo, min(lo + 1, 65535), 65535]))
+        rules["sport_lo" if k % 3 else "dport_lo"][k] = lo
+        rules["sport_hi" if k % 3 else "dport_hi"][k] = hi
+    rules["proto"][::31] = 47
+    n = 20_000
+    pk = oracle.gen_traffic_uniform(n, 79)
+    pk["src_ip"][:4000] = rng.choice(edge_ips, 4000)
+    pk["dst_ip"][2000:6000] = rng.choice(edge_ips, 4000)
+    pk["src_port"][::3] = rng.choice(np.array([0, 1, 80, 1023, 1024, 65534, 65535], np.uint16), len(pk["src_port"][::3]))
+    pk["dst_port"][::5] = rng.choice(np.array([0, 1, 80, 1023, 1024, 65534, 65535], np.uint16), len(pk["dst_port"][::5]))
+    pk["proto"][::11] = 17
+    pk["proto"][::13] = 1
+    pk["proto"][::17] = 47
+    pk["proto"][::19] = 0
+    pk["proto"][::23] = 200
+    c = compiled(rules)
+    assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
+    _native.set_tuning("algo", 2)
+    for lo, hi in ((0, R), (1, R - 1), (31, 32), (32, 1024 % R), (300, 301), (64, 700)):
+        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))

@@ -72,16 +72,21 @@ def rules_and_packets(draw):
 @pytest.fixture(autouse=True)
 def _reset():
     yield
-    for k, v in (("proto_split", 0), ("first_pass", 1024), ("ks", 8)):
+    for k, v in (("proto_split", 0), ("first_pass", 1024), ("ks", 8), ("algo", 0), ("ms_words", 2)):
         _native.set_tuning(k, v)
 
 
-@settings(max_examples=60, deadline=None, suppress_health_check=list(HealthCheck))
-@given(case=rules_and_packets(), split=st.booleans(), fp=st.sampled_from([32, 64, 1024]))
-def test_random_boundary_cases_bit_exact(case, split, fp):
+@settings(max_examples=90, deadline=None, suppress_health_check=list(HealthCheck))
+@given(case=rules_and_packets(), mode=st.sampled_from(["matchset", "rule", "split"]),
+       fp=st.sampled_from([32, 64, 1024]), words=st.sampled_from([1, 2, 4]))
+def test_random_boundary_cases_bit_exact(case, mode, fp, words):
+    """Match-set scan, rule-by-rule scan and protocol-split chains on the same
+    boundary-heavy random cases."""
     cols, pk, lo, hi = case
-    _native.set_tuning("proto_split", int(split))
+    _native.set_tuning("algo", {"matchset": 2, "rule": 1, "split": 1}[mode])
+    _native.set_tuning("proto_split", int(mode == "split"))
     _native.set_tuning("first_pass", fp)
+    _native.set_tuning("ms_words", words)
     c = pfw.CompiledRuleset.from_columns(cols, device=0)
     p = pfw.PacketArrays.from_columns(*[pk[f] for f in PKT_FIELDS], device=0)
     np.testing.assert_array_equal(c.scan_range(p, lo, hi), oracle.scan_range(cols, pk, lo, hi))
