@@ -204,6 +204,7 @@ def main() -> int:
     ap.add_argument("--algo", type=int, default=-1,
                     help="0 auto (match sets when built), 1 rule-by-rule scan, 2 match sets")
     ap.add_argument("--ms-words", type=int, default=0, help="match-set scan: words per lane per step (1, 2, 4)")
+    ap.add_argument("--ms-group", type=int, default=0, help="match-set scan: lanes per packet (8, 16, 32)")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--sc", type=int, default=-1, help="warp-level short-circuit of the port tests (0/1)")
     ap.add_argument("--bucket", type=int, default=-1, help="group large batches by protocol (0/1)")
@@ -250,6 +251,8 @@ def main() -> int:
         _native.set_tuning("algo", args.algo)
     if args.ms_words:
         _native.set_tuning("ms_words", args.ms_words)
+    if args.ms_group:
+        _native.set_tuning("ms_group", args.ms_group)
     if args.ks:
         _native.set_tuning("ks", args.ks)
     if args.sc >= 0:

@@ -24,12 +24,16 @@
 // leading lines (where most first matches are) stay resident in L2.
 
 constexpr int MS_BLOCK = 256;
+#ifndef PFW_MS_MINB
+#define PFW_MS_MINB 5  // resident blocks per SM the scan is register-limited to
+#endif
 enum { MSD_SRC = 0, MSD_DST = 1, MSD_SPORT = 2, MSD_DPORT = 3 };
 
 int g_matchset = 1;            // build match sets at ruleset creation
 int g_algo = 0;                // 0 auto (match sets when built), 1 rule-by-rule scan, 2 match sets
 int64_t g_ms_budget_mb = 0;    // device-memory budget for the tables (0 = a quarter of free memory)
-int g_ms_words = 2;            // words per lane per step: 1024 * g_ms_words rules per step (1, 2, 4)
+int g_ms_group = 0;            // lanes per packet (8, 16, 32; 0 = by ruleset size): 32 / group packets in flight per warp
+int g_ms_words = 4;            // words per lane per step: 32 * group * words rules per step
 
 struct MsBuildArgs {
     const uint32_t *base, *mask;  // IP fields
@@ -106,72 +110,102 @@ __device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint2 *c,
     return lo - 1;
 }
 
+// The four rows' words of one step, loaded by one asm block so that all four
+// loads are in flight together (ptxas otherwise may hold the last one back
+// behind the first three to save registers: two L2 round trips per step).
 template <int V>
-struct MsWords;
+struct MsStep;
 template <>
-struct MsWords<1> {
-    uint32_t w[1];
-    __device__ __forceinline__ void load(const uint32_t *q) { w[0] = __ldg(q); }
-};
-template <>
-struct MsWords<2> {
-    uint32_t w[2];
-    __device__ __forceinline__ void load(const uint32_t *q) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(q));
-        w[0] = v.x;
-        w[1] = v.y;
+struct MsStep<4> {
+    uint32_t w[4][4];
+    __device__ __forceinline__ void load(const uint32_t *a, const uint32_t *b, const uint32_t *c,
+                                         const uint32_t *d) {
+        asm volatile(
+            "ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%16];\n\t"
+            "ld.global.nc.v4.u32 {%4, %5, %6, %7}, [%17];\n\t"
+            "ld.global.nc.v4.u32 {%8, %9, %10, %11}, [%18];\n\t"
+            "ld.global.nc.v4.u32 {%12, %13, %14, %15}, [%19];"
+            : "=r"(w[0][0]), "=r"(w[0][1]), "=r"(w[0][2]), "=r"(w[0][3]), "=r"(w[1][0]), "=r"(w[1][1]),
+              "=r"(w[1][2]), "=r"(w[1][3]), "=r"(w[2][0]), "=r"(w[2][1]), "=r"(w[2][2]), "=r"(w[2][3]),
+              "=r"(w[3][0]), "=r"(w[3][1]), "=r"(w[3][2]), "=r"(w[3][3])
+            : "l"(a), "l"(b), "l"(c), "l"(d));
     }
 };
 template <>
-struct MsWords<4> {
-    uint32_t w[4];
-    __device__ __forceinline__ void load(const uint32_t *q) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(q));
-        w[0] = v.x;
-        w[1] = v.y;
-        w[2] = v.z;
-        w[3] = v.w;
+struct MsStep<2> {
+    uint32_t w[4][2];
+    __device__ __forceinline__ void load(const uint32_t *a, const uint32_t *b, const uint32_t *c,
+                                         const uint32_t *d) {
+        asm volatile(
+            "ld.global.nc.v2.u32 {%0, %1}, [%8];\n\t"
+            "ld.global.nc.v2.u32 {%2, %3}, [%9];\n\t"
+            "ld.global.nc.v2.u32 {%4, %5}, [%10];\n\t"
+            "ld.global.nc.v2.u32 {%6, %7}, [%11];"
+            : "=r"(w[0][0]), "=r"(w[0][1]), "=r"(w[1][0]), "=r"(w[1][1]), "=r"(w[2][0]), "=r"(w[2][1]),
+              "=r"(w[3][0]), "=r"(w[3][1])
+            : "l"(a), "l"(b), "l"(c), "l"(d));
+    }
+};
+template <>
+struct MsStep<1> {
+    uint32_t w[4][1];
+    __device__ __forceinline__ void load(const uint32_t *a, const uint32_t *b, const uint32_t *c,
+                                         const uint32_t *d) {
+        asm volatile(
+            "ld.global.nc.u32 %0, [%4];\n\t"
+            "ld.global.nc.u32 %1, [%5];\n\t"
+            "ld.global.nc.u32 %2, [%6];\n\t"
+            "ld.global.nc.u32 %3, [%7];"
+            : "=r"(w[0][0]), "=r"(w[1][0]), "=r"(w[2][0]), "=r"(w[3][0])
+            : "l"(a), "l"(b), "l"(c), "l"(d));
     }
 };
 
 // Warps own batches of 32 packets (grid-stride).  Lane l looks up packet l's
-// four rows; then the warp walks the batch one packet at a time: per step
-// every lane reads V consecutive words of each of the packet's four rows
-// (32*V words = 1024*V rules per step, one vector load per row), ANDs them,
-// and one ballot finds the first lane holding a non-zero word.  The window
-// masks apply only on the first and last step.
+// four rows (word offsets into shared memory).  The warp then works as 32/G
+// independent groups of G lanes: each group searches one packet, reading V
+// consecutive words per lane of each of the packet's four rows per step
+// (G*V words = 32*G*V rules, one vector load per row per lane), ANDs them;
+// one ballot per iteration serves every group (the group's slice of it finds
+// its first non-zero word).  A group that finishes its packet (match, or
+// window exhausted) takes the batch's next packet at once, so groups advance
+// independently and the warp's loads stay spread over 32/G packets.
 // WIN: the window is not the whole table, so the first / last step mask
 // words outside it (a whole-table scan needs no masks: bits past the last
 // rule are zero and rows are whole steps long).
-template <int MODE, int V, bool WIN>
-__global__ void __launch_bounds__(MS_BLOCK) ms_scan_kernel(ScanParams p, MsView t) {
-    constexpr uint32_t STEP = 32u * V;  // words per step
-    const int lane = threadIdx.x & 31;
+template <int MODE, int G, int V, bool WIN>
+__global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanParams p, MsView t) {
+    constexpr int P = 32 / G;                      // packets in flight per warp
+    constexpr uint32_t STEP = (uint32_t)G * V;     // words per step
+    constexpr uint32_t GMASK = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
+    __shared__ uint4 s_off[MS_BLOCK / 32][32];     // per warp: row offsets of the batch's packets
+    __shared__ uint32_t s_res[MS_BLOCK / 32][32];  // per warp: first match of the batch's packets
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
     const int64_t n = p.n;
     const uint32_t span = (uint32_t)(p.win_hi > p.win_lo ? p.win_hi - p.win_lo : 0);
     const bool empty = p.lo >= p.hi;
     const uint32_t wlo = (uint32_t)(p.lo >> 5), whi = empty ? 0u : (uint32_t)((p.hi - 1) >> 5);
-    const uint32_t cbeg = wlo & ~(STEP - 1u);                 // step-aligned start
+    const uint32_t cbeg = wlo & ~(STEP - 1u);      // step-aligned start
     const int nsteps = empty ? 0 : (int)((whi - cbeg) / STEP) + 1;
-    // this lane's masks on the first and the last step
+    // this lane's masks on the first and the last step (WIN)
     uint32_t mfirst[V], mlast[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
-        const uint32_t w0 = cbeg + (uint32_t)lane * V + v;
-        const uint32_t wl = cbeg + (uint32_t)(nsteps - 1) * STEP + (uint32_t)lane * V + v;
+        const uint32_t w0 = cbeg + (uint32_t)gl * V + v;
+        const uint32_t wl = cbeg + (uint32_t)(nsteps - 1) * STEP + (uint32_t)gl * V + v;
         mfirst[v] = w0 < wlo ? 0u : (w0 == wlo ? (0xFFFFFFFFu << (p.lo & 31)) : 0xFFFFFFFFu);
         mlast[v] = wl > whi ? 0u : (wl == whi ? (0xFFFFFFFFu >> (31 - ((p.hi - 1) & 31))) : 0xFFFFFFFFu);
     }
+    const uint32_t lv = (uint32_t)gl * V;
     unsigned long long st_sum = 0;
     unsigned st_max = 0;
 
     for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
         const int64_t i = b0 + lane;
         const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
-        // row offsets (words) of this lane's packet, at the first step
-        uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
         if (i < n) {
             uint4 v;
             if (p.pkts) {
@@ -182,60 +216,98 @@ __global__ void __launch_bounds__(MS_BLOCK) ms_scan_kernel(ScanParams p, MsView 
                 v.z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
                 v.w = __ldg(p.cols.proto + i);
             }
-            const uint32_t wp = (uint32_t)t.wp, at = cbeg;
-            o0 = ms_ip_row(t.ipb[0], t.ipc[0], v.x) * wp + at;
-            o1 = ms_ip_row(t.ipb[1], t.ipc[1], v.y) * wp + at;
-            o2 = ((uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16))) * wp + at;
-            o3 = __ldg(t.port[1] + (v.z & 0xFFFFu)) * wp + at;
+            const uint32_t wp = (uint32_t)t.wp;
+            uint4 o;
+            o.x = ms_ip_row(t.ipb[0], t.ipc[0], v.x) * wp + cbeg;
+            o.y = ms_ip_row(t.ipb[1], t.ipc[1], v.y) * wp + cbeg;
+            o.z = ((uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16))) * wp + cbeg;
+            o.w = __ldg(t.port[1] + (v.z & 0xFFFFu)) * wp + cbeg;
+            s_off[warp][lane] = o;
         }
-        uint32_t res = PFW_NO_MATCH;
-        // + this lane's V words of each step
-        const uint32_t *const t0 = t.bits[0] + lane * V, *const t1 = t.bits[1] + lane * V;
-        const uint32_t *const t2 = t.bits[2] + lane * V, *const t3 = t.bits[3] + lane * V;
-        for (int j = 0; j < nv; j++) {
-            const uint32_t *r0 = t0 + __shfl_sync(0xFFFFFFFFu, o0, j);
-            const uint32_t *r1 = t1 + __shfl_sync(0xFFFFFFFFu, o1, j);
-            const uint32_t *r2 = t2 + __shfl_sync(0xFFFFFFFFu, o2, j);
-            const uint32_t *r3 = t3 + __shfl_sync(0xFFFFFFFFu, o3, j);
-            for (int s = 0; s < nsteps; s++) {
-                const uint32_t so = (uint32_t)s * STEP;
-                MsWords<V> a, b, c, d;
-                a.load(r0);
-                b.load(r1);
-                c.load(r2);
-                d.load(r3);
-                r0 += STEP;
-                r1 += STEP;
-                r2 += STEP;
-                r3 += STEP;
+        s_res[warp][lane] = PFW_NO_MATCH;
+        __syncwarp();
+        if (nsteps > 0) {
+            // group state (group-uniform): packet pj (-1 idle), step s, the
+            // packet's four row offsets at this lane's words of step s.
+            // Packets are handed out in group order, so once every packet is
+            // taken the idle-group count is next - nv: the loop ends when it
+            // reaches P.
+            int pj = grp < nv ? grp : -1;
+            int next = P;
+            int s = 0;
+            uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+            if (pj >= 0) {
+                const uint4 o = s_off[warp][pj];
+                o0 = o.x + lv;
+                o1 = o.y + lv;
+                o2 = o.z + lv;
+                o3 = o.w + lv;
+            }
+            while (next < nv + P) {
+                const bool act = pj >= 0;
                 uint32_t x[V], any = 0u;
 #pragma unroll
-                for (int v = 0; v < V; v++) {
-                    x[v] = a.w[v] & b.w[v] & c.w[v] & d.w[v];
-                    if (WIN) {
-                        if (s == 0) x[v] &= mfirst[v];
-                        if (s == nsteps - 1) x[v] &= mlast[v];
+                for (int v = 0; v < V; v++) x[v] = 0u;
+                if (act) {
+                    MsStep<V> st;
+                    st.load(t.bits[0] + o0, t.bits[1] + o1, t.bits[2] + o2, t.bits[3] + o3);
+#pragma unroll
+                    for (int v = 0; v < V; v++) {
+                        x[v] = st.w[0][v] & st.w[1][v] & st.w[2][v] & st.w[3][v];
+                        if (WIN) {
+                            if (s == 0) x[v] &= mfirst[v];
+                            if (s == nsteps - 1) x[v] &= mlast[v];
+                        }
+                        any |= x[v];
                     }
-                    any |= x[v];
                 }
                 const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
-                if (bal) {
-                    // lowest set bit: first lane with a non-zero word, its
-                    // first non-zero word, that word's lowest bit
-                    uint32_t cand = 0;
+                const uint32_t gbits = (bal >> gbase) & GMASK;
+                // this lane's lowest set bit: first non-zero word, its lowest bit
+                uint32_t wsel = x[V - 1], widx = V - 1;
 #pragma unroll
-                    for (int v = V - 1; v >= 0; v--)
-                        if (x[v]) cand = (cbeg + so + (uint32_t)lane * V + v) * 32u + (uint32_t)(__ffs(x[v]) - 1);
-                    cand = __shfl_sync(0xFFFFFFFFu, cand, __ffs(bal) - 1);
-                    if (lane == j) res = cand;
-                    break;
+                for (int v = V - 2; v >= 0; v--) {
+                    if (x[v]) {
+                        wsel = x[v];
+                        widx = v;
+                    }
                 }
+                const uint32_t cand = __shfl_sync(0xFFFFFFFFu,
+                                                  (cbeg + (uint32_t)s * STEP + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1),
+                                                  gbase + (__ffs(gbits) - 1) * (gbits != 0u));
+                const bool found = gbits != 0u;  // (idle groups have no bits)
+                if (found && gl == 0) s_res[warp][pj] = cand;
+                const bool done = act && (found || s + 1 >= nsteps);
+                const unsigned dmask = __ballot_sync(0xFFFFFFFFu, done && gl == 0);
+                if (done) {
+                    // take the next packet (rank of this group among the done ones)
+                    const int np = next + __popc(dmask & ((1u << gbase) - 1u));
+                    pj = np < nv ? np : -1;
+                    s = 0;
+                    if (pj >= 0) {
+                        const uint4 o = s_off[warp][pj];
+                        o0 = o.x + lv;
+                        o1 = o.y + lv;
+                        o2 = o.z + lv;
+                        o3 = o.w + lv;
+                    }
+                } else if (act) {
+                    s++;
+                    o0 += STEP;
+                    o1 += STEP;
+                    o2 += STEP;
+                    o3 += STEP;
+                }
+                next += __popc(dmask);
             }
         }
+        __syncwarp();
         if (i < n) {
+            const uint32_t res = s_res[warp][lane];
             PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
             emit_result<MODE>(p, (uint32_t)i, res, span, st_sum, st_max);
         }
+        __syncwarp();
     }
     if (p.stats) {
 #pragma unroll
@@ -464,16 +536,23 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     t.cls = m->d_cls;
     t.wp = m->wp;
     t.sp_rows = (uint32_t)m->sp_rows;
-    void (*kern)(ScanParams, MsView);
+    void (*kern)(ScanParams, MsView) = nullptr;
     const bool win = !(p.lo == 0 && p.hi == h->n);
-    switch (g_ms_words * 2 + (win ? 1 : 0)) {
-        case 2: kern = ms_scan_kernel<MODE, 1, false>; break;
-        case 3: kern = ms_scan_kernel<MODE, 1, true>; break;
-        case 8: kern = ms_scan_kernel<MODE, 4, false>; break;
-        case 9: kern = ms_scan_kernel<MODE, 4, true>; break;
-        case 5: kern = ms_scan_kernel<MODE, 2, true>; break;
-        default: kern = ms_scan_kernel<MODE, 2, false>; break;
-    }
+    // auto: 8 lanes (4 packets in flight, 1024-rule steps) while the rows'
+    // leading lines fit in L2; 16 lanes (2048-rule steps, fewer iterations)
+    // for large rulesets whose scans run long and mostly miss L2
+    const int grp = g_ms_group ? g_ms_group : (h->n > 16384 ? 16 : 8);
+#define PFW_MS_PICK(G_, V_)                                                                     \
+    if (grp == G_ && g_ms_words == V_)                                                   \
+        kern = win ? ms_scan_kernel<MODE, G_, V_, true> : ms_scan_kernel<MODE, G_, V_, false>;
+    PFW_MS_PICK(8, 4)
+    PFW_MS_PICK(8, 2)
+    PFW_MS_PICK(16, 4)
+    PFW_MS_PICK(16, 2)
+    PFW_MS_PICK(32, 2)
+    PFW_MS_PICK(32, 1)
+#undef PFW_MS_PICK
+    if (!kern) return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
     int occ = g_ctas_per_sm;
     if (occ <= 0) {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MS_BLOCK, 0));

@@ -1353,6 +1353,10 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "ms_words")) {
         if (value != 1 && value != 2 && value != 4) return set_err(PFW_ERR_INVALID, "ms_words: 1, 2 or 4");
         g_ms_words = (int)value;
+    } else if (!strcmp(key, "ms_group")) {
+        if (value != 0 && value != 8 && value != 16 && value != 32)
+            return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");
+        g_ms_group = (int)value;
     } else {
         return set_err(PFW_ERR_INVALID, "unknown tuning key '%s'", key);
     }

@@ -38,7 +38,7 @@ def _reset_tuning():
     yield
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
-                 ("algo", 0), ("ms_words", 2), ("matchset", 1), ("matchset_budget_mb", 0)):
+                 ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0)):
         _native.set_tuning(k, v)
 
 
@@ -577,15 +577,23 @@ def test_match_sets_built_for_every_config_ruleset():
         assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
 
 
-@pytest.mark.parametrize("words", [1, 2, 4])
-def test_match_set_words_per_step(words):
+MS_SHAPES = [(8, 4), (8, 2), (16, 4), (16, 2), (32, 2), (32, 1)]
+
+
+@pytest.mark.parametrize("group,words", MS_SHAPES)
+def test_match_set_step_shapes(group, words):
+    """Lanes per packet x words per lane (rules per step = 32 x group x words)."""
     _native.set_tuning("algo", 2)
+    _native.set_tuning("ms_group", group)
     _native.set_tuning("ms_words", words)
     test_scan_matches_reference_golden("r2048_t1000", "r2048_s21_w15", "t1000_s22")
     test_scan_matches_reference_golden("r1000_t3000icmp", "r1000_s1", "t3000_s11_icmp")
     test_windows_every_alignment_vs_oracle()
     test_engine_models_match_reference_golden("hybrid")
+    test_engine_models_match_reference_golden("function")
     test_ragged_sizes_and_empty()
+    test_adversarial_recipe_sample()
+    test_fused_min_combine_virtual_ranks(0)
 
 
 def test_match_set_budget_falls_back_to_rule_scan():
@@ -638,5 +646,8 @@ def test_match_set_interval_edges():
     c = compiled(rules)
     assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
     _native.set_tuning("algo", 2)
-    for lo, hi in ((0, R), (1, R - 1), (31, 32), (32, 1024 % R), (300, 301), (64, 700)):
-        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+    for group, words in MS_SHAPES:
+        _native.set_tuning("ms_group", group)
+        _native.set_tuning("ms_words", words)
+        for lo, hi in ((0, R), (1, R - 1), (31, 32), (32, 1024 % R), (300, 301), (64, 700)):
+            np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
