@@ -33,7 +33,19 @@ sys.path.insert(0, ROOT)
 
 K_OPS = 10  # int32 ops per rule test: 5 fields x (compare + combine), SURVEY.md 8(d)
 INT32_LANES_PER_SM_CLK = 128  # 4 SMSP x 32 lanes, issue bound across ALU + FMA pipes
-PKT_BYTES, OUT_BYTES = 16, 4  # algorithmic HBM bytes per packet: uint4 in, uint32 index out
+PKT_BYTES, OUT_BYTES = 16, 5  # algorithmic bytes per packet: uint4 in, uint32 index + u8 verdict out
+MS_BYTES_PER_RULE = 0.5       # match-set scan: one bit per rule from each of the 4 rows
+
+
+def load_l2_peak():
+    """Measured L2 read bandwidth (tools/l2_probe.cu, committed under profiles/)."""
+    path = os.path.join(ROOT, "profiles", "l2_peak.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["l2_read_gbs"]), d.get("source", path)
+    except (OSError, ValueError, KeyError):
+        return None, None
 
 
 def load_peaks() -> dict:
@@ -62,7 +74,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20",
                  "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -102,20 +114,23 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def measured_traffic(config: str, n: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one step, from the
-    committed ncu --set full capture (profiles/traffic.json), scaled to n."""
+def measured_traffic(key: str, n: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum (and, for the match-set
+    scan, the L2 read sectors) of one step, from the committed ncu --set full
+    capture (profiles/traffic.json), scaled to n packets."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            d = json.load(fh).get(config)
+            d = json.load(fh).get(key)
     except (OSError, ValueError):
         return None
     if not d:
         return None
-    return {"bytes_per_step": round(d["dram_bytes_per_step"] * n / d["packets"]),
-            "bytes_per_packet": round(d["dram_bytes_per_step"] / d["packets"], 1),
-            "algorithmic_bytes_per_packet": PKT_BYTES + OUT_BYTES, "source": d["source"]}
+    out = {"bytes_per_step": round(d["dram_bytes_per_step"] * n / d["packets"]),
+           "bytes_per_packet": round(d["dram_bytes_per_step"] / d["packets"], 1), "source": d["source"]}
+    if "l2_read_bytes_per_step" in d:
+        out["l2_read_bytes_per_packet"] = round(d["l2_read_bytes_per_step"] / d["packets"], 1)
+    return out
 
 
 def dist_setup():
@@ -186,7 +201,7 @@ CPU_SAMPLE = {"oracle": 100_000, "data": 2_000_000, "grid": 2_000_000, "function
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="data", choices=("data", "grid", "function", "adversarial", "oracle"))
@@ -273,6 +288,9 @@ def main() -> int:
     cols = workloads.rule_columns(w)
     compiled = CompiledRuleset.from_columns(cols, device=local)
     R = compiled.num_rules
+    ms_bytes = int(_native.lib().pfw_ruleset_matchset_bytes(compiled.handle))
+    rule_scan = args.algo == 1 or args.proto_split or args.sc == 1
+    algo = "matchset" if ms_bytes and not rule_scan else "rule scan"
     weak = args.scaling == "weak" and w.model != "function"
     total_packets = w.packets * world if weak else w.packets
     if w.model == "function":
@@ -375,20 +393,38 @@ def main() -> int:
     # --- roofline for the dominant kernel (the scan), per GPU
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     clk = float(peaks.get("sm_max_mhz", 1965.0))
-    int_peak = sms * INT32_LANES_PER_SM_CLK * clk * 1e6 / 1e12  # T int-ops/s
     avg_launch_s = (total_ms / args.steps) / 1e3
-    achieved = local_comps * K_OPS / avg_launch_s / 1e12
     hbm_achieved = n * (PKT_BYTES + OUT_BYTES) / avg_launch_s / 1e9
-    roof = {
-        "bound": "int32", "achieved": round(achieved, 3), "peak": round(int_peak, 3), "unit": "Tops/s",
-        "frac": round(achieved / int_peak, 4), "traffic": measured_traffic(w.name, n),
-        "ops_per_rule_test": K_OPS, "rule_tests_per_launch": local_comps,
-        "peak_source": f"derived: {sms} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x "
-                       f"sm_max_mhz {clk:.0f} ({peaks['_source']})",
-        "hbm": {"achieved": round(hbm_achieved, 2), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                "frac": round(hbm_achieved / float(peaks.get("hbm_gbs", 6536.4)), 5),
-                "bytes_per_packet": PKT_BYTES + OUT_BYTES},
-    }
+    hbm = {"achieved": round(hbm_achieved, 2), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+           "frac": round(hbm_achieved / float(peaks.get("hbm_gbs", 6536.4)), 5),
+           "bytes_per_packet": PKT_BYTES + OUT_BYTES}
+    l2_peak, l2_src = load_l2_peak()
+    if algo == "matchset" and l2_peak:
+        # bytes the first-match search must read: one bit per rule resolved
+        # from each of the 4 rows (comparisons = the reference's algorithmic
+        # work) + the packet in / results out
+        alg_bytes = local_comps * MS_BYTES_PER_RULE + n * (PKT_BYTES + OUT_BYTES)
+        achieved = alg_bytes / avg_launch_s / 1e9
+        roof = {
+            "bound": "l2", "achieved": round(achieved, 1), "peak": l2_peak, "unit": "GB/s",
+            "frac": round(achieved / l2_peak, 4), "traffic": measured_traffic(f"{w.name}/matchset", n),
+            "algorithmic_bytes_per_launch": round(alg_bytes),
+            "algorithmic_bytes_per_packet": round(alg_bytes / max(n, 1), 1),
+            "bytes_per_rule_resolved": MS_BYTES_PER_RULE, "rules_resolved_per_launch": local_comps,
+            "peak_source": f"measured L2 read bandwidth, L2-resident buffer ({l2_src})",
+            "hbm": hbm,
+        }
+    else:
+        int_peak = sms * INT32_LANES_PER_SM_CLK * clk * 1e6 / 1e12  # T int-ops/s
+        achieved = local_comps * K_OPS / avg_launch_s / 1e12
+        roof = {
+            "bound": "int32", "achieved": round(achieved, 3), "peak": round(int_peak, 3), "unit": "Tops/s",
+            "frac": round(achieved / int_peak, 4), "traffic": measured_traffic(w.name, n),
+            "ops_per_rule_test": K_OPS, "rule_tests_per_launch": local_comps,
+            "peak_source": f"derived: {sms} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x "
+                           f"sm_max_mhz {clk:.0f} ({peaks['_source']})",
+            "hbm": hbm,
+        }
 
     # --- end to end through the C-ABI with host buffers (pfw_classify_host)
     e2e = None
@@ -448,6 +484,8 @@ def main() -> int:
                                       + (" (fused NVLink-atomic combine)" if fused is not None else
                                          " (NCCL MIN all-reduce)" if w.model == "function" else ""),
                        "l2": "flushed between timed steps (256 MiB write)",
+                       "algorithm": (f"match-set scan (per-field interval bitmaps, {ms_bytes / 2**20:.0f} MiB)"
+                                     if algo == "matchset" else "rule-by-rule scan"),
                        "rule_layout": "protocol-split chains" if args.proto_split else "single ordered table",
                        "kernel": _native.version()},
             "roofline": roof,

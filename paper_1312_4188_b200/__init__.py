@@ -23,7 +23,7 @@ from .traffic import (MatchMode, RulesetGenParams, TrafficFormatError, TrafficGe
 
 from .harness import BenchReport, SweepAxis, SweepSpec, emit_csv, run_point, run_sweep
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 
 def __getattr__(name):

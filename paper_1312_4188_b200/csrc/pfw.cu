@@ -40,7 +40,7 @@
 
 #include "../../include/pfw.h"
 
-#define PFW_VERSION "0.1.0"
+#define PFW_VERSION "0.2.0"
 
 // -DPFW_CHECKS builds device-side bounds assertions into every derived index
 // (compute-sanitizer is not available on the GPU pool): a violated check
@@ -1296,7 +1296,8 @@ extern "C" {
 const char *pfw_last_error(void) { return g_err.c_str(); }
 
 const char *pfw_version(void) {
-    return "pfw " PFW_VERSION " sm_100a range-test packet x rule grid (KS=2/4/8) + TMA bulk stage ring";
+    return "pfw " PFW_VERSION " sm_100a: match-set scan (per-field interval bitmaps, lane-group ballot) + "
+           "rule-by-rule range-test grid (KS=2/4/6/8, TMA bulk stage ring)";
 }
 
 int pfw_device_count(void) {

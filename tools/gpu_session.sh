@@ -1,7 +1,5 @@
 mkdir -p gpurun_out
-./tools/l2_probe > gpurun_out/l2_probe.txt 2>&1
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
-for cfg in data grid adversarial function oracle; do
-    timeout 300 python bench.py --config $cfg --steps 5 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$cfg', d['value'], d['ms_per_step'])"
-done
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > gpurun_out/ms_default.json 2>&1; tail -1 gpurun_out/ms_default.json | cut -c1-400
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/r1_bench.json 2>gpurun_out/r1_bench.err; tail -1 gpurun_out/r1_bench.json | cut -c1-300
+timeout 600 python bench.py --impl reference > gpurun_out/r1_ref.json 2>&1; tail -1 gpurun_out/r1_ref.json | cut -c1-200
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/r1_ncu.log 2>&1; echo ncu rc=$?

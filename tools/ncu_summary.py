@@ -21,6 +21,10 @@ KEYS = [
     ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lsu_%"),
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
+    ("lts__t_sectors_srcunit_tex_op_read.sum", "l2_read_sectors"),
+    ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_throughput_%"),
+    ("l1tex__t_sector_hit_rate.pct", "l1_hit_%"),
     ("launch__registers_per_thread", "regs"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%"),
     ("launch__grid_size", "grid"),
