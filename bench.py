@@ -133,6 +133,23 @@ def measured_traffic(key: str, n: int):
     return out
 
 
+def host_link_peaks(dev) -> dict:
+    """Pinned host -> device copy bandwidth on this box (512 MiB, best of 5,
+    CUDA events): the ceiling of the e2e path's input stream."""
+    import torch
+    src = torch.empty(512 << 20, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, src.numel() / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return {"h2d_gbs": round(best, 2), "source": "measured: pinned 512 MiB H2D copy, best of 6"}
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,6 +237,7 @@ def main() -> int:
                     help="0 auto (match sets when built), 1 rule-by-rule scan, 2 match sets")
     ap.add_argument("--ms-words", type=int, default=0, help="match-set scan: words per lane per step (1, 2, 4)")
     ap.add_argument("--ms-group", type=int, default=0, help="match-set scan: lanes per packet (8, 16, 32)")
+    ap.add_argument("--ms-summary", type=int, default=-1, help="match-set block summaries: 0 off, 1 on, 2 auto")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--sc", type=int, default=-1, help="warp-level short-circuit of the port tests (0/1)")
     ap.add_argument("--bucket", type=int, default=-1, help="group large batches by protocol (0/1)")
@@ -268,6 +286,8 @@ def main() -> int:
         _native.set_tuning("ms_words", args.ms_words)
     if args.ms_group:
         _native.set_tuning("ms_group", args.ms_group)
+    if args.ms_summary >= 0:
+        _native.set_tuning("ms_summary", args.ms_summary)
     if args.ks:
         _native.set_tuning("ks", args.ks)
     if args.sc >= 0:
@@ -458,8 +478,14 @@ def main() -> int:
             et.append(time.perf_counter() - t0)
         tt = torch.tensor([sum(et)], dtype=torch.float64, device=dev)
         parallel.all_reduce(tt, dist.ReduceOp.MAX)
+        e2e_s = float(tt.item()) / args.steps
+        link = host_link_peaks(dev)
         e2e = {"value": pk_per_step * args.steps / float(tt.item()) / 1e6, "unit": "Mpps",
                "h2d_bytes_per_step": n * 13, "d2h_bytes_per_step": n * 5,
+               # the host link bounds this path: H2D of the 13-byte columns
+               "h2d_gbs": round(n * 13 / e2e_s / 1e9, 2), "h2d_peak_gbs": link["h2d_gbs"],
+               "h2d_frac": round(n * 13 / e2e_s / 1e9 / link["h2d_gbs"], 4),
+               "link_peak_source": link["source"],
                "api": f"pfw_classify_host_columns (C-ABI, the reference's PacketArrays columns in "
                       f"pinned host memory, {args.e2e_chunk}-packet chunks, copy-in / 2x compute / "
                       "copy-out streams, 3 slots)"}

@@ -209,7 +209,8 @@ int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t 
  * "algo" (0 auto: match sets when built, 1 rule-by-rule scan, 2 match sets),
  * "matchset" (build match sets at ruleset creation, default 1),
  * "matchset_budget_mb" (0 = a quarter of free device memory), "ms_group"
- * (lanes per packet), "ms_words" (words per lane per step),
+ * (lanes per packet), "ms_words" (words per lane per step), "ms_summary" (1024-rule
+ * block summaries: 0 off, 1 on, 2 auto; applies to rulesets created afterwards),
  * and the rule-scan options "ks", "tile", "first_pass", "bucket",
  * "bucket_min", "proto_split", "short_circuit", "force_imad", "ctas_per_sm". */
 int64_t pfw_launch_count(void);

@@ -34,6 +34,8 @@ int g_algo = 0;                // 0 auto (match sets when built), 1 rule-by-rule
 int64_t g_ms_budget_mb = 0;    // device-memory budget for the tables (0 = a quarter of free memory)
 int g_ms_group = 0;            // lanes per packet (8, 16, 32; 0 = by ruleset size): 32 / group packets in flight per warp
 int g_ms_words = 4;            // words per lane per step: 32 * group * words rules per step
+int g_ms_summary = 2;          // block summaries: 0 off, 1 on, 2 auto (built and used when they skip enough)
+constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 
 struct MsBuildArgs {
     const uint32_t *base, *mask;  // IP fields
@@ -88,6 +90,30 @@ __global__ void __launch_bounds__(MS_BLOCK) ms_build_kernel(MsBuildArgs a) {
     }
 }
 
+// Summary rows: warp per (row, summary word j); lane k ORs block 32j+k's 32
+// words (eight 16-byte loads) and one ballot forms the word.
+__global__ void __launch_bounds__(MS_BLOCK) ms_sum_kernel(const uint32_t *bits, int64_t rows, int64_t wp,
+                                                          int64_t sw, uint32_t *sum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    const int64_t blocks = wp / 32;
+    for (int64_t t = gw; t < rows * sw; t += nw) {
+        const int64_t row = t / sw, j = t - row * sw, blk = j * 32 + lane;
+        uint32_t any = 0;
+        if (blk < blocks) {
+            const uint4 *q = reinterpret_cast<const uint4 *>(bits + row * wp + blk * 32);
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint4 v = __ldg(q + k);
+                any |= v.x | v.y | v.z | v.w;
+            }
+        }
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, any != 0u);
+        if (lane == 0) sum[row * sw + j] = b;
+    }
+}
+
 struct MsView {
     const uint32_t *bits[4];
     const uint32_t *ipb[2];   // src / dst boundaries
@@ -97,6 +123,13 @@ struct MsView {
     int64_t wp;
     uint32_t sp_rows;
 };
+
+// Block summaries (SUM variant only; the other variants take the empty type)
+struct MsSum {
+    const uint32_t *sum[4];   // summary rows: bit k = block k of the row non-zero
+    uint32_t sw;              // summary words per row
+};
+struct MsNoSum {};
 
 // interval of an IP: index of the last boundary <= ip (boundary 0 is 0)
 __device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint2 *c, uint32_t ip) {
@@ -173,12 +206,21 @@ struct MsStep<1> {
 // WIN: the window is not the whole table, so the first / last step mask
 // words outside it (a whole-table scan needs no masks: bits past the last
 // rule are zero and rows are whole steps long).
-template <int MODE, int G, int V, bool WIN>
-__global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanParams p, MsView t) {
+// SUM (G*V = 32 words: one step = one 1024-rule block): with the first step
+// a group also loads the packet's four summary rows (bit k = block k of the
+// row has a bit set; lane gl holds blocks 32*gl..32*gl+31) and ANDs them;
+// later steps jump to the next block whose AND-summary bit is set, skipping
+// blocks no rule of which can match this packet (a set bit may still be a
+// false candidate: the block is then read and the search moves on).
+template <int MODE, int G, int V, bool WIN, bool SUM = false>
+__global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
+    ms_scan_kernel(ScanParams p, MsView t, std::conditional_t<SUM, MsSum, MsNoSum> u) {
+    static_assert(!SUM || G * V == 32, "summary blocks are one step");
     constexpr int P = 32 / G;                      // packets in flight per warp
     constexpr uint32_t STEP = (uint32_t)G * V;     // words per step
     constexpr uint32_t GMASK = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
     __shared__ uint4 s_off[MS_BLOCK / 32][32];     // per warp: row offsets of the batch's packets
+    __shared__ uint4 s_row[SUM ? MS_BLOCK / 32 : 1][32];  // per warp: row indices (SUM)
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];  // per warp: first match of the batch's packets
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
@@ -223,6 +265,9 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanPara
             o.z = ((uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16))) * wp + cbeg;
             o.w = __ldg(t.port[1] + (v.z & 0xFFFFu)) * wp + cbeg;
             s_off[warp][lane] = o;
+            if (SUM)
+                s_row[SUM ? warp : 0][lane] = make_uint4((o.x - cbeg) / wp, (o.y - cbeg) / wp, (o.z - cbeg) / wp,
+                                                         (o.w - cbeg) / wp);
         }
         s_res[warp][lane] = PFW_NO_MATCH;
         __syncwarp();
@@ -236,6 +281,8 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanPara
             int next = P;
             int s = 0;
             uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
+            uint32_t scand = 0;  // SUM: candidate blocks after the current one (this lane's 32)
+            const uint32_t b0 = cbeg / 32u, blast = whi / 32u;  // SUM: first / last block
             if (pj >= 0) {
                 const uint4 o = s_off[warp][pj];
                 o0 = o.x + lv;
@@ -248,6 +295,23 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanPara
                 uint32_t x[V], any = 0u;
 #pragma unroll
                 for (int v = 0; v < V; v++) x[v] = 0u;
+                if constexpr (SUM) {
+                    if (act && s == 0) {
+                        // the packet's first step: its AND-summary, restricted
+                        // to the blocks after this one, up to the window's last
+                        scand = 0u;
+                        if ((uint32_t)gl < u.sw) {
+                            const uint4 rw = s_row[SUM ? warp : 0][pj];
+                            scand = __ldg(u.sum[0] + (size_t)rw.x * u.sw + gl) &
+                                    __ldg(u.sum[1] + (size_t)rw.y * u.sw + gl) &
+                                    __ldg(u.sum[2] + (size_t)rw.z * u.sw + gl) &
+                                    __ldg(u.sum[3] + (size_t)rw.w * u.sw + gl);
+                            const int rel0 = (int)b0 - 32 * gl, rel1 = (int)blast - 32 * gl;
+                            scand &= rel0 < 0 ? 0xFFFFFFFFu : (rel0 >= 31 ? 0u : (0xFFFFFFFFu << (rel0 + 1)));
+                            scand &= rel1 < 0 ? 0u : (rel1 >= 31 ? 0xFFFFFFFFu : ((2u << rel1) - 1u));
+                        }
+                    }
+                }
                 if (act) {
                     MsStep<V> st;
                     st.load(t.bits[0] + o0, t.bits[1] + o1, t.bits[2] + o2, t.bits[3] + o3);
@@ -277,7 +341,21 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanPara
                                                   gbase + (__ffs(gbits) - 1) * (gbits != 0u));
                 const bool found = gbits != 0u;  // (idle groups have no bits)
                 if (found && gl == 0) s_res[warp][pj] = cand;
-                const bool done = act && (found || s + 1 >= nsteps);
+                bool done = act && (found || s + 1 >= nsteps);
+                int ns = s + 1;  // next step (SUM: the next candidate block)
+                if constexpr (SUM) {
+                    // next candidate block of the groups still searching
+                    const uint32_t cm = (act && !found) ? scand : 0u;
+                    const uint32_t cbits = (__ballot_sync(0xFFFFFFFFu, cm != 0u) >> gbase) & GMASK;
+                    const int nb = __shfl_sync(0xFFFFFFFFu, 32 * gl + __ffs(cm) - 1,
+                                               gbase + (__ffs(cbits) - 1) * (cbits != 0u));
+                    done = act && (found || cbits == 0u);
+                    if (!done && act) {
+                        ns = nb - (int)b0;
+                        const int rel = nb - 32 * gl;  // drop candidates up to nb
+                        scand &= rel < 0 ? 0xFFFFFFFFu : (rel >= 31 ? 0u : (0xFFFFFFFFu << (rel + 1)));
+                    }
+                }
                 const unsigned dmask = __ballot_sync(0xFFFFFFFFu, done && gl == 0);
                 if (done) {
                     // take the next packet (rank of this group among the done ones)
@@ -292,11 +370,20 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanPara
                         o3 = o.w + lv;
                     }
                 } else if (act) {
-                    s++;
-                    o0 += STEP;
-                    o1 += STEP;
-                    o2 += STEP;
-                    o3 += STEP;
+                    if constexpr (SUM) {
+                        const uint32_t adv = (uint32_t)(ns - s) * STEP;
+                        s = ns;
+                        o0 += adv;
+                        o1 += adv;
+                        o2 += adv;
+                        o3 += adv;
+                    } else {
+                        s++;
+                        o0 += STEP;
+                        o1 += STEP;
+                        o2 += STEP;
+                        o3 += STEP;
+                    }
                 }
                 next += __popc(dmask);
             }
@@ -325,6 +412,8 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB) ms_scan_kernel(ScanPara
 void ms_free(MatchSet *m) {
     if (!m) return;
     for (auto *b : m->d_bits)
+        if (b) cudaFree(b);
+    for (auto *b : m->d_sum)
         if (b) cudaFree(b);
     for (auto *b : m->d_ipb)
         if (b) cudaFree(b);
@@ -372,6 +461,62 @@ cudaError_t ms_upload(T **d, const T *h, size_t count) {
     cudaError_t e = cudaMalloc(d, count * sizeof(T) + 16);
     if (e == cudaSuccess && count) e = cudaMemcpy(*d, h, count * sizeof(T), cudaMemcpyHostToDevice);
     return e;
+}
+
+// Block summaries (one bit per 1024-rule block per row) and the auto decision:
+// the expected fraction of blocks a packet's AND-summary keeps, for packet
+// fields uniform over their domains -- per dimension the interval-length-
+// weighted fraction of set summary bits, multiplied over the dimensions.
+// Random rulesets keep ~100% (every 1024-rule block has some rule matching
+// any value), so they scan without; rulesets whose rules cluster (e.g. the
+// adversarial recipe's decoys, all in 128.0.0.0/1) skip most blocks.
+int ms_summaries(pfw_ruleset *h, const std::vector<uint32_t> &bs, const std::vector<uint32_t> &bd,
+                 const std::vector<uint32_t> &bsp, const std::vector<uint32_t> &bdp) {
+    MatchSet *m = h->ms;
+    const int64_t blocks = m->wp / 32;             // blocks per row (incl. the padding of the last step)
+    const int64_t real = (h->n + 1023) / 1024;     // blocks holding rules
+    if (!g_ms_summary || real < 2 || blocks > 32 * 8) return PFW_OK;  // 8 lanes x 32 blocks
+    const int64_t sw = (blocks + 31) / 32;
+    cudaError_t e = cudaSuccess;
+    for (int d = 0; d < 4 && e == cudaSuccess; d++) e = cudaMalloc(&m->d_sum[d], ((size_t)m->rows[d] * sw + 8) * 4);
+    for (int d = 0; d < 4 && e == cudaSuccess; d++) {
+        ms_sum_kernel<<<(unsigned)(h->sms * 8), MS_BLOCK>>>(m->d_bits[d], m->rows[d], m->wp, sw, m->d_sum[d]);
+        g_launches++;
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    double keep = 1.0;
+    const std::vector<uint32_t> *bnd[4] = {&bs, &bd, &bsp, &bdp};
+    for (int d = 0; d < 4 && e == cudaSuccess; d++) {
+        std::vector<uint32_t> hs((size_t)m->rows[d] * sw);
+        e = cudaMemcpy(hs.data(), m->d_sum[d], hs.size() * 4, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) break;
+        const std::vector<uint32_t> &b = *bnd[d];
+        const double dom = d < 2 ? 4294967296.0 : 65536.0;
+        double acc = 0.0, wsum = 0.0;
+        for (int64_t row = 0; row < m->rows[d]; row++) {
+            const int64_t i = d == MSD_SPORT ? row % m->sp_rows : row;  // every protocol class weighs alike
+            const double len = (i + 1 < (int64_t)b.size() ? (double)b[(size_t)i + 1] : dom) - (double)b[(size_t)i];
+            int ones = 0;
+            for (int64_t j = 0; j < sw; j++) ones += __builtin_popcount(hs[(size_t)(row * sw + j)]);
+            acc += len * ones / (double)real;
+            wsum += len;
+        }
+        keep *= wsum > 0 ? acc / wsum : 1.0;
+    }
+    if (e != cudaSuccess) {
+        for (auto *&q : m->d_sum)
+            if (q) cudaFree(q), q = nullptr;
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            return PFW_OK;
+        }
+        return set_err(PFW_ERR_CUDA, "match-set summaries failed: %s", cudaGetErrorString(e));
+    }
+    m->sw = sw;
+    m->sum_keep = keep;
+    m->use_sum = g_ms_summary == 1 || keep < MS_SUM_KEEP_MAX;
+    for (int d = 0; d < 4; d++) m->bytes += ((size_t)m->rows[d] * sw + 8) * 4;
+    return PFW_OK;
 }
 
 // Build the match sets of ruleset h (host columns as given to
@@ -519,7 +664,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
         return set_err(PFW_ERR_CUDA, "match-set build failed: %s", cudaGetErrorString(e));
     }
     h->ms = m;
-    return PFW_OK;
+    return ms_summaries(h, bs, bd, bsp, bdp);
 }
 
 template <int MODE>
@@ -536,12 +681,19 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     t.cls = m->d_cls;
     t.wp = m->wp;
     t.sp_rows = (uint32_t)m->sp_rows;
-    void (*kern)(ScanParams, MsView) = nullptr;
+    MsSum u{};
+    for (int d = 0; d < 4; d++) u.sum[d] = m->d_sum[d];
+    u.sw = (uint32_t)m->sw;
+    void (*kern)(ScanParams, MsView, MsNoSum) = nullptr;
+    void (*kern_s)(ScanParams, MsView, MsSum) = nullptr;
     const bool win = !(p.lo == 0 && p.hi == h->n);
     // auto: 8 lanes (4 packets in flight, 1024-rule steps) while the rows'
     // leading lines fit in L2; 16 lanes (2048-rule steps, fewer iterations)
     // for large rulesets whose scans run long and mostly miss L2
     const int grp = g_ms_group ? g_ms_group : (h->n > 16384 ? 16 : 8);
+    // block summaries: one step = one 1024-rule block (8 lanes x 4 words)
+    const bool sum = m->use_sum && m->sw > 0 && g_ms_summary != 0 && g_ms_words == 4 &&
+                     (g_ms_group == 0 || g_ms_group == 8);
 #define PFW_MS_PICK(G_, V_)                                                                     \
     if (grp == G_ && g_ms_words == V_)                                                   \
         kern = win ? ms_scan_kernel<MODE, G_, V_, true> : ms_scan_kernel<MODE, G_, V_, false>;
@@ -552,17 +704,20 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     PFW_MS_PICK(32, 2)
     PFW_MS_PICK(32, 1)
 #undef PFW_MS_PICK
-    if (!kern) return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
+    if (sum) kern_s = win ? ms_scan_kernel<MODE, 8, 4, true, true> : ms_scan_kernel<MODE, 8, 4, false, true>;
+    if (!kern && !kern_s) return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
     int occ = g_ctas_per_sm;
     if (occ <= 0) {
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MS_BLOCK, 0));
+        if (kern_s) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_s, MS_BLOCK, 0));
+        else CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MS_BLOCK, 0));
         if (occ < 1) occ = 1;
     }
     int64_t grid = (int64_t)h->sms * occ;
     const int64_t need = (p.n + MS_BLOCK - 1) / MS_BLOCK;  // one 32-packet batch per warp
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t);
+    if (kern_s) kern_s<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, u);
+    else kern<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, MsNoSum{});
     CUDA_TRY(cudaGetLastError());
     g_launches++;
     return PFW_OK;

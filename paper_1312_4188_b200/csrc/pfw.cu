@@ -37,6 +37,7 @@
 #include <vector>
 #include <atomic>
 #include <algorithm>
+#include <type_traits>
 
 #include "../../include/pfw.h"
 
@@ -149,6 +150,11 @@ struct MatchSet {
     uint8_t *d_cls = nullptr;   // protocol -> class (256 entries)
     int64_t sp_rows = 0;        // sport intervals = rows per protocol class
     size_t bytes = 0;           // device bytes of all of the above
+    // summaries: bit k of a row's summary = block k (1024 rules) of the row non-zero
+    uint32_t *d_sum[4] = {};
+    int64_t sw = 0;             // summary words per row (0: not built)
+    double sum_keep = 1.0;      // expected fraction of blocks a packet's AND-summary keeps
+    bool use_sum = false;       // scan with summaries (auto: sum_keep below the threshold)
 };
 
 struct pfw_ruleset {
@@ -1354,6 +1360,9 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "ms_words")) {
         if (value != 1 && value != 2 && value != 4) return set_err(PFW_ERR_INVALID, "ms_words: 1, 2 or 4");
         g_ms_words = (int)value;
+    } else if (!strcmp(key, "ms_summary")) {
+        if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_summary: 0 off, 1 on, 2 auto");
+        g_ms_summary = (int)value;
     } else if (!strcmp(key, "ms_group")) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");

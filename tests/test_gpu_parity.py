@@ -38,7 +38,8 @@ def _reset_tuning():
     yield
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
-                 ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0)):
+                 ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
+                 ("ms_summary", 2)):
         _native.set_tuning(k, v)
 
 
@@ -651,3 +652,26 @@ def test_match_set_interval_edges():
         _native.set_tuning("ms_words", words)
         for lo, hi in ((0, R), (1, R - 1), (31, 32), (32, 1024 % R), (300, 301), (64, 700)):
             np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+
+
+@pytest.mark.parametrize("summary", [0, 1])
+def test_match_set_block_summaries(summary):
+    """Block summaries (skip 1024-rule blocks whose AND-summary is zero) forced
+    off / on: goldens, windows, engines, the adversarial recipe (where the auto
+    mode turns them on) -- identical results."""
+    _native.set_tuning("ms_summary", summary)   # applies to rulesets built from here on
+    _native.set_tuning("algo", 2)
+    test_adversarial_recipe_sample()
+    test_scan_matches_reference_golden("r2048_t1000", "r2048_s21_w15", "t1000_s22")
+    test_scan_matches_reference_golden("oracle_r1000_t100000", "r1000_s1", "t100000_s2")
+    test_windows_every_alignment_vs_oracle()
+    for model in ("function", "hybrid"):
+        test_engine_models_match_reference_golden(model)
+    test_function_parallel_100k_rules()
+    test_fused_min_combine_virtual_ranks(1)
+    # windows over the adversarial ruleset: blocks skipped inside partial windows
+    rules = oracle.adversarial_rules(50_000)
+    pk = oracle.adversarial_traffic(6_000)
+    c = compiled(rules)
+    for lo, hi in ((0, 50_000), (1, 49_999), (1000, 45_001), (44_999, 45_003), (45_001, 50_000), (30_000, 30_001)):
+        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))

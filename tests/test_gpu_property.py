@@ -72,21 +72,24 @@ def rules_and_packets(draw):
 @pytest.fixture(autouse=True)
 def _reset():
     yield
-    for k, v in (("proto_split", 0), ("first_pass", 1024), ("ks", 8), ("algo", 0), ("ms_group", 0), ("ms_words", 4)):
+    for k, v in (("proto_split", 0), ("first_pass", 1024), ("ks", 8), ("algo", 0), ("ms_group", 0), ("ms_words", 4),
+                 ("ms_summary", 2)):
         _native.set_tuning(k, v)
 
 
 @settings(max_examples=90, deadline=None, suppress_health_check=list(HealthCheck))
 @given(case=rules_and_packets(), mode=st.sampled_from(["matchset", "rule", "split"]),
        fp=st.sampled_from([32, 64, 1024]),
-       shape=st.sampled_from([(8, 4), (8, 2), (16, 4), (16, 2), (32, 2), (32, 1)]))
-def test_random_boundary_cases_bit_exact(case, mode, fp, shape):
+       shape=st.sampled_from([(8, 4), (8, 2), (16, 4), (16, 2), (32, 2), (32, 1)]),
+       summary=st.sampled_from([0, 1]))
+def test_random_boundary_cases_bit_exact(case, mode, fp, shape, summary):
     """Match-set scan, rule-by-rule scan and protocol-split chains on the same
     boundary-heavy random cases."""
     cols, pk, lo, hi = case
     _native.set_tuning("algo", {"matchset": 2, "rule": 1, "split": 1}[mode])
     _native.set_tuning("proto_split", int(mode == "split"))
     _native.set_tuning("first_pass", fp)
+    _native.set_tuning("ms_summary", summary)
     _native.set_tuning("ms_group", shape[0])
     _native.set_tuning("ms_words", shape[1])
     c = pfw.CompiledRuleset.from_columns(cols, device=0)

@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 600 python bench.py > gpurun_out/r1_bench.json 2>gpurun_out/r1_bench.err; tail -1 gpurun_out/r1_bench.json | cut -c1-300
-timeout 600 python bench.py --impl reference > gpurun_out/r1_ref.json 2>&1; tail -1 gpurun_out/r1_ref.json | cut -c1-200
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/r1_ncu.log 2>&1; echo ncu rc=$?
+timeout 900 python -m pytest tests -x -q -m gpu -k "not fullsize" 2>&1 | tail -3
+for cfg in adversarial data function grid; do
+  for sm in 0 1 2; do
+    timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu --no-e2e --ms-summary $sm 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$cfg summary $sm', d['value'], d['ms_per_step'])"
+  done
+done
