@@ -384,6 +384,16 @@ def main() -> int:
         torch.cuda.synchronize()
     # algorithmic work of one step: sum of this rank's (per-task) comparisons
     local_comps = int(stats[0].item())
+    # the match-set scan with block summaries skips blocks: count the blocks it
+    # reads in one extra (untimed) step for its roofline
+    blocks_read = 0
+    if algo == "matchset":
+        _native.read_counter("blocks_read")
+        _native.set_tuning("count_blocks", 1)
+        step()
+        torch.cuda.synchronize()
+        _native.set_tuning("count_blocks", 0)
+        blocks_read = _native.read_counter("blocks_read")
 
     times = []
     launches0 = _native.launch_count()
@@ -420,17 +430,30 @@ def main() -> int:
            "bytes_per_packet": PKT_BYTES + OUT_BYTES}
     l2_peak, l2_src = load_l2_peak()
     if algo == "matchset" and l2_peak:
-        # bytes the first-match search must read: one bit per rule resolved
-        # from each of the 4 rows (comparisons = the reference's algorithmic
-        # work) + the packet in / results out
-        alg_bytes = local_comps * MS_BYTES_PER_RULE + n * (PKT_BYTES + OUT_BYTES)
+        if blocks_read:
+            # block summaries: the search reads the packet's 4 summary rows
+            # (sw words each) and the 4 rows' 128-byte line of every block it
+            # visits (counted by the kernel) + the packet in / results out
+            wp = -(-(-(-R // 32)) // 128) * 128
+            sw = -(-(wp // 32) // 32)
+            alg_bytes = blocks_read * 4 * 128 + n * (4 * 4 * sw + PKT_BYTES + OUT_BYTES)
+            model = {"bytes_model": "block summaries: 4 rows x 128 B per block read (kernel-counted) + "
+                                    "4 x 4 B x summary words + 21 B packet in / results out",
+                     "blocks_read_per_launch": blocks_read,
+                     "blocks_read_per_packet": round(blocks_read / max(n, 1), 2)}
+        else:
+            # bytes the first-match search must read: one bit per rule resolved
+            # from each of the 4 rows (comparisons = the reference's algorithmic
+            # work) + the packet in / results out
+            alg_bytes = local_comps * MS_BYTES_PER_RULE + n * (PKT_BYTES + OUT_BYTES)
+            model = {"bytes_model": "0.5 B per rule resolved (1 bit x 4 rows) + 21 B packet in / results out",
+                     "bytes_per_rule_resolved": MS_BYTES_PER_RULE, "rules_resolved_per_launch": local_comps}
         achieved = alg_bytes / avg_launch_s / 1e9
         roof = {
             "bound": "l2", "achieved": round(achieved, 1), "peak": l2_peak, "unit": "GB/s",
             "frac": round(achieved / l2_peak, 4), "traffic": measured_traffic(f"{w.name}/matchset", n),
             "algorithmic_bytes_per_launch": round(alg_bytes),
-            "algorithmic_bytes_per_packet": round(alg_bytes / max(n, 1), 1),
-            "bytes_per_rule_resolved": MS_BYTES_PER_RULE, "rules_resolved_per_launch": local_comps,
+            "algorithmic_bytes_per_packet": round(alg_bytes / max(n, 1), 1), **model,
             "peak_source": f"measured L2 read bandwidth, L2-resident buffer ({l2_src})",
             "hbm": hbm,
         }
@@ -510,7 +533,8 @@ def main() -> int:
                                       + (" (fused NVLink-atomic combine)" if fused is not None else
                                          " (NCCL MIN all-reduce)" if w.model == "function" else ""),
                        "l2": "flushed between timed steps (256 MiB write)",
-                       "algorithm": (f"match-set scan (per-field interval bitmaps, {ms_bytes / 2**20:.0f} MiB)"
+                       "algorithm": (f"match-set scan (per-field interval bitmaps, {ms_bytes / 2**20:.0f} MiB"
+                                     + (", block summaries" if blocks_read else "") + ")"
                                      if algo == "matchset" else "rule-by-rule scan"),
                        "rule_layout": "protocol-split chains" if args.proto_split else "single ordered table",
                        "kernel": _native.version()},

@@ -214,6 +214,10 @@ int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t 
  * and the rule-scan options "ks", "tile", "first_pass", "bucket",
  * "bucket_min", "proto_split", "short_circuit", "force_imad", "ctas_per_sm". */
 int64_t pfw_launch_count(void);
+/* Instrumentation counters, read and reset: "blocks_read" = 1024-rule blocks
+ * the match-set scan with block summaries read (counted while tuning
+ * "count_blocks" is 1; used by bench.py for that variant's roofline). */
+int pfw_read_counter(const char *name, int64_t *value);
 int pfw_set_tuning(const char *key, int64_t value);
 
 #ifdef __cplusplus

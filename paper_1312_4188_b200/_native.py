@@ -67,6 +67,7 @@ _SIGS = {
     "pfw_parse_traffic": (_I32, [_P, _I64, _I64, _P, _P, ctypes.POINTER(_I64)]),
     "pfw_format_results": (_I32, [_P, _P, _P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
     "pfw_launch_count": (_I64, []),
+    "pfw_read_counter": (_I32, [ctypes.c_char_p, ctypes.POINTER(_I64)]),
     "pfw_set_tuning": (_I32, [ctypes.c_char_p, _I64]),
 }
 
@@ -119,6 +120,13 @@ def require_device() -> None:
 
 def launch_count() -> int:
     return int(lib().pfw_launch_count())
+
+
+def read_counter(name: str) -> int:
+    """Read and reset an instrumentation counter (pfw_read_counter)."""
+    v = ctypes.c_int64(0)
+    check(lib().pfw_read_counter(name.encode(), ctypes.byref(v)), f"pfw_read_counter({name})")
+    return int(v.value)
 
 
 def set_tuning(key: str, value: int) -> None:

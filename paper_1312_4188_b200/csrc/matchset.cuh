@@ -36,6 +36,8 @@ int g_ms_group = 0;            // lanes per packet (8, 16, 32; 0 = by ruleset si
 int g_ms_words = 4;            // words per lane per step: 32 * group * words rules per step
 int g_ms_summary = 2;          // block summaries: 0 off, 1 on, 2 auto (built and used when they skip enough)
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
+int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
+unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
 
 struct MsBuildArgs {
     const uint32_t *base, *mask;  // IP fields
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
         mlast[v] = wl > whi ? 0u : (wl == whi ? (0xFFFFFFFFu >> (31 - ((p.hi - 1) & 31))) : 0xFFFFFFFFu);
     }
     const uint32_t lv = (uint32_t)gl * V;
-    unsigned long long st_sum = 0;
+    unsigned long long st_sum = 0, st_blocks = 0;
     unsigned st_max = 0;
 
     for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
             int s = 0;
             uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
             uint32_t scand = 0;  // SUM: candidate blocks after the current one (this lane's 32)
+            unsigned nrd = 0;    // SUM: block reads of this lane's group (counted on lane gl == 0)
             const uint32_t b0 = cbeg / 32u, blast = whi / 32u;  // SUM: first / last block
             if (pj >= 0) {
                 const uint4 o = s_off[warp][pj];
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         }
                     }
                 }
+                if (SUM && act && gl == 0) nrd++;
                 if (act) {
                     MsStep<V> st;
                     st.load(t.bits[0] + o0, t.bits[1] + o1, t.bits[2] + o2, t.bits[3] + o3);
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 }
                 next += __popc(dmask);
             }
+            if constexpr (SUM) st_blocks += nrd;
         }
         __syncwarp();
         if (i < n) {
@@ -405,6 +410,13 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
         if (lane == 0) {
             if (st_sum) atomicAdd(&p.stats[0], st_sum);
             if (st_max) atomicMax(&p.stats[1], (unsigned long long)st_max);
+        }
+    }
+    if constexpr (SUM) {
+        if (p.blocks_read) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) st_blocks += __shfl_xor_sync(0xFFFFFFFFu, st_blocks, o);
+            if (lane == 0 && st_blocks) atomicAdd(p.blocks_read, st_blocks);
         }
     }
 }
@@ -716,7 +728,17 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     const int64_t need = (p.n + MS_BLOCK - 1) / MS_BLOCK;  // one 32-packet batch per warp
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    if (kern_s) kern_s<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, u);
+    if (kern_s) {
+        ScanParams pc = p;
+        if (g_count_blocks) {
+            if (!g_counter_dev) {
+                CUDA_TRY(cudaMalloc(&g_counter_dev, sizeof(unsigned long long)));
+                CUDA_TRY(cudaMemset(g_counter_dev, 0, sizeof(unsigned long long)));
+            }
+            pc.blocks_read = g_counter_dev;
+        }
+        kern_s<<<(unsigned)grid, MS_BLOCK, 0, st>>>(pc, t, u);
+    }
     else kern<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, MsNoSum{});
     CUDA_TRY(cudaGetLastError());
     g_launches++;

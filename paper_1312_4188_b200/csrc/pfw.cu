@@ -232,6 +232,7 @@ struct ScanParams {
     uint8_t *verdict;
     unsigned long long *stats;
     unsigned int *tile_counter;
+    unsigned long long *blocks_read;  // match-set scan with summaries: block reads (null = not counted)
     int tile;
     uint32_t one;  // runtime 1: keeps ptxas from folding x*1+c into IADD3
     // MODE_PEER (fused function-parallel combine): result buffers of every
@@ -1317,6 +1318,19 @@ int pfw_device_count(void) {
 
 int64_t pfw_launch_count(void) { return g_launches.load(); }
 
+int pfw_read_counter(const char *name, int64_t *value) {
+    if (!name || !value) return set_err(PFW_ERR_INVALID, "null argument");
+    if (strcmp(name, "blocks_read")) return set_err(PFW_ERR_INVALID, "unknown counter '%s'", name);
+    *value = 0;
+    if (!g_counter_dev) return PFW_OK;
+    unsigned long long v = 0;
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(&v, g_counter_dev, sizeof v, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemset(g_counter_dev, 0, sizeof v));
+    *value = (int64_t)v;
+    return PFW_OK;
+}
+
 static uint32_t f2u(float f) {
     uint32_t u;
     memcpy(&u, &f, 4);
@@ -1360,6 +1374,8 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "ms_words")) {
         if (value != 1 && value != 2 && value != 4) return set_err(PFW_ERR_INVALID, "ms_words: 1, 2 or 4");
         g_ms_words = (int)value;
+    } else if (!strcmp(key, "count_blocks")) {
+        g_count_blocks = value != 0;
     } else if (!strcmp(key, "ms_summary")) {
         if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_summary: 0 off, 1 on, 2 auto");
         g_ms_summary = (int)value;

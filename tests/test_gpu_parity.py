@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2)):
+                 ("ms_summary", 2), ("count_blocks", 0)):
         _native.set_tuning(k, v)
 
 
@@ -675,3 +675,15 @@ def test_match_set_block_summaries(summary):
     c = compiled(rules)
     for lo, hi in ((0, 50_000), (1, 49_999), (1000, 45_001), (44_999, 45_003), (45_001, 50_000), (30_000, 30_001)):
         np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+    # the block-read counter (bench roofline): only the summary variant counts
+    _native.read_counter("blocks_read")
+    _native.set_tuning("count_blocks", 1)
+    try:
+        c.scan_range(dev_pkts(pk), 0, 50_000)
+        got = _native.read_counter("blocks_read")
+    finally:
+        _native.set_tuning("count_blocks", 0)
+    if summary:
+        assert len(pk["proto"]) <= got < len(pk["proto"]) * 49 // 4   # most decoy blocks skipped
+    else:
+        assert got == 0
