@@ -1,6 +1,7 @@
 """Full-size parity: every BASELINE.json configuration at its full size, the
 CUDA path against the C oracle (all host threads), bit-exact on every packet:
-first-match index, verdict, and the comparison counters.
+first-match index, verdict, and the comparison counters -- for both scans
+(the match-set scan and the rule-by-rule scan) against one oracle answer.
 
     data-parallel 10K rules x 64Mi packets, grid 4096 x 16Mi, function-parallel
     100K rules x 16Mi (G = 1 and the 8-way partitioned model on a subsample),
@@ -17,29 +18,29 @@ pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 import paper_1312_4188_b200 as pfw  # noqa: E402
-from paper_1312_4188_b200 import workloads  # noqa: E402
+from paper_1312_4188_b200 import _native, workloads  # noqa: E402
 from paper_1312_4188_b200.classifier import NO_MATCH  # noqa: E402
 from oracle import oracle  # noqa: E402
 
 
-def gpu_scan(w):
+def gpu_scan(c, p):
     import torch
-    cols = workloads.rule_columns(w)
-    c = pfw.CompiledRuleset.from_columns(cols, device=0)
-    p = workloads.packets(w, 0, w.packets, 0)
     n = len(p)
     verdict = torch.empty(n, dtype=torch.uint8, device="cuda:0")
     stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
     first = c.scan_range_device(p, 0, c.num_rules, verdict=verdict, stats=stats)
     f = first.cpu().numpy().astype(np.int64)
     f[f == NO_MATCH] = -1
-    return cols, p, f, verdict.cpu().numpy(), stats.cpu().tolist()
+    return f, verdict.cpu().numpy(), stats.cpu().tolist()
 
 
 @pytest.mark.parametrize("name", ["oracle", "grid", "data", "adversarial", "function"])
 def test_baseline_config_full_size_bit_exact(name):
     w = workloads.WORKLOADS[name]
-    cols, p, got, verdict, stats = gpu_scan(w)
+    cols = workloads.rule_columns(w)
+    c = pfw.CompiledRuleset.from_columns(cols, device=0)
+    assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
+    p = workloads.packets(w, 0, w.packets, 0)
     host = p.columns()
     # the device generator reproduces the reference stream (oracle C generator)
     if name == "adversarial":
@@ -49,13 +50,19 @@ def test_baseline_config_full_size_bit_exact(name):
     for f in oracle.PKT_FIELDS:
         np.testing.assert_array_equal(host[f], ref_pk[f])
     want = oracle.scan_range(cols, ref_pk, 0, w.rules)
-    np.testing.assert_array_equal(got, want)
     acc = np.zeros(len(want), np.uint8)
     hit = want >= 0
     acc[hit] = cols["action_accept"][want[hit]]
-    np.testing.assert_array_equal(verdict, acc)
     comps = oracle.sequential_comparisons(want, w.rules)
-    assert stats == [int(comps.sum()), int(comps.max())]
+    try:
+        for algo in (0, 1):  # match-set scan, rule-by-rule scan
+            _native.set_tuning("algo", algo)
+            got, verdict, stats = gpu_scan(c, p)
+            np.testing.assert_array_equal(got, want)
+            np.testing.assert_array_equal(verdict, acc)
+            assert stats == [int(comps.sum()), int(comps.max())]
+    finally:
+        _native.set_tuning("algo", 0)
 
 
 def test_function_parallel_8_partitions_full_rules():

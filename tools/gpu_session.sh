@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -x -q -m gpu -k "not fullsize" 2>&1 | tail -3
-for cfg in adversarial data; do
-  timeout 300 python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu > gpurun_out/b_$cfg.json 2>&1; tail -1 gpurun_out/b_$cfg.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$cfg', d['value'], r['frac'], r.get('blocks_read_per_packet'), r['algorithmic_bytes_per_packet'], d['e2e']['value'], d['config']['algorithm'])"
-done
+timeout 1500 python -m pytest tests -q -m gpu 2>&1 | tail -3
+timeout 300 python bench.py --config adversarial --steps 5 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1 && \
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:ms_scan -s 3 -c 1 -o gpurun_out/ms_adv -f \
+  python bench.py --config adversarial --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_adv.log 2>&1
+echo ncu rc=$?
