@@ -27,6 +27,9 @@ constexpr int MS_BLOCK = 256;
 #ifndef PFW_MS_MINB
 #define PFW_MS_MINB 5  // resident blocks per SM the scan is register-limited to
 #endif
+#ifndef PFW_MS_LPB
+#define PFW_MS_LPB 1   // packets per lane per batch (batch = 32 * LPB packets per warp)
+#endif
 enum { MSD_SRC = 0, MSD_DST = 1, MSD_SPORT = 2, MSD_DPORT = 3 };
 
 int g_matchset = 1;            // build match sets at ruleset creation
@@ -117,7 +120,8 @@ __global__ void __launch_bounds__(MS_BLOCK) ms_sum_kernel(const uint32_t *bits, 
 }
 
 struct MsView {
-    const uint32_t *bits[4];
+    const uint32_t *bits0;    // the four dimensions' rows, one allocation
+    uint32_t off[4];          // word offset of each dimension's rows from bits0
     const uint32_t *ipb[2];   // src / dst boundaries
     const uint2 *ipc[2];      // per /16 block: [first, end) boundary index
     const uint32_t *port[2];  // sport / dport -> interval
@@ -221,9 +225,10 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
     constexpr int P = 32 / G;                      // packets in flight per warp
     constexpr uint32_t STEP = (uint32_t)G * V;     // words per step
     constexpr uint32_t GMASK = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
-    __shared__ uint4 s_off[MS_BLOCK / 32][32];     // per warp: row offsets of the batch's packets
-    __shared__ uint4 s_row[SUM ? MS_BLOCK / 32 : 1][32];  // per warp: row indices (SUM)
-    __shared__ uint32_t s_res[MS_BLOCK / 32][32];  // per warp: first match of the batch's packets
+    constexpr int LPB = PFW_MS_LPB, BATCH = 32 * LPB;  // packets per warp batch
+    __shared__ uint4 s_off[MS_BLOCK / 32][BATCH];     // per warp: row offsets of the batch's packets
+    __shared__ uint4 s_row[SUM ? MS_BLOCK / 32 : 1][BATCH];  // per warp: row indices (SUM)
+    __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match of the batch's packets
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
@@ -247,31 +252,41 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
     unsigned long long st_sum = 0, st_blocks = 0;
     unsigned st_max = 0;
 
-    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
-        const int64_t i = b0 + lane;
-        const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
-        if (i < n) {
-            uint4 v;
-            if (p.pkts) {
-                v = __ldg(p.pkts + i);
-            } else {
-                v.x = __ldg(p.cols.src + i);
-                v.y = __ldg(p.cols.dst + i);
-                v.z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
-                v.w = __ldg(p.cols.proto + i);
+    for (int64_t b0 = gw * BATCH; b0 < n; b0 += nw * BATCH) {
+        const int nv = (int)((n - b0) < BATCH ? (n - b0) : BATCH);
+        // the batch's packets (all LPB loads in flight), then their rows
+        uint4 v[LPB];
+#pragma unroll
+        for (int k = 0; k < LPB; k++) {
+            const int64_t i = b0 + k * 32 + lane;
+            v[k] = make_uint4(0u, 0u, 0u, 0u);
+            if (i < n) {
+                if (p.pkts) {
+                    v[k] = __ldg(p.pkts + i);
+                } else {
+                    v[k].x = __ldg(p.cols.src + i);
+                    v[k].y = __ldg(p.cols.dst + i);
+                    v[k].z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
+                    v[k].w = __ldg(p.cols.proto + i);
+                }
             }
-            const uint32_t wp = (uint32_t)t.wp;
-            uint4 o;
-            o.x = ms_ip_row(t.ipb[0], t.ipc[0], v.x) * wp + cbeg;
-            o.y = ms_ip_row(t.ipb[1], t.ipc[1], v.y) * wp + cbeg;
-            o.z = ((uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16))) * wp + cbeg;
-            o.w = __ldg(t.port[1] + (v.z & 0xFFFFu)) * wp + cbeg;
-            s_off[warp][lane] = o;
-            if (SUM)
-                s_row[SUM ? warp : 0][lane] = make_uint4((o.x - cbeg) / wp, (o.y - cbeg) / wp, (o.z - cbeg) / wp,
-                                                         (o.w - cbeg) / wp);
         }
-        s_res[warp][lane] = PFW_NO_MATCH;
+#pragma unroll
+        for (int k = 0; k < LPB; k++) {
+            const int64_t i = b0 + k * 32 + lane;
+            if (i < n) {
+                const uint32_t wp = (uint32_t)t.wp;
+                const uint4 r = make_uint4(
+                    ms_ip_row(t.ipb[0], t.ipc[0], v[k].x), ms_ip_row(t.ipb[1], t.ipc[1], v[k].y),
+                    (uint32_t)__ldg(t.cls + (v[k].w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v[k].z >> 16)),
+                    __ldg(t.port[1] + (v[k].z & 0xFFFFu)));
+                // word offsets from the common base, at the first step
+                s_off[warp][k * 32 + lane] = make_uint4(r.x * wp + cbeg + t.off[0], r.y * wp + cbeg + t.off[1],
+                                                        r.z * wp + cbeg + t.off[2], r.w * wp + cbeg + t.off[3]);
+                if (SUM) s_row[SUM ? warp : 0][k * 32 + lane] = r;
+            }
+            s_res[warp][k * 32 + lane] = PFW_NO_MATCH;
+        }
         __syncwarp();
         if (nsteps > 0) {
             // group state (group-uniform): packet pj (-1 idle), step s, the
@@ -285,7 +300,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
             uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
             uint32_t scand = 0;  // SUM: candidate blocks after the current one (this lane's 32)
             unsigned nrd = 0;    // SUM: block reads of this lane's group (counted on lane gl == 0)
-            const uint32_t b0 = cbeg / 32u, blast = whi / 32u;  // SUM: first / last block
+            const uint32_t blk0 = cbeg / 32u, blast = whi / 32u;  // SUM: first / last block
             if (pj >= 0) {
                 const uint4 o = s_off[warp][pj];
                 o0 = o.x + lv;
@@ -309,7 +324,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                                     __ldg(u.sum[1] + (size_t)rw.y * u.sw + gl) &
                                     __ldg(u.sum[2] + (size_t)rw.z * u.sw + gl) &
                                     __ldg(u.sum[3] + (size_t)rw.w * u.sw + gl);
-                            const int rel0 = (int)b0 - 32 * gl, rel1 = (int)blast - 32 * gl;
+                            const int rel0 = (int)blk0 - 32 * gl, rel1 = (int)blast - 32 * gl;
                             scand &= rel0 < 0 ? 0xFFFFFFFFu : (rel0 >= 31 ? 0u : (0xFFFFFFFFu << (rel0 + 1)));
                             scand &= rel1 < 0 ? 0u : (rel1 >= 31 ? 0xFFFFFFFFu : ((2u << rel1) - 1u));
                         }
@@ -318,7 +333,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 if (SUM && act && gl == 0) nrd++;
                 if (act) {
                     MsStep<V> st;
-                    st.load(t.bits[0] + o0, t.bits[1] + o1, t.bits[2] + o2, t.bits[3] + o3);
+                    st.load(t.bits0 + o0, t.bits0 + o1, t.bits0 + o2, t.bits0 + o3);
 #pragma unroll
                     for (int v = 0; v < V; v++) {
                         x[v] = st.w[0][v] & st.w[1][v] & st.w[2][v] & st.w[3][v];
@@ -331,20 +346,22 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 }
                 const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
                 const uint32_t gbits = (bal >> gbase) & GMASK;
-                // this lane's lowest set bit: first non-zero word, its lowest bit
-                uint32_t wsel = x[V - 1], widx = V - 1;
-#pragma unroll
-                for (int v = V - 2; v >= 0; v--) {
-                    if (x[v]) {
-                        wsel = x[v];
-                        widx = v;
-                    }
-                }
-                const uint32_t cand = __shfl_sync(0xFFFFFFFFu,
-                                                  (cbeg + (uint32_t)s * STEP + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1),
-                                                  gbase + (__ffs(gbits) - 1) * (gbits != 0u));
                 const bool found = gbits != 0u;  // (idle groups have no bits)
-                if (found && gl == 0) s_res[warp][pj] = cand;
+                if (bal) {  // warp-uniform: some group found its packet's first match
+                    // this lane's lowest set bit: first non-zero word, its lowest bit
+                    uint32_t wsel = x[V - 1], widx = V - 1;
+#pragma unroll
+                    for (int v = V - 2; v >= 0; v--) {
+                        if (x[v]) {
+                            wsel = x[v];
+                            widx = v;
+                        }
+                    }
+                    const uint32_t cand =
+                        __shfl_sync(0xFFFFFFFFu, (cbeg + (uint32_t)s * STEP + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1),
+                                    gbase + (__ffs(gbits) - 1) * (gbits != 0u));
+                    if (found && gl == 0) s_res[warp][pj] = cand;
+                }
                 bool done = act && (found || s + 1 >= nsteps);
                 int ns = s + 1;  // next step (SUM: the next candidate block)
                 if constexpr (SUM) {
@@ -355,7 +372,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                                                gbase + (__ffs(cbits) - 1) * (cbits != 0u));
                     done = act && (found || cbits == 0u);
                     if (!done && act) {
-                        ns = nb - (int)b0;
+                        ns = nb - (int)blk0;
                         const int rel = nb - 32 * gl;  // drop candidates up to nb
                         scand &= rel < 0 ? 0xFFFFFFFFu : (rel >= 31 ? 0u : (0xFFFFFFFFu << (rel + 1)));
                     }
@@ -394,10 +411,14 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
             if constexpr (SUM) st_blocks += nrd;
         }
         __syncwarp();
-        if (i < n) {
-            const uint32_t res = s_res[warp][lane];
-            PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
-            emit_result<MODE>(p, (uint32_t)i, res, span, st_sum, st_max);
+#pragma unroll
+        for (int k = 0; k < LPB; k++) {
+            const int64_t i = b0 + k * 32 + lane;
+            if (i < n) {
+                const uint32_t res = s_res[warp][k * 32 + lane];
+                PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
+                emit_result<MODE>(p, (uint32_t)i, res, span, st_sum, st_max);
+            }
         }
         __syncwarp();
     }
@@ -423,8 +444,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
 
 void ms_free(MatchSet *m) {
     if (!m) return;
-    for (auto *b : m->d_bits)
-        if (b) cudaFree(b);
+    if (m->d_bits_all) cudaFree(m->d_bits_all);
     for (auto *b : m->d_sum)
         if (b) cudaFree(b);
     for (auto *b : m->d_ipb)
@@ -572,8 +592,9 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
     const size_t budget = g_ms_budget_mb > 0 ? (size_t)g_ms_budget_mb << 20 : free_b / 4;
     bool fits = bytes <= budget;
-    for (int d = 0; d < 4; d++)  // word offsets are 32-bit in the scan
-        fits = fits && (uint64_t)m->rows[d] * (uint64_t)m->wp + 4 * 32 < (1ull << 32);
+    uint64_t all_words = 0;  // word offsets from the common base are 32-bit in the scan
+    for (int d = 0; d < 4; d++) all_words += (uint64_t)m->rows[d] * (uint64_t)m->wp + 4 * 32;
+    fits = fits && all_words < (1ull << 32);
     if (!fits) {
         delete m;
         return PFW_OK;  // too large for the budget: rule-by-rule scan
@@ -609,12 +630,21 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     uint8_t *d_pr = nullptr;
     int *d_clsp = nullptr;
     cudaError_t e = cudaSuccess;
-    // + one 4-word-per-lane step of padding: the last step of a row may read
-    // past its end (masked), also on the last row
-    for (int d = 0; d < 4 && e == cudaSuccess; d++)
-        e = cudaMalloc(&m->d_bits[d], ((size_t)m->rows[d] * (size_t)m->wp + 4 * 32) * 4);
-    for (int d = 0; d < 4 && e == cudaSuccess; d++)
-        e = cudaMemsetAsync(m->d_bits[d] + (size_t)m->rows[d] * (size_t)m->wp, 0, 4 * 32 * 4);
+    // one allocation for the four dimensions (the scan addresses every row
+    // from one base); + one 4-word-per-lane step of padding after each: the
+    // last step of a row may read past its end (masked), also on a last row
+    {
+        size_t words = 0;
+        for (int d = 0; d < 4; d++) words += (size_t)m->rows[d] * (size_t)m->wp + 4 * 32;
+        e = cudaMalloc(&m->d_bits_all, words * 4);
+        size_t off = 0;
+        for (int d = 0; d < 4 && e == cudaSuccess; d++) {
+            m->d_bits[d] = m->d_bits_all + off;
+            off += (size_t)m->rows[d] * (size_t)m->wp;
+            e = cudaMemsetAsync(m->d_bits_all + off, 0, 4 * 32 * 4);
+            off += 4 * 32;
+        }
+    }
     if (e == cudaSuccess) e = ms_upload(&m->d_ipb[0], bs.data(), bs.size());
     if (e == cudaSuccess) e = ms_upload(&m->d_ipb[1], bd.data(), bd.size());
     if (e == cudaSuccess) e = ms_upload(&m->d_ipc[0], ipc[0].data(), ipc[0].size());
@@ -683,7 +713,8 @@ template <int MODE>
 int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     const MatchSet *m = h->ms;
     MsView t{};
-    for (int d = 0; d < 4; d++) t.bits[d] = m->d_bits[d];
+    t.bits0 = m->d_bits_all;
+    for (int d = 0; d < 4; d++) t.off[d] = (uint32_t)(m->d_bits[d] - m->d_bits_all);
     t.ipb[0] = m->d_ipb[0];
     t.ipb[1] = m->d_ipb[1];
     t.ipc[0] = m->d_ipc[0];
@@ -725,7 +756,7 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
         if (occ < 1) occ = 1;
     }
     int64_t grid = (int64_t)h->sms * occ;
-    const int64_t need = (p.n + MS_BLOCK - 1) / MS_BLOCK;  // one 32-packet batch per warp
+    const int64_t need = (p.n + MS_BLOCK * PFW_MS_LPB - 1) / (MS_BLOCK * PFW_MS_LPB);  // one batch per warp
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
     if (kern_s) {

@@ -143,7 +143,8 @@ struct ScanWs {
 struct MatchSet {
     int64_t wp = 0;             // 32-bit words per bitmap row (whole 128-byte lines)
     int64_t rows[4] = {};       // rows of src, dst, (protocol class, sport), dport
-    uint32_t *d_bits[4] = {};   // rows[d] * wp words each
+    uint32_t *d_bits_all = nullptr;  // the four dimensions' rows, one allocation
+    uint32_t *d_bits[4] = {};   // rows[d] * wp words each (inside d_bits_all)
     uint32_t *d_ipb[2] = {};    // src / dst interval boundaries (sorted, [0] = 0)
     uint2 *d_ipc[2] = {};       // per /16 block: [first, end) index into the boundaries
     uint32_t *d_port[2] = {};   // sport / dport -> interval (65536 entries each)
