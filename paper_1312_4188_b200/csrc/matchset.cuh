@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(MS_BLOCK) ms_build_kernel(MsBuildArgs a) {
             const uint32_t b = __ballot_sync(0xFFFFFFFFu, m);
             if (lane == k) mine = b;
         }
+        PFW_CHECK(row < a.rows && g * 32 + lane < a.wp);
         a.bits[row * a.wp + g * 32 + lane] = mine;
     }
 }
@@ -128,6 +129,10 @@ struct MsView {
     const uint8_t *cls;       // protocol -> class
     int64_t wp;
     uint32_t sp_rows;
+#ifdef PFW_CHECKS
+    uint32_t nrows[4];        // rows per dimension
+    uint64_t words;           // words of the bits0 allocation
+#endif
 };
 
 // Block summaries (SUM variant only; the other variants take the empty type)
@@ -280,6 +285,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     ms_ip_row(t.ipb[0], t.ipc[0], v[k].x), ms_ip_row(t.ipb[1], t.ipc[1], v[k].y),
                     (uint32_t)__ldg(t.cls + (v[k].w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v[k].z >> 16)),
                     __ldg(t.port[1] + (v[k].z & 0xFFFFu)));
+                PFW_CHECK(r.x < t.nrows[0] && r.y < t.nrows[1] && r.z < t.nrows[2] && r.w < t.nrows[3]);
                 // word offsets from the common base, at the first step
                 s_off[warp][k * 32 + lane] = make_uint4(r.x * wp + cbeg + t.off[0], r.y * wp + cbeg + t.off[1],
                                                         r.z * wp + cbeg + t.off[2], r.w * wp + cbeg + t.off[3]);
@@ -320,6 +326,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         scand = 0u;
                         if ((uint32_t)gl < u.sw) {
                             const uint4 rw = s_row[SUM ? warp : 0][pj];
+                            PFW_CHECK(rw.x < t.nrows[0] && rw.y < t.nrows[1] && rw.z < t.nrows[2] && rw.w < t.nrows[3]);
                             scand = __ldg(u.sum[0] + (size_t)rw.x * u.sw + gl) &
                                     __ldg(u.sum[1] + (size_t)rw.y * u.sw + gl) &
                                     __ldg(u.sum[2] + (size_t)rw.z * u.sw + gl) &
@@ -331,6 +338,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     }
                 }
                 if (SUM && act && gl == 0) nrd++;
+                PFW_CHECK(!act || (pj < nv && (uint64_t)max(max(o0, o1), max(o2, o3)) + V <= t.words));
                 if (act) {
                     MsStep<V> st;
                     st.load(t.bits0 + o0, t.bits0 + o1, t.bits0 + o2, t.bits0 + o3);
@@ -715,6 +723,11 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     MsView t{};
     t.bits0 = m->d_bits_all;
     for (int d = 0; d < 4; d++) t.off[d] = (uint32_t)(m->d_bits[d] - m->d_bits_all);
+#ifdef PFW_CHECKS
+    for (int d = 0; d < 4; d++) t.nrows[d] = (uint32_t)m->rows[d];
+    t.words = 0;
+    for (int d = 0; d < 4; d++) t.words += (uint64_t)m->rows[d] * (uint64_t)m->wp + 4 * 32;
+#endif
     t.ipb[0] = m->d_ipb[0];
     t.ipb[1] = m->d_ipb[1];
     t.ipc[0] = m->d_ipc[0];

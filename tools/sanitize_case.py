@@ -37,6 +37,31 @@ for fp in (64, 1024):           # multi-pass with several passes / a single pass
         np.testing.assert_array_equal(res.comparisons, comps)
         checks += 1
 _native.set_tuning("proto_split", 0)
+# match-set scan: every step shape, block summaries off / on, windows, partitions
+for summary in (0, 1):
+    _native.set_tuning("ms_summary", summary)   # applies to rulesets built from here on
+    cs = pfw.CompiledRuleset.from_columns(rules, device=0)
+    _native.set_tuning("algo", 2)
+    for group, words in ((8, 4), (8, 2), (16, 4), (16, 2), (32, 2), (32, 1)):
+        _native.set_tuning("ms_group", group)
+        _native.set_tuning("ms_words", words)
+        for lo, hi in ((0, 700), (37, 650), (699, 700)):
+            np.testing.assert_array_equal(cs.scan_range(p, lo, hi), oracle.scan_range(rules, pk, lo, hi))
+            checks += 1
+        res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=3)).run_arrays(cs, p)
+        np.testing.assert_array_equal(res.first, oracle.engine_run(rules, pk, "function", 3)[0])
+        checks += 1
+    _native.set_tuning("ms_group", 0)
+    _native.set_tuning("ms_words", 4)
+    _native.set_tuning("algo", 0)
+_native.set_tuning("ms_summary", 2)
+adv_rules = oracle.adversarial_rules(50_000)
+adv_pk = oracle.adversarial_traffic(4_000)
+ca = pfw.CompiledRuleset.from_columns(adv_rules, device=0)
+pa = pfw.PacketArrays.from_columns(*[adv_pk[f] for f in oracle.PKT_FIELDS], device=0)
+for lo, hi in ((0, 50_000), (1000, 45_003)):
+    np.testing.assert_array_equal(ca.scan_range(pa, lo, hi), oracle.scan_range(adv_rules, adv_pk, lo, hi))
+    checks += 1
 fused = FusedFunctionParallel(c, len(p))
 f, cm = fused.run(p)
 np.testing.assert_array_equal(pfw.classifier.first_to_host(f), oracle.engine_run(rules, pk, "function", 1)[0])
