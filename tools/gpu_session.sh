@@ -1,10 +1,17 @@
 mkdir -p gpurun_out/final
-timeout 600 python bench.py > gpurun_out/final/bench.json 2>gpurun_out/final/bench.err
-timeout 600 python bench.py --impl reference > gpurun_out/final/ref.json 2>&1
-for cfg in grid adversarial function oracle; do
-  timeout 600 python bench.py --config $cfg --steps 30 --warmup 3 --no-cpu > gpurun_out/final/$cfg.json 2>&1
-done
-timeout 600 python bench.py --config function --steps 30 --warmup 3 --no-cpu --fused > gpurun_out/final/function_fused.json 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:ms_scan -s 3 -c 1 -o gpurun_out/final/ms_data -f \
-  python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/final/ncu.log 2>&1
-echo ncu rc=$?
+timeout 600 python - <<'PY'
+import time, torch
+import paper_1312_4188_b200 as pfw
+from paper_1312_4188_b200 import _native, workloads
+torch.cuda.init()
+for name in ["oracle", "grid", "data", "adversarial", "function"]:
+    w = workloads.WORKLOADS[name]
+    cols = workloads.rule_columns(w)
+    for rep in range(2):
+        t0 = time.perf_counter()
+        c = pfw.CompiledRuleset.from_columns(cols, device=0)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    print(f"create {name:12s} R={w.rules:6d}: {dt*1e3:8.1f} ms, match sets {_native.lib().pfw_ruleset_matchset_bytes(c.handle)/2**20:8.1f} MiB", flush=True)
+PY
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/final/launch_ncu.log 2>&1; echo ncu rc=$?
