@@ -16,12 +16,14 @@
 // are built by the reference predicate itself, evaluated on each interval's
 // first value.
 //
-// Layout in HBM (struct MatchSet): per field, rows x wp words (wp = rules/32
-// rounded up to a whole step of 128 words, 512 bytes); IP value -> interval through the
-// sorted boundaries and a 65536-entry table of boundary ranges per /16 block;
-// port value -> interval through a direct 65536-entry table; protocol ->
-// class through a 256-entry table.  The lookup tables (~1.5 MB) and the rows'
-// leading lines (where most first matches are) stay resident in L2.
+// Layout in HBM (struct MatchSet): the four dimensions' rows in one
+// allocation, rows x wp words each (wp = rules/32 rounded up to a whole step
+// of 128 words, 512 bytes); optional block summaries (one bit per 1024-rule
+// block per row); IP value -> interval through the sorted boundaries and a
+// 65536-entry table of boundary ranges per /16 block; port value -> interval
+// through a direct 65536-entry table; protocol -> class through a 256-entry
+// table.  The lookup tables (~1.5 MB) and the rows' leading lines (where most
+// first matches are) stay resident in L2 up to ~10K rules.
 
 constexpr int MS_BLOCK = 256;
 #ifndef PFW_MS_MINB
