@@ -306,8 +306,16 @@ def main() -> int:
 
     # ---------------------------------------------------------- workload
     cols = workloads.rule_columns(w)
-    compiled = CompiledRuleset.from_columns(cols, device=local)
-    R = compiled.num_rules
+    R = len(cols["proto"])
+    if w.model == "function":
+        # rules sharded: this rank uploads only its partition (its own match
+        # sets, local windows, global indices)
+        r_lo, r_hi = parallel.rule_shard(R, info)
+        compiled = CompiledRuleset.from_columns({k: v[r_lo:r_hi] for k, v in cols.items()}, device=local,
+                                                shard=(r_lo, R))
+    else:
+        r_lo, r_hi = 0, R
+        compiled = CompiledRuleset.from_columns(cols, device=local)
     ms_bytes = int(_native.lib().pfw_ruleset_matchset_bytes(compiled.handle))
     rule_scan = args.algo == 1 or args.proto_split or args.sc == 1
     algo = "matchset" if ms_bytes and not rule_scan else "rule scan"
@@ -315,11 +323,9 @@ def main() -> int:
     total_packets = w.packets * world if weak else w.packets
     if w.model == "function":
         p_lo, p_hi = 0, w.packets                       # packets replicated
-        r_lo, r_hi = parallel.rule_shard(R, info)       # rules sharded
     else:
         # packets sharded: contiguous partition_bounds shards of the global stream
         p_lo, p_hi = parallel.packet_shard(total_packets, info)
-        r_lo, r_hi = 0, R
     # the generator draws from the global stream of total_packets packets
     wgen = workloads.Workload(w.name, w.rules, total_packets, w.model, w.description)
     pkts = workloads.packets(wgen, p_lo, p_hi - p_lo, local)
@@ -342,7 +348,7 @@ def main() -> int:
         elif w.model == "function":
             _native.check(_native.lib().pfw_accumulator_init(n, first.data_ptr(), comps.data_ptr(),
                                                              stream.cuda_stream), "init")
-            compiled.scan_partition_accumulate(pkts, r_lo, r_hi, first, comps, stats,
+            compiled.scan_partition_accumulate(pkts, 0, compiled.num_rules, first, comps, stats,
                                                stream=stream.cuda_stream)
             parallel.function_parallel_combine(first, comps, None)
         else:
@@ -529,6 +535,7 @@ def main() -> int:
                     "TrafficProfile(N, seed=2)), generated on the GPU bit-exactly",
             "config": {"workload": w.description, "rules": R, "packets": total_packets,
                        "packets_per_gpu": n, "execution_model": w.model,
+                       **({"rules_per_gpu": [r_lo, r_hi]} if w.model == "function" else {}),
                        "parallelism": f"{'rule' if w.model == 'function' else 'packet'}-sharded x{world}"
                                       + (" (fused NVLink-atomic combine)" if fused is not None else
                                          " (NCCL MIN all-reduce)" if w.model == "function" else ""),

@@ -77,6 +77,14 @@ int pfw_ruleset_device(pfw_ruleset_t h);
 /* Device bytes of the ruleset's match sets; 0 when they were not built (the
  * ruleset then scans rule by rule). */
 int64_t pfw_ruleset_matchset_bytes(pfw_ruleset_t h);
+/* Mark the handle as a rule shard: its rules are positions [index_base,
+ * index_base + n) of an ordered ruleset of `total` rules (function-parallel:
+ * each GPU uploads only its partition, engines.py:316-321).  Scan windows stay
+ * in local positions [0, n); every reported first-match index (outputs, the
+ * accumulate min, the fused peer combine) becomes index_base + local; the
+ * comparison counts are window-relative as before.  pfw_verdicts rejects a
+ * partial shard (combined indices need the whole ruleset's actions). */
+int pfw_ruleset_set_shard(pfw_ruleset_t h, int64_t index_base, int64_t total);
 
 /* Host packet packing.  Replaces PacketArrays.from_packets
  * (classifier.py:75-83) for column input: writes n 16-byte records. */

@@ -43,6 +43,7 @@ _SIGS = {
     "pfw_ruleset_destroy": (_I32, [_P]),
     "pfw_ruleset_size": (_I64, [_P]),
     "pfw_ruleset_matchset_bytes": (_I64, [_P]),
+    "pfw_ruleset_set_shard": (_I32, [_P, _I64, _I64]),
     "pfw_ruleset_device": (_I32, [_P]),
     "pfw_pack_packets_host": (_I32, [_I64, _P, _P, _P, _P, _P, _P]),
     "pfw_scan_range": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P]),

@@ -222,7 +222,7 @@ class CompiledRuleset:
     """Ruleset uploaded to one GPU (drop-in for classifier.py:98-185)."""
 
     def __init__(self, ruleset: Ruleset | None = None, device: int | None = None, *,
-                 columns: dict | None = None) -> None:
+                 columns: dict | None = None, shard: tuple[int, int] | None = None) -> None:
         if (ruleset is None) == (columns is None):
             raise TypeError("pass exactly one of ruleset or columns")
         if columns is not None:
@@ -243,10 +243,33 @@ class CompiledRuleset:
                                                 ctypes.byref(h)), "pfw_ruleset_create")
         self._h = h
         self._finalizer = weakref.finalize(self, _native.lib().pfw_ruleset_destroy, h)
+        # rule shard (function-parallel, engines.py:316-321): these rules are
+        # positions [index_base, index_base + n) of a ruleset of total_rules;
+        # windows are local, reported indices global
+        self.index_base, self.total_rules = 0, n
+        if shard is not None:
+            base, total = int(shard[0]), int(shard[1])
+            check(_native.lib().pfw_ruleset_set_shard(h, base, total), "pfw_ruleset_set_shard")
+            self.index_base, self.total_rules = base, total
 
     @classmethod
-    def from_columns(cls, columns: dict, device: int | None = None) -> "CompiledRuleset":
-        return cls(None, device, columns=columns)
+    def from_columns(cls, columns: dict, device: int | None = None,
+                     shard: tuple[int, int] | None = None) -> "CompiledRuleset":
+        return cls(None, device, columns=columns, shard=shard)
+
+    def shard(self, lo: int, hi: int) -> "CompiledRuleset":
+        """Rules [lo, hi) uploaded on their own (their own match sets): scans of
+        the shard take local windows and report global rule indices."""
+        lo, hi = int(lo), int(hi)
+        if not 0 <= lo <= hi <= self.num_rules:
+            raise ValueError(f"shard [{lo}, {hi}) outside a ruleset of {self.num_rules} rules")
+        cols = {f: getattr(self, f)[lo:hi] for f in RULE_COLUMNS}
+        return CompiledRuleset.from_columns(cols, self.device,
+                                            shard=(self.index_base + lo, self.total_rules))
+
+    @property
+    def is_shard(self) -> bool:
+        return self.total_rules != self.num_rules
 
     @property
     def handle(self) -> ctypes.c_void_p:

@@ -161,6 +161,8 @@ struct MatchSet {
 struct pfw_ruleset {
     int device;
     int64_t n;       // rules
+    int64_t index_base = 0;  // rule shard: these are rules [index_base, index_base + n) of total
+    int64_t total = -1;      // size of the whole ruleset (-1: this handle is the whole ruleset)
     int64_t rpad;    // padded row length (multiple of 32, >= n + max stage)
     uint32_t *d_rules = nullptr;   // NF * rpad
     uint8_t *d_accept = nullptr;   // rpad
@@ -236,6 +238,7 @@ struct ScanParams {
     unsigned long long *blocks_read;  // match-set scan with summaries: block reads (null = not counted)
     int tile;
     uint32_t one;  // runtime 1: keeps ptxas from folding x*1+c into IADD3
+    uint32_t index_base;  // rule shard: reported indices are index_base + local position
     // MODE_PEER (fused function-parallel combine): result buffers of every
     // rank, reached over NVLink through CUDA IPC mappings
     uint32_t *const *peer_first;
@@ -255,6 +258,8 @@ template <int MODE>
 __device__ __forceinline__ void emit_result(const ScanParams &p, uint32_t id, uint32_t f, uint32_t span,
                                             unsigned long long &st_sum, unsigned &st_max) {
     const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.win_lo + 1) : span;
+    const uint32_t fl = f;  // local position (actions)
+    if (f != PFW_NO_MATCH) f += p.index_base;  // reported index (rule shards: global)
     if (MODE == MODE_ACC) {
         if (f != PFW_NO_MATCH) p.first[id] = min(p.first[id], f);
         p.comps[id] += c;
@@ -280,7 +285,7 @@ __device__ __forceinline__ void emit_result(const ScanParams &p, uint32_t id, ui
     } else {
         p.first[id] = f;
         if (p.comps) p.comps[id] = c;
-        if (p.verdict) p.verdict[id] = (f != PFW_NO_MATCH) ? p.accept[f] : (uint8_t)0;
+        if (p.verdict) p.verdict[id] = (fl != PFW_NO_MATCH) ? p.accept[fl] : (uint8_t)0;
     }
     st_sum += c;
     st_max = max(st_max, c);
@@ -1207,6 +1212,7 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
     p.stats = reinterpret_cast<unsigned long long *>(stats);
     p.tile = g_tile;
     p.one = 1;
+    p.index_base = (uint32_t)h->index_base;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
     if (peer) {
@@ -1552,6 +1558,16 @@ int64_t pfw_ruleset_size(pfw_ruleset_t h) { return h ? h->n : -1; }
 int pfw_ruleset_device(pfw_ruleset_t h) { return h ? h->device : -1; }
 int64_t pfw_ruleset_matchset_bytes(pfw_ruleset_t h) { return h && h->ms ? (int64_t)h->ms->bytes : 0; }
 
+int pfw_ruleset_set_shard(pfw_ruleset_t h, int64_t index_base, int64_t total) {
+    if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
+    if (index_base < 0 || total < 0 || index_base + h->n > total || total > PFW_MAX_RULES)
+        return set_err(PFW_ERR_INVALID, "shard [%lld, %lld) outside a ruleset of %lld rules",
+                       (long long)index_base, (long long)(index_base + h->n), (long long)total);
+    h->index_base = index_base;
+    h->total = total;
+    return PFW_OK;
+}
+
 int pfw_pack_packets_host(int64_t n, const uint8_t *proto, const uint32_t *src_ip,
                           const uint16_t *src_port, const uint32_t *dst_ip,
                           const uint16_t *dst_port, void *h_out) {
@@ -1681,6 +1697,9 @@ int pfw_verdicts(pfw_ruleset_t h, const uint32_t *d_first, int64_t n, uint8_t *d
                  void *stream) {
     if (!h || n < 0 || (n > 0 && (!d_first || !d_verdict)))
         return set_err(PFW_ERR_INVALID, "bad verdict arguments");
+    if (h->total >= 0 && h->total != h->n)
+        return set_err(PFW_ERR_INVALID, "verdicts of combined results need the whole ruleset's actions, not a "
+                                        "shard of %lld of %lld rules", (long long)h->n, (long long)h->total);
     if (n == 0) return PFW_OK;
     DeviceGuard g(h->device);
     verdict_kernel<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(h->d_accept, d_first, n, d_verdict);

@@ -211,7 +211,12 @@ class FusedFunctionParallel:
         if self.comps is not None:
             self.comps.zero_()
         self._barrier()  # nobody writes into a buffer before its owner reset it
-        lo, hi = rule_shard(self.compiled.num_rules, self.info)
+        # a rule-shard handle holds exactly this rank's rules (local window,
+        # global indices); a whole-ruleset handle scans this rank's window
+        if getattr(self.compiled, "is_shard", False):
+            lo, hi = 0, self.compiled.num_rules
+        else:
+            lo, hi = rule_shard(self.compiled.num_rules, self.info)
         st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
         _native.check(_native.lib().pfw_scan_fused_min(
             self.compiled.handle, lo, hi, pkts.data.data_ptr(), len(pkts), self._peer_first,

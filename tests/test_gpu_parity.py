@@ -687,3 +687,68 @@ def test_match_set_block_summaries(summary):
         assert len(pk["proto"]) <= got < len(pk["proto"]) * 49 // 4   # most decoy blocks skipped
     else:
         assert got == 0
+
+
+# ------------------------------------------------------------- rule shards
+
+@pytest.mark.parametrize("algo", [0, 1])
+def test_rule_shards_function_parallel(algo):
+    """Function-parallel with per-rank rule shards (each uploads only its
+    partition, engines.py:316-321): local windows, global indices; the
+    accumulate and the fused combine over G shard handles equal the
+    reference's function-parallel golden results."""
+    import ctypes
+    _native.set_tuning("algo", algo)
+    g = golden("engine_r503_t600.npz")
+    full = compiled(golden_rules("r503_s24_w30"))
+    p = dev_pkts(golden_traffic("t600_s25"))
+    n = len(p)
+    for G in (1, 2, 3, 8):
+        shards = [full.shard(lo, hi) for lo, hi in pfw.partition_bounds(full.num_rules, G)]
+        assert all(s.is_shard for s in shards) == (G > 1)
+        first = torch.full((n,), NO_MATCH, dtype=torch.int32, device="cuda:0")
+        comps = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+        stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+        for s in shards:
+            s.scan_partition_accumulate(p, 0, s.num_rules, first, comps, stats)
+        np.testing.assert_array_equal(first_to_host(first), g[f"function_{G}_first"])
+        np.testing.assert_array_equal(comps.cpu().numpy(), g[f"function_{G}_comps"])
+        total, mx, _ = g[f"function_{G}_stats"].tolist()
+        assert stats.cpu().tolist() == [total, mx]
+        # fused combine from shard handles (virtual ranks, scatter layout)
+        ff = torch.full((n,), NO_MATCH, dtype=torch.int32, device="cuda:0")
+        fc = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+        bounds = pfw.partition_bounds(n, G)
+        P = ctypes.c_void_p
+        fptr = (P * G)(*[ff.data_ptr() + 4 * a for a, _ in bounds])
+        cptr = (P * G)(*[fc.data_ptr() + 4 * a for a, _ in bounds])
+        for s in shards:
+            _native.check(_native.lib().pfw_scan_fused_min(
+                s.handle, 0, s.num_rules, p.data.data_ptr(), n, fptr, cptr, G, 1, None,
+                torch.cuda.current_stream().cuda_stream), "fused")
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(first_to_host(ff), g[f"function_{G}_first"])
+        np.testing.assert_array_equal(fc.cpu().numpy(), g[f"function_{G}_comps"])
+
+
+def test_rule_shard_windows_and_verdicts():
+    rules = golden_rules("r2048_s21_w15")
+    pk = golden_traffic("t10000_s41")
+    full = compiled(rules)
+    s = full.shard(300, 1700)
+    assert (s.index_base, s.num_rules, s.total_rules) == (300, 1400, 2048)
+    d = dev_pkts(pk)
+    for lo, hi in ((0, 1400), (17, 1399), (700, 701)):
+        np.testing.assert_array_equal(s.scan_range(d, lo, hi), oracle.scan_range(rules, pk, 300 + lo, 300 + hi))
+    # verdicts written by the scan use the shard's own actions
+    verdict = torch.empty(len(d), dtype=torch.uint8, device="cuda:0")
+    f = first_to_host(s.scan_range_device(d, 0, 1400, verdict=verdict))
+    want = np.where(f >= 0, rules["action_accept"][np.maximum(f, 0)], False)
+    np.testing.assert_array_equal(verdict.cpu().numpy().astype(bool), want)
+    # verdicts of combined indices need the whole ruleset's actions
+    with pytest.raises(ValueError, match="whole ruleset"):
+        s.verdicts_device(torch.zeros(4, dtype=torch.int32, device="cuda:0"))
+    with pytest.raises(ValueError):
+        full.shard(5, 3000)
+    with pytest.raises(ValueError, match="outside"):
+        _native.check(_native.lib().pfw_ruleset_set_shard(s.handle, 1000, 2048), "set_shard")
