@@ -481,14 +481,6 @@ __device__ __forceinline__ void scan_live(const uint32_t (&r)[KS][NF], const uin
     }
 }
 
-#ifndef PFW_GROUP_HALF
-#define PFW_GROUP_HALF 0
-#endif
-constexpr bool GROUP_HALF = PFW_GROUP_HALF;
-#ifndef PFW_GROUP
-#define PFW_GROUP 3
-#endif
-constexpr int GROUP = PFW_GROUP;  // packets per warp iteration (ILP)
 constexpr int BLOCK = 256;
 constexpr int NWARPS = BLOCK / 32;
 
