@@ -79,3 +79,27 @@ def test_function_parallel_8_partitions_full_rules():
     np.testing.assert_array_equal(res.first, first)
     np.testing.assert_array_equal(res.comparisons, comps)
     assert (res.stats.total_comparisons, res.stats.max_worker_comparisons) == (total, mx)
+
+
+def test_more_than_2g_packets():
+    """A batch of 2^31 + 5 packets (32 GB of records): packet ids past INT32_MAX
+    through the match-set scan; a strided subsample against the oracle plus
+    the comparison checksum on every packet."""
+    import torch
+    n = (1 << 31) + 5
+    free, _ = torch.cuda.mem_get_info(0)
+    if free < n * 16 + n * 4 + (8 << 30):
+        pytest.skip("not enough device memory")
+    rules = oracle.gen_ruleset(1000, 1)
+    c = pfw.CompiledRuleset.from_columns(rules, device=0)
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=2), device=0)
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+    first = c.scan_range_device(p, 0, 1000, stats=stats)
+    idx = np.concatenate([np.arange(0, n, 1 << 20), np.arange(n - 4097, n)])
+    sub = pfw.PacketArrays(p.data[torch.as_tensor(idx, device="cuda:0")]).columns()
+    got = first[torch.as_tensor(idx, device="cuda:0")].cpu().numpy().astype(np.int64)
+    got[got == NO_MATCH] = -1
+    np.testing.assert_array_equal(got, oracle.scan_range(rules, sub, 0, 1000))
+    f = first.to(torch.int64)
+    comps = torch.where(f == NO_MATCH, torch.full_like(f, 1000), f + 1)
+    assert stats.cpu().tolist() == [int(comps.sum().item()), int(comps.max().item())]

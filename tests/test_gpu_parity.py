@@ -752,3 +752,16 @@ def test_rule_shard_windows_and_verdicts():
         full.shard(5, 3000)
     with pytest.raises(ValueError, match="outside"):
         _native.check(_native.lib().pfw_ruleset_set_shard(s.handle, 1000, 2048), "set_shard")
+
+
+@pytest.mark.parametrize("R", [1, 2, 31, 32, 33, 127, 128, 129, 1023, 1024, 1025, 2047, 4095, 4096, 4097, 5000])
+def test_rule_counts_at_word_line_and_step_edges(R):
+    """Ruleset sizes at the edges of a 32-rule word, a 1024-rule line and a
+    4096-rule step (match-set row padding) and of the rule scan's stages."""
+    rules = oracle.gen_ruleset(R, 900 + R, wp=0.3)
+    pk = oracle.gen_traffic_uniform(3000, 901)
+    c = compiled(rules)
+    for algo in (2, 1):
+        _native.set_tuning("algo", algo)
+        for lo, hi in ((0, R), (R // 2, R), (max(R - 1, 0), R)):
+            np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
