@@ -38,14 +38,17 @@ MS_BYTES_PER_RULE = 0.5       # match-set scan: one bit per rule from each of th
 
 
 def load_l2_peak():
-    """Measured L2 read bandwidth (tools/l2_probe.cu, committed under profiles/)."""
+    """Measured L2 read bandwidth (tools/l2_probe.cu, committed under profiles/):
+    (random 128-byte-line ceiling -- the match-set scan's access pattern --,
+    streaming ceiling, source)."""
     path = os.path.join(ROOT, "profiles", "l2_peak.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return float(d["l2_read_gbs"]), d.get("source", path)
+        stream = float(d["l2_read_gbs"])
+        return float(d.get("l2_random_line_read_gbs", stream)), stream, d.get("source", path)
     except (OSError, ValueError, KeyError):
-        return None, None
+        return None, None, None
 
 
 def load_peaks() -> dict:
@@ -434,7 +437,7 @@ def main() -> int:
     hbm = {"achieved": round(hbm_achieved, 2), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
            "frac": round(hbm_achieved / float(peaks.get("hbm_gbs", 6536.4)), 5),
            "bytes_per_packet": PKT_BYTES + OUT_BYTES}
-    l2_peak, l2_src = load_l2_peak()
+    l2_peak, l2_stream, l2_src = load_l2_peak()
     if algo == "matchset" and l2_peak:
         if blocks_read:
             # block summaries: the search reads the packet's 4 summary rows
@@ -460,7 +463,9 @@ def main() -> int:
             "frac": round(achieved / l2_peak, 4), "traffic": measured_traffic(f"{w.name}/matchset", n),
             "algorithmic_bytes_per_launch": round(alg_bytes),
             "algorithmic_bytes_per_packet": round(alg_bytes / max(n, 1), 1), **model,
-            "peak_source": f"measured L2 read bandwidth, L2-resident buffer ({l2_src})",
+            "peak_source": "measured L2 read bandwidth for this kernel's access pattern (random 128-byte "
+                           f"lines, 8-lane groups; {l2_src})",
+            "peak_l2_streaming": l2_stream, "frac_of_streaming_peak": round(achieved / l2_stream, 4),
             "hbm": hbm,
         }
     else:

@@ -1,2 +1,7 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "edges" 2>&1 | tail -2
-timeout 900 python -m pytest tests/test_gpu_fullsize.py -x -q -m gpu -k "2g" 2>&1 | tail -5
+mkdir -p gpurun_out/final
+timeout 600 python bench.py > gpurun_out/final/bench.json 2>gpurun_out/final/bench.err
+for cfg in grid adversarial function oracle; do
+  timeout 600 python bench.py --config $cfg --steps 30 --warmup 3 --no-cpu > gpurun_out/final/$cfg.json 2>&1
+done
+timeout 600 python bench.py --config function --steps 30 --warmup 3 --no-cpu --fused > gpurun_out/final/function_fused.json 2>&1
+echo done

@@ -18,6 +18,29 @@ __global__ void rd16(const uint4 *__restrict__ p, size_t n16, int reps, uint32_t
     if (acc == 0x12345678u) *out = acc;
 }
 
+// The match-set scan's access pattern: each group of 8 lanes reads one
+// random 128-byte line (16 bytes per lane), K independent lines per lane in
+// flight per iteration (the scan: 4, one per row), over an L2-resident buffer.
+template <int K>
+__global__ void __launch_bounds__(256) rd_random_lines(const uint4 *__restrict__ p, uint32_t nlines, int iters,
+                                                       uint32_t *out) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    uint32_t x = 0x9E3779B9u * (blockIdx.x * 32u + (threadIdx.x >> 5) * 4u + grp + 1u);
+    uint32_t acc = 0;
+    for (int it = 0; it < iters; it++) {
+        uint4 v[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            x = x * 1664525u + 1013904223u;           // per-group LCG (group-uniform)
+            const uint32_t line = (uint32_t)(((uint64_t)(x >> 8) * nlines) >> 24);
+            v[k] = __ldg(p + (size_t)line * 8 + gl);
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) acc ^= v[k].x ^ v[k].y ^ v[k].z ^ v[k].w;
+    }
+    if (acc == 0x12345678u) *out = acc;
+}
+
 int main() {
     uint32_t *out;
     cudaMalloc(&out, 4);
@@ -50,6 +73,38 @@ int main() {
         }
         cudaFree(p);
     }
-    printf("{\"l2_read_gbs\": %.1f, \"hbm_read_gbs\": %.1f}\n", best_l2, best_hbm);
+    // random 128-byte lines, 8-lane groups, K lines in flight per lane
+    double best_rl = 0;
+    {
+        const size_t bytes = (size_t)48 << 20;
+        uint4 *p;
+        cudaMalloc(&p, bytes);
+        cudaMemset(p, 1, bytes);
+        const uint32_t nlines = (uint32_t)(bytes / 128);
+        for (int occ : {4, 5, 8}) {
+            for (int K : {2, 4, 8}) {
+                const int iters = 4096;
+                auto run = [&](int it) {
+                    if (K == 2) rd_random_lines<2><<<sms * occ, 256>>>(p, nlines, it, out);
+                    else if (K == 4) rd_random_lines<4><<<sms * occ, 256>>>(p, nlines, it, out);
+                    else rd_random_lines<8><<<sms * occ, 256>>>(p, nlines, it, out);
+                };
+                run(16);
+                cudaEventRecord(a);
+                run(iters);
+                cudaEventRecord(b);
+                cudaEventSynchronize(b);
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                const double lines = (double)sms * occ * 256 / 8 * K * iters;
+                const double gbs = lines * 128 / ms / 1e6;
+                printf("random 128B lines  48 MB  blocks/SM %d  lines in flight/lane %d: %8.1f GB/s\n", occ, K, gbs);
+                best_rl = gbs > best_rl ? gbs : best_rl;
+            }
+        }
+        cudaFree(p);
+    }
+    printf("{\"l2_read_gbs\": %.1f, \"hbm_read_gbs\": %.1f, \"l2_random_line_read_gbs\": %.1f}\n", best_l2,
+           best_hbm, best_rl);
     return 0;
 }
