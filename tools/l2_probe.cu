@@ -21,10 +21,10 @@ __global__ void rd16(const uint4 *__restrict__ p, size_t n16, int reps, uint32_t
 // The match-set scan's access pattern: each group of 8 lanes reads one
 // random 128-byte line (16 bytes per lane), K independent lines per lane in
 // flight per iteration (the scan: 4, one per row), over an L2-resident buffer.
-template <int K>
+template <int K, int GL = 8>
 __global__ void __launch_bounds__(256) rd_random_lines(const uint4 *__restrict__ p, uint32_t nlines, int iters,
                                                        uint32_t *out) {
-    const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const int lane = threadIdx.x & 31, grp = lane / GL, gl = lane % GL;
     uint32_t x = 0x9E3779B9u * (blockIdx.x * 32u + (threadIdx.x >> 5) * 4u + grp + 1u);
     uint32_t acc = 0;
     for (int it = 0; it < iters; it++) {
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) rd_random_lines(const uint4 *__restrict__
         for (int k = 0; k < K; k++) {
             x = x * 1664525u + 1013904223u;           // per-group LCG (group-uniform)
             const uint32_t line = (uint32_t)(((uint64_t)(x >> 8) * nlines) >> 24);
-            v[k] = __ldg(p + (size_t)line * 8 + gl);
+            v[k] = __ldg(p + (size_t)line * GL + gl);
         }
 #pragma unroll
         for (int k = 0; k < K; k++) acc ^= v[k].x ^ v[k].y ^ v[k].z ^ v[k].w;
@@ -101,6 +101,27 @@ int main() {
                 printf("random 128B lines  48 MB  blocks/SM %d  lines in flight/lane %d: %8.1f GB/s\n", occ, K, gbs);
                 best_rl = gbs > best_rl ? gbs : best_rl;
             }
+        }
+        cudaFree(p);
+    }
+    // 64-byte random segments (4-lane groups): the 512-rule-step shape
+    {
+        const size_t bytes = (size_t)48 << 20;
+        uint4 *p;
+        cudaMalloc(&p, bytes);
+        cudaMemset(p, 1, bytes);
+        const uint32_t nseg = (uint32_t)(bytes / 64);
+        for (int occ : {5, 8}) {
+            const int iters = 4096;
+            rd_random_lines<4, 4><<<sms * occ, 256>>>(p, nseg, 16, out);
+            cudaEventRecord(a);
+            rd_random_lines<4, 4><<<sms * occ, 256>>>(p, nseg, iters, out);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            const double segs = (double)sms * occ * 256 / 4 * 4 * iters;
+            printf("random 64B segments 48 MB  blocks/SM %d  4 in flight/lane: %8.1f GB/s\n", occ, segs * 64 / ms / 1e6);
         }
         cudaFree(p);
     }
