@@ -241,6 +241,7 @@ def main() -> int:
     ap.add_argument("--ms-words", type=int, default=0, help="match-set scan: words per lane per step (1, 2, 4)")
     ap.add_argument("--ms-group", type=int, default=0, help="match-set scan: lanes per packet (8, 16, 32)")
     ap.add_argument("--ms-summary", type=int, default=-1, help="match-set block summaries: 0 off, 1 on, 2 auto")
+    ap.add_argument("--ms-compress", type=int, default=-1, help="compressed match-set rows: 0 off, 1 on, 2 auto")
     ap.add_argument("--ks", type=int, default=0)
     ap.add_argument("--sc", type=int, default=-1, help="warp-level short-circuit of the port tests (0/1)")
     ap.add_argument("--bucket", type=int, default=-1, help="group large batches by protocol (0/1)")
@@ -291,6 +292,8 @@ def main() -> int:
         _native.set_tuning("ms_group", args.ms_group)
     if args.ms_summary >= 0:
         _native.set_tuning("ms_summary", args.ms_summary)
+    if args.ms_compress >= 0:
+        _native.set_tuning("ms_compress", args.ms_compress)
     if args.ks:
         _native.set_tuning("ks", args.ks)
     if args.sc >= 0:

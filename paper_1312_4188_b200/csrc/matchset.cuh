@@ -40,6 +40,7 @@ int64_t g_ms_budget_mb = 0;    // device-memory budget for the tables (0 = a qua
 int g_ms_group = 0;            // lanes per packet (8, 16, 32; 0 = by ruleset size): 32 / group packets in flight per warp
 int g_ms_words = 4;            // words per lane per step: 32 * group * words rules per step
 int g_ms_summary = 2;          // block summaries: 0 off, 1 on, 2 auto (built and used when they skip enough)
+int g_ms_compress = 2;         // compressed rows: 0 off, 1 on, 2 auto (when the plain rows exceed the budget)
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
@@ -122,6 +123,100 @@ __global__ void __launch_bounds__(MS_BLOCK) ms_sum_kernel(const uint32_t *bits, 
     }
 }
 
+// Compressed rows: one descriptor per distinct line of (dimension, block).
+struct MsLineDesc {
+    uint32_t v;      // first value of the block-local interval
+    uint32_t b;      // block (rules 1024 b .. 1024 b + 1023)
+    uint16_t d, c;   // dimension, protocol class (sport)
+};
+
+// warp per line: lane = rule inside each word, one ballot per word (as
+// ms_build_kernel, on the block's 1024 rules only)
+__global__ void __launch_bounds__(MS_BLOCK) ms_line_kernel(const MsLineDesc *desc, int64_t nlines, int64_t n,
+                                                           const uint32_t *sb, const uint32_t *sm,
+                                                           const uint32_t *db, const uint32_t *dm,
+                                                           const uint16_t *slo, const uint16_t *shi,
+                                                           const uint16_t *dlo, const uint16_t *dhi,
+                                                           const uint8_t *proto, const int *cls_proto,
+                                                           uint32_t *lines) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    for (int64_t li = gw; li < nlines; li += nw) {
+        const MsLineDesc L = desc[li];
+        const int pcl = L.d == MSD_SPORT ? __ldg(cls_proto + L.c) : -1;
+        uint32_t mine = 0;
+#pragma unroll 4
+        for (int k = 0; k < 32; k++) {
+            const int64_t r = (int64_t)L.b * 1024 + k * 32 + lane;
+            bool m = false;
+            if (r < n) {
+                switch (L.d) {
+                    case MSD_SRC: m = (L.v & __ldg(sm + r)) == __ldg(sb + r); break;   // model.py:119-121
+                    case MSD_DST: m = (L.v & __ldg(dm + r)) == __ldg(db + r); break;
+                    case MSD_SPORT: {                                                // model.py:144-145, 224-225
+                        const int rp = __ldg(proto + r);
+                        m = (uint32_t)__ldg(slo + r) <= L.v && L.v <= (uint32_t)__ldg(shi + r) &&
+                            (rp == 0 || rp == pcl);
+                        break;
+                    }
+                    default: m = (uint32_t)__ldg(dlo + r) <= L.v && L.v <= (uint32_t)__ldg(dhi + r); break;
+                }
+            }
+            const uint32_t b = __ballot_sync(0xFFFFFFFFu, m);
+            if (lane == k) mine = b;
+        }
+        lines[li * 32 + lane] = mine;
+    }
+}
+
+// thread per (row, block) of one dimension: the row's block-local interval
+// (the last block boundary <= the row's first value) -> its line index
+__global__ void ms_ptr_kernel(const uint32_t *vals, int64_t rows, int64_t ivl, int is_sport, int64_t nblk,
+                              const uint32_t *bnd, const uint32_t *boff, uint16_t *ptr, int64_t pstride) {
+    const int64_t total = rows * nblk;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / nblk, b = t - row * nblk;
+        const int64_t c = is_sport ? row / ivl : 0;
+        const uint32_t v = __ldg(vals + (is_sport ? row - c * ivl : row));
+        const uint32_t b0 = __ldg(boff + b), cnt = __ldg(boff + b + 1) - b0;
+        uint32_t lo = 0, hi = cnt;  // first boundary > v
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(bnd + b0 + mid) <= v) lo = mid + 1;
+            else hi = mid;
+        }
+        PFW_CHECK(lo >= 1 && c * cnt + lo - 1 < 65536);
+        ptr[row * pstride + b] = (uint16_t)(c * cnt + lo - 1);
+    }
+}
+
+// Summary rows from compressed rows: lane k of word j looks at block 32j+k's
+// line of the row and tests it for a set bit.
+__global__ void __launch_bounds__(MS_BLOCK) ms_sum_cmp_kernel(const uint32_t *lines, const uint32_t *loff,
+                                                              const uint16_t *ptr, int64_t pstride, int64_t rows,
+                                                              int64_t blocks, int64_t sw, uint32_t *sum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    for (int64_t t = gw; t < rows * sw; t += nw) {
+        const int64_t row = t / sw, j = t - row * sw, blk = j * 32 + lane;
+        uint32_t any = 0;
+        if (blk < blocks) {
+            const uint4 *q = reinterpret_cast<const uint4 *>(
+                lines + ((size_t)__ldg(loff + blk) + __ldg(ptr + row * pstride + blk)) * 32);
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint4 v = __ldg(q + k);
+                any |= v.x | v.y | v.z | v.w;
+            }
+        }
+        const uint32_t b = __ballot_sync(0xFFFFFFFFu, any != 0u);
+        if (lane == 0) sum[row * sw + j] = b;
+    }
+}
+
 struct MsView {
     const uint32_t *bits0;    // the four dimensions' rows, one allocation
     uint32_t off[4];          // word offset of each dimension's rows from bits0
@@ -143,6 +238,20 @@ struct MsSum {
     uint32_t sw;              // summary words per row
 };
 struct MsNoSum {};
+// Compressed rows (CMP variant; also carries the summaries)
+struct MsCmp {
+    const uint32_t *sum[4];
+    uint32_t sw;
+    uint32_t pstride, nblk;   // u16 line indices per row, blocks per row
+    const uint16_t *ptr;      // line indices of every dimension's rows
+    uint64_t ptr_off[4];
+    const uint32_t *lines;    // distinct lines, 32 words each
+    const uint32_t *loff;     // [4 * nblk]: first line of (dimension, block)
+};
+template <bool SUM, bool CMP>
+struct MsArg {
+    using type = std::conditional_t<CMP, MsCmp, std::conditional_t<SUM, MsSum, MsNoSum>>;
+};
 
 // interval of an IP: index of the last boundary <= ip (boundary 0 is 0)
 __device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint2 *c, uint32_t ip) {
@@ -225,16 +334,21 @@ struct MsStep<1> {
 // later steps jump to the next block whose AND-summary bit is set, skipping
 // blocks no rule of which can match this packet (a set bit may still be a
 // false candidate: the block is then read and the search moves on).
-template <int MODE, int G, int V, bool WIN, bool SUM = false>
+// CMP: the rows are compressed (MatchSet::cmp): the lookup phase also parks
+// each packet's line indices for 16 blocks in shared memory; a step reads the
+// line (loff[d][block] + index) of each dimension (beyond those 16 blocks the
+// index comes from global memory).
+template <int MODE, int G, int V, bool WIN, bool SUM = false, bool CMP = false>
 __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
-    ms_scan_kernel(ScanParams p, MsView t, std::conditional_t<SUM, MsSum, MsNoSum> u) {
-    static_assert(!SUM || G * V == 32, "summary blocks are one step");
+    ms_scan_kernel(ScanParams p, MsView t, typename MsArg<SUM, CMP>::type u) {
+    static_assert(!(SUM || CMP) || G * V == 32, "summary / compressed blocks are one step");
     constexpr int P = 32 / G;                      // packets in flight per warp
     constexpr uint32_t STEP = (uint32_t)G * V;     // words per step
     constexpr uint32_t GMASK = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
     constexpr int LPB = PFW_MS_LPB, BATCH = 32 * LPB;  // packets per warp batch
     __shared__ uint4 s_off[MS_BLOCK / 32][BATCH];     // per warp: row offsets of the batch's packets
-    __shared__ uint4 s_row[SUM ? MS_BLOCK / 32 : 1][BATCH];  // per warp: row indices (SUM)
+    __shared__ uint4 s_row[(SUM || CMP) ? MS_BLOCK / 32 : 1][BATCH];  // per warp: row indices (SUM / CMP)
+    __shared__ uint4 s_ptr[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][8];  // CMP: line indices, 16 blocks x 4 dims
     __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match of the batch's packets
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
@@ -256,6 +370,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
         mlast[v] = wl > whi ? 0u : (wl == whi ? (0xFFFFFFFFu >> (31 - ((p.hi - 1) & 31))) : 0xFFFFFFFFu);
     }
     const uint32_t lv = (uint32_t)gl * V;
+    const uint32_t cab = (cbeg / 32u) & ~7u;  // CMP: first block of the parked line indices
     unsigned long long st_sum = 0, st_blocks = 0;
     unsigned st_max = 0;
 
@@ -291,7 +406,18 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 // word offsets from the common base, at the first step
                 s_off[warp][k * 32 + lane] = make_uint4(r.x * wp + cbeg + t.off[0], r.y * wp + cbeg + t.off[1],
                                                         r.z * wp + cbeg + t.off[2], r.w * wp + cbeg + t.off[3]);
-                if (SUM) s_row[SUM ? warp : 0][k * 32 + lane] = r;
+                if (SUM || CMP) s_row[(SUM || CMP) ? warp : 0][k * 32 + lane] = r;
+                if constexpr (CMP) {
+                    // line indices of 16 blocks from the 8-aligned block at or below the first
+                    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                    for (int d = 0; d < 4; d++) {
+                        const uint4 *q = reinterpret_cast<const uint4 *>(u.ptr + u.ptr_off[d] +
+                                                                         (size_t)rr[d] * u.pstride + cab);
+                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d] = __ldg(q);
+                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d + 1] = __ldg(q + 1);
+                    }
+                }
             }
             s_res[warp][k * 32 + lane] = PFW_NO_MATCH;
         }
@@ -327,7 +453,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         // to the blocks after this one, up to the window's last
                         scand = 0u;
                         if ((uint32_t)gl < u.sw) {
-                            const uint4 rw = s_row[SUM ? warp : 0][pj];
+                            const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
                             PFW_CHECK(rw.x < t.nrows[0] && rw.y < t.nrows[1] && rw.z < t.nrows[2] && rw.w < t.nrows[3]);
                             scand = __ldg(u.sum[0] + (size_t)rw.x * u.sw + gl) &
                                     __ldg(u.sum[1] + (size_t)rw.y * u.sw + gl) &
@@ -340,10 +466,34 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     }
                 }
                 if (SUM && act && gl == 0) nrd++;
-                PFW_CHECK(!act || (pj < nv && (uint64_t)max(max(o0, o1), max(o2, o3)) + V <= t.words));
+                PFW_CHECK(!act || (pj < nv && (CMP || (uint64_t)max(max(o0, o1), max(o2, o3)) + V <= t.words)));
                 if (act) {
                     MsStep<V> st;
-                    st.load(t.bits0 + o0, t.bits0 + o1, t.bits0 + o2, t.bits0 + o3);
+                    if constexpr (CMP) {
+                        const uint32_t b = cbeg / 32u + (uint32_t)s;  // this step's block
+                        const int j = (int)(b - cab);
+                        uint32_t q0, q1, q2, q3;
+                        if (j < 16) {
+                            const uint16_t *sp = reinterpret_cast<const uint16_t *>(&s_ptr[CMP ? warp : 0][CMP ? pj : 0][0]);
+                            q0 = sp[j];
+                            q1 = sp[16 + j];
+                            q2 = sp[32 + j];
+                            q3 = sp[48 + j];
+                        } else {
+                            const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
+                            q0 = __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
+                            q1 = __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
+                            q2 = __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
+                            q3 = __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
+                        }
+                        const uint32_t *l = u.lines + lv;
+                        st.load(l + ((size_t)(__ldg(u.loff + b) + q0) << 5),
+                                l + ((size_t)(__ldg(u.loff + u.nblk + b) + q1) << 5),
+                                l + ((size_t)(__ldg(u.loff + 2 * u.nblk + b) + q2) << 5),
+                                l + ((size_t)(__ldg(u.loff + 3 * u.nblk + b) + q3) << 5));
+                    } else {
+                        st.load(t.bits0 + o0, t.bits0 + o1, t.bits0 + o2, t.bits0 + o3);
+                    }
 #pragma unroll
                     for (int v = 0; v < V; v++) {
                         x[v] = st.w[0][v] & st.w[1][v] & st.w[2][v] & st.w[3][v];
@@ -455,6 +605,9 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
 void ms_free(MatchSet *m) {
     if (!m) return;
     if (m->d_bits_all) cudaFree(m->d_bits_all);
+    if (m->d_lines) cudaFree(m->d_lines);
+    if (m->d_loff) cudaFree(m->d_loff);
+    if (m->d_ptr_all) cudaFree(m->d_ptr_all);
     for (auto *b : m->d_sum)
         if (b) cudaFree(b);
     for (auto *b : m->d_ipb)
@@ -522,7 +675,12 @@ int ms_summaries(pfw_ruleset *h, const std::vector<uint32_t> &bs, const std::vec
     cudaError_t e = cudaSuccess;
     for (int d = 0; d < 4 && e == cudaSuccess; d++) e = cudaMalloc(&m->d_sum[d], ((size_t)m->rows[d] * sw + 8) * 4);
     for (int d = 0; d < 4 && e == cudaSuccess; d++) {
-        ms_sum_kernel<<<(unsigned)(h->sms * 8), MS_BLOCK>>>(m->d_bits[d], m->rows[d], m->wp, sw, m->d_sum[d]);
+        if (m->cmp)
+            ms_sum_cmp_kernel<<<(unsigned)(h->sms * 8), MS_BLOCK>>>(m->d_lines, m->d_loff + d * m->nblk,
+                                                                    m->d_ptr_all + m->ptr_off[d], m->pstride,
+                                                                    m->rows[d], blocks, sw, m->d_sum[d]);
+        else
+            ms_sum_kernel<<<(unsigned)(h->sms * 8), MS_BLOCK>>>(m->d_bits[d], m->rows[d], m->wp, sw, m->d_sum[d]);
         g_launches++;
     }
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -559,6 +717,98 @@ int ms_summaries(pfw_ruleset *h, const std::vector<uint32_t> &bs, const std::vec
     m->use_sum = g_ms_summary == 1 || keep < MS_SUM_KEEP_MAX;
     for (int d = 0; d < 4; d++) m->bytes += ((size_t)m->rows[d] * sw + 8) * 4;
     return PFW_OK;
+}
+
+// Compressed rows (see MatchSet::cmp): per (dimension, block) the block's own
+// boundaries -> its distinct lines (built by the reference predicate on the
+// block's rules), and per row and block the index of the row's line.  The
+// device rule columns / interval values come from ms_create's build.
+// Returns cudaSuccess with m->cmp unset when a block has more than 65536
+// lines (u16 indices).
+cudaError_t ms_compress_build(pfw_ruleset *h, MatchSet *m, int64_t n, const uint8_t *proto,
+                              const uint32_t *src_base, const uint32_t *src_mask, const uint16_t *sport_lo,
+                              const uint16_t *sport_hi, const uint32_t *dst_base, const uint32_t *dst_mask,
+                              const uint16_t *dport_lo, const uint16_t *dport_hi, int ncls,
+                              const uint32_t *d_sb, const uint32_t *d_sm, const uint32_t *d_db,
+                              const uint32_t *d_dm, const uint16_t *d_slo, const uint16_t *d_shi,
+                              const uint16_t *d_dlo, const uint16_t *d_dhi, const uint8_t *d_pr,
+                              const int *d_clsp, uint32_t *const *d_vals, size_t budget) {
+    const int64_t nblk = m->wp / 32;
+    std::vector<uint32_t> bnd, boff((size_t)(4 * nblk + 1)), loff((size_t)(4 * nblk + 1));
+    std::vector<MsLineDesc> desc;
+    std::vector<uint32_t> v;
+    for (int d = 0; d < 4; d++) {
+        for (int64_t b = 0; b < nblk; b++) {
+            v.assign(1, 0u);
+            const int64_t r0 = b * 1024, r1 = std::min<int64_t>(n, r0 + 1024);
+            for (int64_t r = r0; r < r1; r++) {
+                if (d < 2) {
+                    const uint32_t base = d == MSD_SRC ? src_base[r] : dst_base[r];
+                    const uint32_t mask = d == MSD_SRC ? src_mask[r] : dst_mask[r];
+                    if (base & ~mask) continue;
+                    v.push_back(base);
+                    const uint64_t e = (uint64_t)(base | ~mask) + 1;
+                    if (e < (1ull << 32)) v.push_back((uint32_t)e);
+                } else {
+                    const uint32_t lo = d == MSD_SPORT ? sport_lo[r] : dport_lo[r];
+                    const uint32_t hi = d == MSD_SPORT ? sport_hi[r] : dport_hi[r];
+                    if (lo > hi) continue;
+                    v.push_back(lo);
+                    if (hi + 1 < 65536u) v.push_back(hi + 1);
+                }
+            }
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            const int ncl = d == MSD_SPORT ? ncls : 1;
+            if ((int64_t)v.size() * ncl > 65536) return cudaSuccess;  // u16 line indices
+            boff[(size_t)(d * nblk + b)] = (uint32_t)bnd.size();
+            loff[(size_t)(d * nblk + b)] = (uint32_t)desc.size();
+            bnd.insert(bnd.end(), v.begin(), v.end());
+            for (int c = 0; c < ncl; c++)
+                for (uint32_t x : v) desc.push_back(MsLineDesc{x, (uint32_t)b, (uint16_t)d, (uint16_t)c});
+        }
+    }
+    boff[(size_t)(4 * nblk)] = (uint32_t)bnd.size();
+    loff[(size_t)(4 * nblk)] = (uint32_t)desc.size();
+    const int64_t pstride = ((nblk + 16 + 7) / 8) * 8;
+    size_t need = desc.size() * 128;
+    for (int d = 0; d < 4; d++) need += (size_t)m->rows[d] * (size_t)pstride * 2;
+    if (need > budget) return cudaSuccess;  // over budget even compressed
+    m->nblk = nblk;
+    m->pstride = pstride;
+    m->nlines = (int64_t)desc.size();
+    uint32_t *d_bnd = nullptr, *d_boff = nullptr;
+    MsLineDesc *d_desc = nullptr;
+    cudaError_t e = ms_upload(&d_bnd, bnd.data(), bnd.size());
+    if (e == cudaSuccess) e = ms_upload(&d_boff, boff.data(), boff.size());
+    if (e == cudaSuccess) e = ms_upload(&m->d_loff, loff.data(), loff.size());
+    if (e == cudaSuccess) e = ms_upload(&d_desc, desc.data(), desc.size());
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_lines, ((size_t)m->nlines * 32 + 4 * 32) * 4);
+    if (e == cudaSuccess) e = cudaMemset(m->d_lines + (size_t)m->nlines * 32, 0, 4 * 32 * 4);
+    size_t pent = 0;
+    for (int d = 0; d < 4; d++) {
+        m->ptr_off[d] = pent;
+        pent += (size_t)m->rows[d] * (size_t)m->pstride;
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_ptr_all, (pent + 16) * 2);
+    if (e == cudaSuccess) e = cudaMemset(m->d_ptr_all, 0, (pent + 16) * 2);
+    if (e == cudaSuccess) {
+        ms_line_kernel<<<(unsigned)(h->sms * 8), MS_BLOCK>>>(d_desc, m->nlines, n, d_sb, d_sm, d_db, d_dm, d_slo,
+                                                             d_shi, d_dlo, d_dhi, d_pr, d_clsp, m->d_lines);
+        g_launches++;
+        for (int d = 0; d < 4; d++) {
+            ms_ptr_kernel<<<(unsigned)(h->sms * 8), 256>>>(d_vals[d], m->rows[d], m->sp_rows, d == MSD_SPORT, nblk,
+                                                           d_bnd, d_boff + d * nblk, m->d_ptr_all + m->ptr_off[d],
+                                                           m->pstride);
+            g_launches++;
+        }
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    for (void *q : {(void *)d_bnd, (void *)d_boff, (void *)d_desc})
+        if (q) cudaFree(q);
+    if (e == cudaSuccess) m->cmp = true;
+    return e;
 }
 
 // Build the match sets of ruleset h (host columns as given to
@@ -605,7 +855,10 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     uint64_t all_words = 0;  // word offsets from the common base are 32-bit in the scan
     for (int d = 0; d < 4; d++) all_words += (uint64_t)m->rows[d] * (uint64_t)m->wp + 4 * 32;
     fits = fits && all_words < (1ull << 32);
-    if (!fits) {
+    // compressed rows: forced, or (auto) when the plain rows do not fit --
+    // they are ~20x smaller but scan slower while the plain rows fit
+    const bool use_cmp = g_ms_compress == 1 || (g_ms_compress == 2 && !fits);
+    if (!fits && !use_cmp) {
         delete m;
         return PFW_OK;  // too large for the budget: rule-by-rule scan
     }
@@ -643,7 +896,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     // one allocation for the four dimensions (the scan addresses every row
     // from one base); + one 4-word-per-lane step of padding after each: the
     // last step of a row may read past its end (masked), also on a last row
-    {
+    if (!use_cmp) {
         size_t words = 0;
         for (int d = 0; d < 4; d++) words += (size_t)m->rows[d] * (size_t)m->wp + 4 * 32;
         e = cudaMalloc(&m->d_bits_all, words * 4);
@@ -676,7 +929,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     if (e == cudaSuccess) e = ms_upload(&d_vals[1], bd.data(), bd.size());
     if (e == cudaSuccess) e = ms_upload(&d_vals[2], bsp.data(), bsp.size());
     if (e == cudaSuccess) e = ms_upload(&d_vals[3], bdp.data(), bdp.size());
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && !use_cmp) {
         MsBuildArgs a{};
         a.n = n;
         a.wp = m->wp;
@@ -703,6 +956,41 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
         e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
     }
+    if (e == cudaSuccess && use_cmp) {
+        e = ms_compress_build(h, m, n, proto, src_base, src_mask, sport_lo, sport_hi, dst_base, dst_mask, dport_lo,
+                              dport_hi, (int)cls_proto.size(), d_sb, d_sm, d_db, d_dm, d_slo, d_shi, d_dlo, d_dhi,
+                              d_pr, d_clsp, d_vals, budget);
+        if (e == cudaSuccess && !m->cmp) e = cudaErrorMemoryAllocation;  // not compressible / over budget
+    }
+    // summaries (from whichever rows were built); when the scan will use them
+    // (rules clustered enough to skip blocks), auto also compresses plain rows:
+    // the summary scan visits few, scattered blocks, which the compressed
+    // rows' small footprint keeps in L2 (adversarial config: +9%)
+    int src = PFW_OK;
+    if (e == cudaSuccess) {
+        h->ms = m;
+        src = ms_summaries(h, bs, bd, bsp, bdp);
+        h->ms = nullptr;
+        if (src == PFW_OK && !m->cmp && m->use_sum && g_ms_compress == 2) {
+            const cudaError_t ec = ms_compress_build(h, m, n, proto, src_base, src_mask, sport_lo, sport_hi, dst_base,
+                                                     dst_mask, dport_lo, dport_hi, (int)cls_proto.size(), d_sb, d_sm,
+                                                     d_db, d_dm, d_slo, d_shi, d_dlo, d_dhi, d_pr, d_clsp, d_vals,
+                                                     budget);
+            if (ec == cudaSuccess && m->cmp) {  // drop the plain rows
+                cudaFree(m->d_bits_all);
+                m->d_bits_all = nullptr;
+                for (auto *&q : m->d_bits) q = nullptr;
+            } else {  // optional: keep the plain rows
+                cudaGetLastError();
+                for (void *q : {(void *)m->d_lines, (void *)m->d_loff, (void *)m->d_ptr_all})
+                    if (q) cudaFree(q);
+                m->d_lines = nullptr;
+                m->d_loff = nullptr;
+                m->d_ptr_all = nullptr;
+                m->cmp = false;
+            }
+        }
+    }
     for (void *q : {(void *)d_sb, (void *)d_sm, (void *)d_db, (void *)d_dm, (void *)d_slo, (void *)d_shi,
                     (void *)d_dlo, (void *)d_dhi, (void *)d_pr, (void *)d_clsp, (void *)d_vals[0],
                     (void *)d_vals[1], (void *)d_vals[2], (void *)d_vals[3]})
@@ -715,8 +1003,19 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
         }
         return set_err(PFW_ERR_CUDA, "match-set build failed: %s", cudaGetErrorString(e));
     }
+    if (src != PFW_OK) {
+        ms_free(m);
+        return src;
+    }
+    if (m->cmp) {  // account the compressed rows instead of the plain ones
+        size_t plain = 0;
+        for (int d = 0; d < 4; d++) plain += (size_t)m->rows[d] * (size_t)m->wp * 4;
+        m->bytes -= plain;
+        m->bytes += ((size_t)m->nlines * 32 + 4 * 32) * 4 + (size_t)(4 * m->nblk + 1) * 4;
+        for (int d = 0; d < 4; d++) m->bytes += (size_t)m->rows[d] * (size_t)m->pstride * 2;
+    }
     h->ms = m;
-    return ms_summaries(h, bs, bd, bsp, bdp);
+    return PFW_OK;
 }
 
 template <int MODE>
@@ -742,16 +1041,27 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     MsSum u{};
     for (int d = 0; d < 4; d++) u.sum[d] = m->d_sum[d];
     u.sw = (uint32_t)m->sw;
+    MsCmp uc{};
+    for (int d = 0; d < 4; d++) uc.sum[d] = m->d_sum[d];
+    uc.sw = (uint32_t)m->sw;
+    uc.pstride = (uint32_t)m->pstride;
+    uc.nblk = (uint32_t)m->nblk;
+    uc.ptr = m->d_ptr_all;
+    for (int d = 0; d < 4; d++) uc.ptr_off[d] = m->ptr_off[d];
+    uc.lines = m->d_lines;
+    uc.loff = m->d_loff;
     void (*kern)(ScanParams, MsView, MsNoSum) = nullptr;
     void (*kern_s)(ScanParams, MsView, MsSum) = nullptr;
+    void (*kern_c)(ScanParams, MsView, MsCmp) = nullptr;
     const bool win = !(p.lo == 0 && p.hi == h->n);
     // auto: 8 lanes (4 packets in flight, 1024-rule steps) while the rows'
     // leading lines fit in L2; 16 lanes (2048-rule steps, fewer iterations)
-    // for large rulesets whose scans run long and mostly miss L2
-    const int grp = g_ms_group ? g_ms_group : (h->n > 16384 ? 16 : 8);
-    // block summaries: one step = one 1024-rule block (8 lanes x 4 words)
-    const bool sum = m->use_sum && m->sw > 0 && g_ms_summary != 0 && g_ms_words == 4 &&
-                     (g_ms_group == 0 || g_ms_group == 8);
+    // for large plain rulesets whose scans run long and mostly miss L2
+    const int grp = g_ms_group ? g_ms_group : (h->n > 16384 && !m->cmp ? 16 : 8);
+    // block summaries / compressed rows: one step = one 1024-rule block (8 lanes x 4 words)
+    const bool sum = m->use_sum && m->sw > 0 && g_ms_summary != 0 &&
+                     (m->cmp || (g_ms_words == 4 && (g_ms_group == 0 || g_ms_group == 8)));
+    // (compressed rows always scan on 8 lanes x 4 words: one step = one block)
 #define PFW_MS_PICK(G_, V_)                                                                     \
     if (grp == G_ && g_ms_words == V_)                                                   \
         kern = win ? ms_scan_kernel<MODE, G_, V_, true> : ms_scan_kernel<MODE, G_, V_, false>;
@@ -762,11 +1072,20 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     PFW_MS_PICK(32, 2)
     PFW_MS_PICK(32, 1)
 #undef PFW_MS_PICK
-    if (sum) kern_s = win ? ms_scan_kernel<MODE, 8, 4, true, true> : ms_scan_kernel<MODE, 8, 4, false, true>;
-    if (!kern && !kern_s) return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
+    if (m->cmp) {
+        kern = nullptr;
+        if (sum) kern_c = win ? ms_scan_kernel<MODE, 8, 4, true, true, true> : ms_scan_kernel<MODE, 8, 4, false, true, true>;
+        else kern_c = win ? ms_scan_kernel<MODE, 8, 4, true, false, true> : ms_scan_kernel<MODE, 8, 4, false, false, true>;
+    } else if (sum) {
+        kern = nullptr;
+        kern_s = win ? ms_scan_kernel<MODE, 8, 4, true, true> : ms_scan_kernel<MODE, 8, 4, false, true>;
+    }
+    if (!kern && !kern_s && !kern_c)
+        return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
     int occ = g_ctas_per_sm;
     if (occ <= 0) {
-        if (kern_s) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_s, MS_BLOCK, 0));
+        if (kern_c) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_c, MS_BLOCK, 0));
+        else if (kern_s) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_s, MS_BLOCK, 0));
         else CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, MS_BLOCK, 0));
         if (occ < 1) occ = 1;
     }
@@ -774,17 +1093,16 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     const int64_t need = (p.n + MS_BLOCK * PFW_MS_LPB - 1) / (MS_BLOCK * PFW_MS_LPB);  // one batch per warp
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
-    if (kern_s) {
-        ScanParams pc = p;
-        if (g_count_blocks) {
-            if (!g_counter_dev) {
-                CUDA_TRY(cudaMalloc(&g_counter_dev, sizeof(unsigned long long)));
-                CUDA_TRY(cudaMemset(g_counter_dev, 0, sizeof(unsigned long long)));
-            }
-            pc.blocks_read = g_counter_dev;
+    ScanParams pc = p;
+    if ((kern_s || (kern_c && sum)) && g_count_blocks) {
+        if (!g_counter_dev) {
+            CUDA_TRY(cudaMalloc(&g_counter_dev, sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemset(g_counter_dev, 0, sizeof(unsigned long long)));
         }
-        kern_s<<<(unsigned)grid, MS_BLOCK, 0, st>>>(pc, t, u);
+        pc.blocks_read = g_counter_dev;
     }
+    if (kern_c) kern_c<<<(unsigned)grid, MS_BLOCK, 0, st>>>(pc, t, uc);
+    else if (kern_s) kern_s<<<(unsigned)grid, MS_BLOCK, 0, st>>>(pc, t, u);
     else kern<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, MsNoSum{});
     CUDA_TRY(cudaGetLastError());
     g_launches++;

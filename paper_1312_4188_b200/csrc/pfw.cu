@@ -156,6 +156,18 @@ struct MatchSet {
     int64_t sw = 0;             // summary words per row (0: not built)
     double sum_keep = 1.0;      // expected fraction of blocks a packet's AND-summary keeps
     bool use_sum = false;       // scan with summaries (auto: sum_keep below the threshold)
+    // compressed rows (large rulesets): inside one 1024-rule block, rows differ
+    // only where a boundary of that block's rules separates them, so each
+    // (dimension, block) stores its <= 2*1024+1 distinct 128-byte lines once and
+    // each row a u16 line index per block; the plain rows are then dropped
+    bool cmp = false;
+    int64_t nblk = 0;           // blocks per row (wp / 32)
+    int64_t pstride = 0;        // u16 entries per row of line indices (>= nblk + 16, multiple of 8)
+    uint16_t *d_ptr_all = nullptr;  // line indices: dimension d's rows at ptr_off[d]
+    uint64_t ptr_off[4] = {};
+    uint32_t *d_lines = nullptr;    // distinct lines, 32 words each
+    uint32_t *d_loff = nullptr;     // [4 * nblk]: first line of (d, block)
+    int64_t nlines = 0;
 };
 
 struct pfw_ruleset {
@@ -1375,6 +1387,9 @@ int pfw_set_tuning(const char *key, int64_t value) {
         g_ms_words = (int)value;
     } else if (!strcmp(key, "count_blocks")) {
         g_count_blocks = value != 0;
+    } else if (!strcmp(key, "ms_compress")) {
+        if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_compress: 0 off, 1 on, 2 auto");
+        g_ms_compress = (int)value;
     } else if (!strcmp(key, "ms_summary")) {
         if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_summary: 0 off, 1 on, 2 auto");
         g_ms_summary = (int)value;

@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2), ("count_blocks", 0)):
+                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2)):
         _native.set_tuning(k, v)
 
 
@@ -765,3 +765,56 @@ def test_rule_counts_at_word_line_and_step_edges(R):
         _native.set_tuning("algo", algo)
         for lo, hi in ((0, R), (R // 2, R), (max(R - 1, 0), R)):
             np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+
+
+# ------------------------------------------------- compressed match-set rows
+
+def test_compressed_rows_forced():
+    """Compressed rows (per block the distinct lines + u16 line indices per
+    row) forced on: goldens, windows, engines, shards, the adversarial recipe
+    (with summaries), every requested shape -- identical results."""
+    _native.set_tuning("ms_compress", 1)   # applies to rulesets built from here on
+    _native.set_tuning("algo", 2)
+    for name, rn, tn in SCANS:
+        test_scan_matches_reference_golden(name, rn, tn)
+    test_scan_windows()
+    test_windows_every_alignment_vs_oracle()
+    for model in ("data", "function", "hybrid"):
+        test_engine_models_match_reference_golden(model)
+    test_function_parallel_100k_rules()
+    test_adversarial_recipe_sample()
+    test_ragged_sizes_and_empty()
+    test_unnormalised_and_inverted_rules_never_match()
+    test_fused_min_combine_virtual_ranks(1)
+    test_rule_shard_windows_and_verdicts()
+    test_match_set_interval_edges()       # (iterates the shapes: compressed rows ignore them)
+    for rn in ("r10000_s1", "r100000_s1"):
+        c = compiled(golden_rules(rn))
+        g = golden(f"scan_{rn}_t20000.npz")
+        p = pfw.generate_traffic_device(pfw.TrafficProfile(count=20_000, seed=2), device=0)
+        np.testing.assert_array_equal(c.scan_range(p, 0, c.num_rules), g["first"])
+        # a window past the 16 parked blocks (line indices from global memory)
+        lo = 20 * 1024 + 7
+        rules = golden_rules(rn)
+        sub = {k: v for k, v in p.columns().items()}
+        if c.num_rules > lo + 100:
+            np.testing.assert_array_equal(c.scan_range(p, lo, c.num_rules),
+                                          oracle.scan_range(rules, sub, lo, c.num_rules))
+
+
+def test_compressed_rows_when_plain_exceeds_budget():
+    """Auto: plain rows over the memory budget -> compressed rows (not the rule
+    scan); the reported size is the compressed one."""
+    big = compiled(golden_rules("r100000_s1"))
+    plain = _native.lib().pfw_ruleset_matchset_bytes(big.handle)
+    _native.set_tuning("matchset_budget_mb", 1024)       # plain 100K rows need ~7 GB
+    c = compiled(golden_rules("r100000_s1"))
+    got = _native.lib().pfw_ruleset_matchset_bytes(c.handle)
+    assert 0 < got < plain // 10
+    g = golden("scan_r100000_s1_t20000.npz")
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=20_000, seed=2), device=0)
+    _native.set_tuning("algo", 2)
+    np.testing.assert_array_equal(c.scan_range(p, 0, c.num_rules), g["first"])
+    _native.set_tuning("ms_compress", 0)                 # compression off: over budget -> rule scan
+    c2 = compiled(golden_rules("r100000_s1"))
+    assert _native.lib().pfw_ruleset_matchset_bytes(c2.handle) == 0

@@ -1,4 +1,4 @@
-mkdir -p gpurun_out/verify
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 1800 python -m pytest tests -q -m gpu 2>&1 | tail -2
-timeout 600 python bench.py --impl reference > gpurun_out/verify/ref.json 2>&1; tail -1 gpurun_out/verify/ref.json | cut -c1-120
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+for cfg in adversarial data function grid; do
+    timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-cpu --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$cfg', d['value'], d['ms_per_step'], d['roofline']['frac'], d['config']['algorithm'])"
+done
