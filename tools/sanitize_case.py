@@ -55,6 +55,21 @@ for summary in (0, 1):
     _native.set_tuning("ms_words", 4)
     _native.set_tuning("algo", 0)
 _native.set_tuning("ms_summary", 2)
+# compressed rows (forced), with and without summaries, windows and partitions
+for summary in (0, 1):
+    _native.set_tuning("ms_summary", summary)
+    _native.set_tuning("ms_compress", 1)
+    cc = pfw.CompiledRuleset.from_columns(rules, device=0)
+    _native.set_tuning("algo", 2)
+    for lo, hi in ((0, 700), (37, 650), (699, 700)):
+        np.testing.assert_array_equal(cc.scan_range(p, lo, hi), oracle.scan_range(rules, pk, lo, hi))
+        checks += 1
+    res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=3)).run_arrays(cc, p)
+    np.testing.assert_array_equal(res.first, oracle.engine_run(rules, pk, "function", 3)[0])
+    checks += 1
+    _native.set_tuning("algo", 0)
+_native.set_tuning("ms_compress", 2)
+_native.set_tuning("ms_summary", 2)
 adv_rules = oracle.adversarial_rules(50_000)
 adv_pk = oracle.adversarial_traffic(4_000)
 ca = pfw.CompiledRuleset.from_columns(adv_rules, device=0)
