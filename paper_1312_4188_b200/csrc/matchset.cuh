@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
     constexpr int LPB = PFW_MS_LPB, BATCH = 32 * LPB;  // packets per warp batch
     __shared__ uint4 s_off[MS_BLOCK / 32][BATCH];     // per warp: row offsets of the batch's packets
     __shared__ uint4 s_row[(SUM || CMP) ? MS_BLOCK / 32 : 1][BATCH];  // per warp: row indices (SUM / CMP)
-    __shared__ uint4 s_ptr[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][8];  // CMP: line indices, 16 blocks x 4 dims
+    __shared__ uint4 s_ptr[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][8];  // CMP: line numbers, 8 blocks x 4 dims (u32)
     __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match of the batch's packets
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
@@ -408,14 +408,20 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                                                         r.z * wp + cbeg + t.off[2], r.w * wp + cbeg + t.off[3]);
                 if (SUM || CMP) s_row[(SUM || CMP) ? warp : 0][k * 32 + lane] = r;
                 if constexpr (CMP) {
-                    // line indices of 16 blocks from the 8-aligned block at or below the first
+                    // absolute line numbers (loff + index) of the 8 blocks from
+                    // the 8-aligned block at or below the first, per dimension
                     const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
                     for (int d = 0; d < 4; d++) {
-                        const uint4 *q = reinterpret_cast<const uint4 *>(u.ptr + u.ptr_off[d] +
-                                                                         (size_t)rr[d] * u.pstride + cab);
-                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d] = __ldg(q);
-                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d + 1] = __ldg(q + 1);
+                        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(u.ptr + u.ptr_off[d] +
+                                                                              (size_t)rr[d] * u.pstride + cab));
+                        const uint32_t *lo = u.loff + d * u.nblk + cab;  // (loff has 8 entries of slack)
+                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d] =
+                            make_uint4(__ldg(lo + 0) + (q.x & 0xFFFFu), __ldg(lo + 1) + (q.x >> 16),
+                                       __ldg(lo + 2) + (q.y & 0xFFFFu), __ldg(lo + 3) + (q.y >> 16));
+                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d + 1] =
+                            make_uint4(__ldg(lo + 4) + (q.z & 0xFFFFu), __ldg(lo + 5) + (q.z >> 16),
+                                       __ldg(lo + 6) + (q.w & 0xFFFFu), __ldg(lo + 7) + (q.w >> 16));
                     }
                 }
             }
@@ -472,25 +478,23 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     if constexpr (CMP) {
                         const uint32_t b = cbeg / 32u + (uint32_t)s;  // this step's block
                         const int j = (int)(b - cab);
-                        uint32_t q0, q1, q2, q3;
-                        if (j < 16) {
-                            const uint16_t *sp = reinterpret_cast<const uint16_t *>(&s_ptr[CMP ? warp : 0][CMP ? pj : 0][0]);
+                        uint32_t q0, q1, q2, q3;  // absolute line numbers
+                        if (j < 8) {
+                            const uint32_t *sp = reinterpret_cast<const uint32_t *>(&s_ptr[CMP ? warp : 0][CMP ? pj : 0][0]);
                             q0 = sp[j];
-                            q1 = sp[16 + j];
-                            q2 = sp[32 + j];
-                            q3 = sp[48 + j];
+                            q1 = sp[8 + j];
+                            q2 = sp[16 + j];
+                            q3 = sp[24 + j];
                         } else {
                             const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
-                            q0 = __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
-                            q1 = __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
-                            q2 = __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
-                            q3 = __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
+                            q0 = __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
+                            q1 = __ldg(u.loff + u.nblk + b) + __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
+                            q2 = __ldg(u.loff + 2 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
+                            q3 = __ldg(u.loff + 3 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
                         }
                         const uint32_t *l = u.lines + lv;
-                        st.load(l + ((size_t)(__ldg(u.loff + b) + q0) << 5),
-                                l + ((size_t)(__ldg(u.loff + u.nblk + b) + q1) << 5),
-                                l + ((size_t)(__ldg(u.loff + 2 * u.nblk + b) + q2) << 5),
-                                l + ((size_t)(__ldg(u.loff + 3 * u.nblk + b) + q3) << 5));
+                        st.load(l + ((size_t)q0 << 5), l + ((size_t)q1 << 5), l + ((size_t)q2 << 5),
+                                l + ((size_t)q3 << 5));
                     } else {
                         st.load(t.bits0 + o0, t.bits0 + o1, t.bits0 + o2, t.bits0 + o3);
                     }
@@ -781,6 +785,7 @@ cudaError_t ms_compress_build(pfw_ruleset *h, MatchSet *m, int64_t n, const uint
     MsLineDesc *d_desc = nullptr;
     cudaError_t e = ms_upload(&d_bnd, bnd.data(), bnd.size());
     if (e == cudaSuccess) e = ms_upload(&d_boff, boff.data(), boff.size());
+    loff.resize(loff.size() + 8, loff.back());  // slack: the lookup phase reads 8 entries from any block
     if (e == cudaSuccess) e = ms_upload(&m->d_loff, loff.data(), loff.size());
     if (e == cudaSuccess) e = ms_upload(&d_desc, desc.data(), desc.size());
     if (e == cudaSuccess) e = cudaMalloc(&m->d_lines, ((size_t)m->nlines * 32 + 4 * 32) * 4);
