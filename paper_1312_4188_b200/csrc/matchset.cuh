@@ -335,9 +335,9 @@ struct MsStep<1> {
 // blocks no rule of which can match this packet (a set bit may still be a
 // false candidate: the block is then read and the search moves on).
 // CMP: the rows are compressed (MatchSet::cmp): the lookup phase also parks
-// each packet's line indices for 16 blocks in shared memory; a step reads the
-// line (loff[d][block] + index) of each dimension (beyond those 16 blocks the
-// index comes from global memory).
+// each packet's absolute line numbers (loff[d][block] + index) for 8 blocks
+// in shared memory; a step reads those lines (beyond the 8 blocks the index
+// comes from global memory).
 template <int MODE, int G, int V, bool WIN, bool SUM = false, bool CMP = false>
 __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
     ms_scan_kernel(ScanParams p, MsView t, typename MsArg<SUM, CMP>::type u) {
