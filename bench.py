@@ -549,6 +549,7 @@ def main() -> int:
                                          " (NCCL MIN all-reduce)" if w.model == "function" else ""),
                        "l2": "flushed between timed steps (256 MiB write)",
                        "algorithm": (f"match-set scan (per-field interval bitmaps, {ms_bytes / 2**20:.0f} MiB"
+                                     + (", compressed rows" if _native.ruleset_info(compiled.handle, "compressed") else "")
                                      + (", block summaries" if blocks_read else "") + ")"
                                      if algo == "matchset" else "rule-by-rule scan"),
                        "rule_layout": "protocol-split chains" if args.proto_split else "single ordered table",

@@ -85,6 +85,9 @@ int64_t pfw_ruleset_matchset_bytes(pfw_ruleset_t h);
  * comparison counts are window-relative as before.  pfw_verdicts rejects a
  * partial shard (combined indices need the whole ruleset's actions). */
 int pfw_ruleset_set_shard(pfw_ruleset_t h, int64_t index_base, int64_t total);
+/* Ruleset introspection: "matchset_bytes", "compressed" (1: compressed match-set
+ * rows), "summaries" (1: the scan uses block summaries), "index_base". */
+int pfw_ruleset_info(pfw_ruleset_t h, const char *key, int64_t *value);
 
 /* Host packet packing.  Replaces PacketArrays.from_packets
  * (classifier.py:75-83) for column input: writes n 16-byte records. */
@@ -216,7 +219,8 @@ int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t 
 /* Launch-count / tuning introspection (bench + tests).  Tuning keys include
  * "algo" (0 auto: match sets when built, 1 rule-by-rule scan, 2 match sets),
  * "matchset" (build match sets at ruleset creation, default 1),
- * "matchset_budget_mb" (0 = a quarter of free device memory), "ms_group"
+ * "matchset_budget_mb" (0 = a quarter of free device memory), "ms_compress"
+ * (compressed rows: 0 off, 1 on, 2 auto), "ms_group"
  * (lanes per packet), "ms_words" (words per lane per step), "ms_summary" (1024-rule
  * block summaries: 0 off, 1 on, 2 auto; applies to rulesets created afterwards),
  * and the rule-scan options "ks", "tile", "first_pass", "bucket",

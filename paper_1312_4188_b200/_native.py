@@ -44,6 +44,7 @@ _SIGS = {
     "pfw_ruleset_size": (_I64, [_P]),
     "pfw_ruleset_matchset_bytes": (_I64, [_P]),
     "pfw_ruleset_set_shard": (_I32, [_P, _I64, _I64]),
+    "pfw_ruleset_info": (_I32, [_P, ctypes.c_char_p, ctypes.POINTER(_I64)]),
     "pfw_ruleset_device": (_I32, [_P]),
     "pfw_pack_packets_host": (_I32, [_I64, _P, _P, _P, _P, _P, _P]),
     "pfw_scan_range": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P, _P]),
@@ -121,6 +122,13 @@ def require_device() -> None:
 
 def launch_count() -> int:
     return int(lib().pfw_launch_count())
+
+
+def ruleset_info(handle, key: str) -> int:
+    """pfw_ruleset_info: matchset_bytes / compressed / summaries / index_base."""
+    v = ctypes.c_int64(0)
+    check(lib().pfw_ruleset_info(handle, key.encode(), ctypes.byref(v)), f"pfw_ruleset_info({key})")
+    return int(v.value)
 
 
 def read_counter(name: str) -> int:

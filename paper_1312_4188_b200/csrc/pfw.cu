@@ -1565,6 +1565,17 @@ int64_t pfw_ruleset_size(pfw_ruleset_t h) { return h ? h->n : -1; }
 int pfw_ruleset_device(pfw_ruleset_t h) { return h ? h->device : -1; }
 int64_t pfw_ruleset_matchset_bytes(pfw_ruleset_t h) { return h && h->ms ? (int64_t)h->ms->bytes : 0; }
 
+int pfw_ruleset_info(pfw_ruleset_t h, const char *key, int64_t *value) {
+    if (!h || !key || !value) return set_err(PFW_ERR_INVALID, "null argument");
+    const MatchSet *m = h->ms;
+    if (!strcmp(key, "matchset_bytes")) *value = m ? (int64_t)m->bytes : 0;
+    else if (!strcmp(key, "compressed")) *value = m && m->cmp ? 1 : 0;
+    else if (!strcmp(key, "summaries")) *value = m && m->use_sum && m->sw > 0 ? 1 : 0;
+    else if (!strcmp(key, "index_base")) *value = h->index_base;
+    else return set_err(PFW_ERR_INVALID, "unknown ruleset info key '%s'", key);
+    return PFW_OK;
+}
+
 int pfw_ruleset_set_shard(pfw_ruleset_t h, int64_t index_base, int64_t total) {
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (index_base < 0 || total < 0 || index_base + h->n > total || total > PFW_MAX_RULES)

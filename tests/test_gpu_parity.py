@@ -683,6 +683,7 @@ def test_match_set_block_summaries(summary):
         got = _native.read_counter("blocks_read")
     finally:
         _native.set_tuning("count_blocks", 0)
+    assert _native.ruleset_info(c.handle, "summaries") == summary
     if summary:
         assert len(pk["proto"]) <= got < len(pk["proto"]) * 49 // 4   # most decoy blocks skipped
     else:
@@ -811,6 +812,8 @@ def test_compressed_rows_when_plain_exceeds_budget():
     c = compiled(golden_rules("r100000_s1"))
     got = _native.lib().pfw_ruleset_matchset_bytes(c.handle)
     assert 0 < got < plain // 10
+    assert _native.ruleset_info(c.handle, "compressed") == 1 and _native.ruleset_info(big.handle, "compressed") == 0
+    assert _native.ruleset_info(c.handle, "matchset_bytes") == got
     g = golden("scan_r100000_s1_t20000.npz")
     p = pfw.generate_traffic_device(pfw.TrafficProfile(count=20_000, seed=2), device=0)
     _native.set_tuning("algo", 2)
