@@ -788,6 +788,7 @@ def test_compressed_rows_forced():
     test_unnormalised_and_inverted_rules_never_match()
     test_fused_min_combine_virtual_ranks(1)
     test_rule_shard_windows_and_verdicts()
+    test_rule_shards_function_parallel(2)  # (its algo argument 2 = match sets)
     test_match_set_interval_edges()       # (iterates the shapes: compressed rows ignore them)
     for rn in ("r10000_s1", "r100000_s1"):
         c = compiled(golden_rules(rn))
