@@ -483,6 +483,23 @@ def main() -> int:
             "hbm": hbm,
         }
 
+    # --- BASELINE.json north_star figure: Mpps as a fraction of the slower of
+    # two rooflines -- HBM for the packet bytes, INT32 for the reference's rule
+    # comparisons (K ops each).  The rule-by-rule scan is that formulation; the
+    # match-set scan resolves comparisons without evaluating them one by one,
+    # so it can exceed it (frac > 1).
+    int_peak_ops = sms * INT32_LANES_PER_SM_CLK * clk * 1e6
+    comps_pp = local_comps / max(n, 1)
+    int32_pps = int_peak_ops / (K_OPS * max(comps_pp, 1e-9))
+    hbm_pps = float(peaks.get("hbm_gbs", 6536.4)) * 1e9 / (PKT_BYTES + OUT_BYTES)
+    per_gpu_pps = n / avg_launch_s
+    ns_roof = {"definition": "per-GPU Mpps / min(HBM roofline: packet bytes, INT32 roofline: "
+                             f"{K_OPS} int ops per reference comparison)",
+               "bound": "int32" if int32_pps < hbm_pps else "hbm",
+               "roofline_mpps": round(min(int32_pps, hbm_pps) / 1e6, 1),
+               "int32_roofline_mpps": round(int32_pps / 1e6, 1), "hbm_roofline_mpps": round(hbm_pps / 1e6, 1),
+               "frac": round(per_gpu_pps / min(int32_pps, hbm_pps), 4)}
+
     # --- end to end through the C-ABI with host buffers (pfw_classify_host)
     e2e = None
     if not args.no_e2e and w.model != "function":
@@ -555,6 +572,7 @@ def main() -> int:
                        "rule_layout": "protocol-split chains" if args.proto_split else "single ordered table",
                        "kernel": _native.version()},
             "roofline": roof,
+            "roofline_north_star": ns_roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks.summary(),
