@@ -6,14 +6,18 @@ Public surface mirrors /root/reference/pkg/src/parafw/classifier.py:
 the data lives and who scans it:
 
 * ``CompiledRuleset`` keeps the reference's ten SoA columns on the host
-  (classifier.py:120-134) and uploads the range-test form to the GPU once
-  (``pfw_ruleset_create``).
+  (classifier.py:120-134) and builds the device forms once
+  (``pfw_ruleset_create``): the per-field match sets (interval bitmaps, plain
+  or compressed rows) and the range-test table of the rule-by-rule scan.
+  ``CompiledRuleset.shard`` uploads one rule partition on its own
+  (function-parallel across GPUs: local windows, global indices).
 * ``PacketArrays`` is a device-resident batch of 16-byte packet records
   {src_ip, dst_ip, sport<<16|dport, proto} (the packet-batch layout that
   replaces the five numpy columns of classifier.py:62-95).
 * ``CompiledRuleset.scan_range`` (classifier.py:146-162) is one launch of the
-  packet x rule grid kernel; comparison counts and stats are produced in the
-  kernel epilogue (classifier.py:200-208).
+  match-set scan (or, with tuning ``algo=1``, the multi-pass packet x rule
+  grid); comparison counts and stats are produced in the kernel epilogue
+  (classifier.py:200-208), bit-exact either way.
 
 There is no CPU fallback: without libpfw.so or a CUDA device every scan
 raises ``NativeUnavailable``.

@@ -2,7 +2,7 @@
 
 Public surface mirrors /root/reference/pkg/src/parafw/engines.py:40-57.
 The reference runs every model as tasks on a CPU pool; here every model is
-a sequence of launches of the packet x rule grid kernel on one GPU, and the
+a sequence of scan launches (match-set or rule-by-rule scan) on one GPU, and the
 multi-GPU layer (``parallel``) maps the models onto GPUs:
 
 * data-parallel (engines.py:302-314): one scan of [0, R) over all packets.
