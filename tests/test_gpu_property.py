@@ -6,6 +6,8 @@ protocol numbers -- scanned over random windows under every layout option,
 bit-exact against the oracle (classifier.py:146-162, model.py:222-230)."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -28,6 +30,7 @@ IP = st.one_of(st.sampled_from([0, 1, 0x7FFFFFFF, 0x80000000, 0xC0000000, 0xFFFF
 PLEN = st.one_of(st.sampled_from([0, 1, 8, 16, 24, 31, 32]), st.integers(0, 32))
 PROTO_RULE = st.sampled_from([0, 0, 1, 6, 17, 47, 255])
 PROTO_PKT = st.sampled_from([1, 6, 17, 47, 255, 0])
+EXAMPLES = int(os.environ.get("PFW_HYP_EXAMPLES", "90"))
 
 
 @st.composite
@@ -73,12 +76,12 @@ def rules_and_packets(draw):
 def _reset():
     yield
     for k, v in (("proto_split", 0), ("first_pass", 1024), ("ks", 8), ("algo", 0), ("ms_group", 0), ("ms_words", 4),
-                 ("ms_summary", 2)):
+                 ("ms_summary", 2), ("ms_compress", 2)):
         _native.set_tuning(k, v)
 
 
-@settings(max_examples=90, deadline=None, suppress_health_check=list(HealthCheck))
-@given(case=rules_and_packets(), mode=st.sampled_from(["matchset", "rule", "split"]),
+@settings(max_examples=EXAMPLES, deadline=None, suppress_health_check=list(HealthCheck))
+@given(case=rules_and_packets(), mode=st.sampled_from(["matchset", "compressed", "rule", "split"]),
        fp=st.sampled_from([32, 64, 1024]),
        shape=st.sampled_from([(8, 4), (8, 2), (16, 4), (16, 2), (32, 2), (32, 1)]),
        summary=st.sampled_from([0, 1]))
@@ -86,7 +89,8 @@ def test_random_boundary_cases_bit_exact(case, mode, fp, shape, summary):
     """Match-set scan, rule-by-rule scan and protocol-split chains on the same
     boundary-heavy random cases."""
     cols, pk, lo, hi = case
-    _native.set_tuning("algo", {"matchset": 2, "rule": 1, "split": 1}[mode])
+    _native.set_tuning("algo", {"matchset": 2, "compressed": 2, "rule": 1, "split": 1}[mode])
+    _native.set_tuning("ms_compress", 1 if mode == "compressed" else 2)
     _native.set_tuning("proto_split", int(mode == "split"))
     _native.set_tuning("first_pass", fp)
     _native.set_tuning("ms_summary", summary)
@@ -97,3 +101,34 @@ def test_random_boundary_cases_bit_exact(case, mode, fp, shape, summary):
     np.testing.assert_array_equal(c.scan_range(p, lo, hi), oracle.scan_range(cols, pk, lo, hi))
     np.testing.assert_array_equal(c.scan_range(p, 0, len(cols["proto"])),
                                   oracle.scan_range(cols, pk, 0, len(cols["proto"])))
+
+
+@settings(max_examples=max(EXAMPLES // 3, 10), deadline=None, suppress_health_check=list(HealthCheck))
+@given(seed=st.integers(0, 2**31 - 1), R=st.integers(1025, 6000), wp=st.floats(0.05, 0.6),
+       cluster=st.floats(0.0, 0.95), mode=st.sampled_from(["plain", "compressed"]),
+       summary=st.sampled_from([0, 1]), lo_f=st.floats(0.0, 1.0), len_f=st.floats(0.0, 1.0))
+def test_multi_block_rulesets_bit_exact(seed, R, wp, cluster, mode, summary, lo_f, len_f):
+    """Rulesets spanning several 1024-rule blocks (summaries, compressed rows,
+    windows across blocks): a fraction of the rules is clustered into one dst
+    half so block summaries can skip blocks; packets partly aimed at rule
+    boundaries."""
+    rng = np.random.default_rng(seed)
+    cols = oracle.gen_ruleset(R, seed % 100_000 + 1, wp=wp)
+    k = rng.random(R) < cluster
+    cols["dst_mask"][k] = np.maximum(cols["dst_mask"][k], np.uint32(0x80000000))
+    cols["dst_base"][k] = (cols["dst_base"][k] | np.uint32(0x80000000)) & cols["dst_mask"][k]
+    pk = oracle.gen_traffic_uniform(3000, seed % 100_000 + 7)
+    pk["dst_ip"][:2000] &= np.uint32(0x7FFFFFFF)          # mostly outside the clustered half
+    r = rng.integers(0, R, 600)
+    pk["src_ip"][2000:2600] = cols["src_base"][r]
+    pk["dst_port"][2000:2600] = cols["dport_hi"][r]
+    pk["src_port"][2600:] = cols["sport_lo"][rng.integers(0, R, 400)]
+    lo = int(lo_f * R)
+    hi = min(R, lo + int(len_f * R) + 1)
+    _native.set_tuning("ms_compress", 1 if mode == "compressed" else 0)
+    _native.set_tuning("ms_summary", summary)
+    _native.set_tuning("algo", 2)
+    c = pfw.CompiledRuleset.from_columns(cols, device=0)
+    p = pfw.PacketArrays.from_columns(*[pk[f] for f in PKT_FIELDS], device=0)
+    np.testing.assert_array_equal(c.scan_range(p, lo, hi), oracle.scan_range(cols, pk, lo, hi))
+    np.testing.assert_array_equal(c.scan_range(p, 0, R), oracle.scan_range(cols, pk, 0, R))
