@@ -216,7 +216,9 @@ int pfw_parse_traffic(const char *buf, int64_t len, int64_t cap, int64_t *ids, v
 int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t *verdict, int64_t n,
                        char *out, int64_t cap, int64_t *written);
 
-/* Launch-count / tuning introspection (bench + tests).  Tuning keys include
+/* Launch-count / tuning introspection (bench + tests).  Tuning values are
+ * process-wide and not synchronised: set them before issuing scans from
+ * several host threads.  Results never depend on them.  Tuning keys include
  * "algo" (0 auto: match sets when built, 1 rule-by-rule scan, 2 match sets),
  * "matchset" (build match sets at ruleset creation, default 1),
  * "matchset_budget_mb" (0 = a quarter of free device memory), "ms_compress"
