@@ -29,6 +29,9 @@ constexpr int MS_BLOCK = 256;
 #ifndef PFW_MS_MINB
 #define PFW_MS_MINB 5  // resident blocks per SM the scan is register-limited to
 #endif
+#ifndef PFW_MS_PARK
+#define PFW_MS_PARK 6  // compressed rows: blocks of line numbers parked per packet and dimension (1..8)
+#endif
 #ifndef PFW_MS_LPB
 #define PFW_MS_LPB 1   // packets per lane per batch (batch = 32 * LPB packets per warp)
 #endif
@@ -40,7 +43,11 @@ int64_t g_ms_budget_mb = 0;    // device-memory budget for the tables (0 = a qua
 int g_ms_group = 0;            // lanes per packet (8, 16, 32; 0 = by ruleset size): 32 / group packets in flight per warp
 int g_ms_words = 4;            // words per lane per step: 32 * group * words rules per step
 int g_ms_summary = 2;          // block summaries: 0 off, 1 on, 2 auto (built and used when they skip enough)
-int g_ms_compress = 2;         // compressed rows: 0 off, 1 on, 2 auto (when the plain rows exceed the budget)
+int g_ms_compress = 2;         // compressed rows: 0 off, 1 on, 2 auto (see ms_create)
+// auto: compressed rows above this many rules.  The plain rows' leading lines
+// outgrow L2 there; the compressed rows stay L2-resident and scan at ~8 Gpps
+// flat from 20K to 100K rules (plain: 9.2 Gpps at 20K, 6.4 at 30K, 5.2 at 100K)
+constexpr int64_t MS_CMP_MIN_RULES = 24576;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
@@ -346,9 +353,9 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
     constexpr uint32_t STEP = (uint32_t)G * V;     // words per step
     constexpr uint32_t GMASK = G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u);
     constexpr int LPB = PFW_MS_LPB, BATCH = 32 * LPB;  // packets per warp batch
-    __shared__ uint4 s_off[MS_BLOCK / 32][BATCH];     // per warp: row offsets of the batch's packets
+    __shared__ uint4 s_off[CMP ? 1 : MS_BLOCK / 32][CMP ? 1 : BATCH];  // per warp: row offsets (plain rows)
     __shared__ uint4 s_row[(SUM || CMP) ? MS_BLOCK / 32 : 1][BATCH];  // per warp: row indices (SUM / CMP)
-    __shared__ uint4 s_ptr[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][8];  // CMP: line numbers, 8 blocks x 4 dims (u32)
+    __shared__ uint32_t s_lnum[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][4 * PFW_MS_PARK];  // CMP: line numbers, 8 blocks x 4 dims (u32)
     __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match of the batch's packets
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
@@ -404,8 +411,10 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     __ldg(t.port[1] + (v[k].z & 0xFFFFu)));
                 PFW_CHECK(r.x < t.nrows[0] && r.y < t.nrows[1] && r.z < t.nrows[2] && r.w < t.nrows[3]);
                 // word offsets from the common base, at the first step
-                s_off[warp][k * 32 + lane] = make_uint4(r.x * wp + cbeg + t.off[0], r.y * wp + cbeg + t.off[1],
-                                                        r.z * wp + cbeg + t.off[2], r.w * wp + cbeg + t.off[3]);
+                if (!CMP)
+                    s_off[CMP ? 0 : warp][CMP ? 0 : k * 32 + lane] =
+                        make_uint4(r.x * wp + cbeg + t.off[0], r.y * wp + cbeg + t.off[1], r.z * wp + cbeg + t.off[2],
+                                   r.w * wp + cbeg + t.off[3]);
                 if (SUM || CMP) s_row[(SUM || CMP) ? warp : 0][k * 32 + lane] = r;
                 if constexpr (CMP) {
                     // absolute line numbers (loff + index) of the 8 blocks from
@@ -416,12 +425,11 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         const uint4 q = __ldg(reinterpret_cast<const uint4 *>(u.ptr + u.ptr_off[d] +
                                                                               (size_t)rr[d] * u.pstride + cab));
                         const uint32_t *lo = u.loff + d * u.nblk + cab;  // (loff has 8 entries of slack)
-                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d] =
-                            make_uint4(__ldg(lo + 0) + (q.x & 0xFFFFu), __ldg(lo + 1) + (q.x >> 16),
-                                       __ldg(lo + 2) + (q.y & 0xFFFFu), __ldg(lo + 3) + (q.y >> 16));
-                        s_ptr[CMP ? warp : 0][CMP ? k * 32 + lane : 0][2 * d + 1] =
-                            make_uint4(__ldg(lo + 4) + (q.z & 0xFFFFu), __ldg(lo + 5) + (q.z >> 16),
-                                       __ldg(lo + 6) + (q.w & 0xFFFFu), __ldg(lo + 7) + (q.w >> 16));
+                        const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+                        uint32_t *dst = &s_lnum[CMP ? warp : 0][CMP ? k * 32 + lane : 0][PFW_MS_PARK * d];
+#pragma unroll
+                        for (int jj = 0; jj < PFW_MS_PARK; jj++)
+                            dst[jj] = __ldg(lo + jj) + ((qq[jj >> 1] >> (16 * (jj & 1))) & 0xFFFFu);
                     }
                 }
             }
@@ -442,7 +450,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
             unsigned nrd = 0;    // SUM: block reads of this lane's group (counted on lane gl == 0)
             const uint32_t blk0 = cbeg / 32u, blast = whi / 32u;  // SUM: first / last block
             if (pj >= 0) {
-                const uint4 o = s_off[warp][pj];
+                const uint4 o = s_off[CMP ? 0 : warp][CMP ? 0 : pj];
                 o0 = o.x + lv;
                 o1 = o.y + lv;
                 o2 = o.z + lv;
@@ -479,12 +487,12 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         const uint32_t b = cbeg / 32u + (uint32_t)s;  // this step's block
                         const int j = (int)(b - cab);
                         uint32_t q0, q1, q2, q3;  // absolute line numbers
-                        if (j < 8) {
-                            const uint32_t *sp = reinterpret_cast<const uint32_t *>(&s_ptr[CMP ? warp : 0][CMP ? pj : 0][0]);
+                        if (j < PFW_MS_PARK) {
+                            const uint32_t *sp = &s_lnum[CMP ? warp : 0][CMP ? pj : 0][0];
                             q0 = sp[j];
-                            q1 = sp[8 + j];
-                            q2 = sp[16 + j];
-                            q3 = sp[24 + j];
+                            q1 = sp[PFW_MS_PARK + j];
+                            q2 = sp[2 * PFW_MS_PARK + j];
+                            q3 = sp[3 * PFW_MS_PARK + j];
                         } else {
                             const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
                             q0 = __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     pj = np < nv ? np : -1;
                     s = 0;
                     if (pj >= 0) {
-                        const uint4 o = s_off[warp][pj];
+                        const uint4 o = s_off[CMP ? 0 : warp][CMP ? 0 : pj];
                         o0 = o.x + lv;
                         o1 = o.y + lv;
                         o2 = o.z + lv;
@@ -860,9 +868,10 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     uint64_t all_words = 0;  // word offsets from the common base are 32-bit in the scan
     for (int d = 0; d < 4; d++) all_words += (uint64_t)m->rows[d] * (uint64_t)m->wp + 4 * 32;
     fits = fits && all_words < (1ull << 32);
-    // compressed rows: forced, or (auto) when the plain rows do not fit --
-    // they are ~20x smaller but scan slower while the plain rows fit
-    const bool use_cmp = g_ms_compress == 1 || (g_ms_compress == 2 && !fits);
+    // compressed rows: forced, or (auto) for large rulesets or when the plain
+    // rows do not fit -- ~20x smaller; slower than plain rows only while
+    // those stay L2-friendly (<= ~24K rules)
+    const bool use_cmp = g_ms_compress == 1 || (g_ms_compress == 2 && (!fits || n > MS_CMP_MIN_RULES));
     if (!fits && !use_cmp) {
         delete m;
         return PFW_OK;  // too large for the budget: rule-by-rule scan

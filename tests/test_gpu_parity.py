@@ -806,19 +806,26 @@ def test_compressed_rows_forced():
 
 def test_compressed_rows_when_plain_exceeds_budget():
     """Auto: plain rows over the memory budget -> compressed rows (not the rule
-    scan); the reported size is the compressed one."""
-    big = compiled(golden_rules("r100000_s1"))
+    scan), also where auto would keep plain rows by size; the reported size is
+    the compressed one."""
+    _native.set_tuning("ms_compress", 0)
+    big = compiled(golden_rules("r10000_s1"))              # plain rows: ~162 MB
     plain = _native.lib().pfw_ruleset_matchset_bytes(big.handle)
-    _native.set_tuning("matchset_budget_mb", 1024)       # plain 100K rows need ~7 GB
-    c = compiled(golden_rules("r100000_s1"))
+    _native.set_tuning("ms_compress", 2)
+    _native.set_tuning("matchset_budget_mb", 64)           # too small for the plain rows
+    c = compiled(golden_rules("r10000_s1"))
     got = _native.lib().pfw_ruleset_matchset_bytes(c.handle)
-    assert 0 < got < plain // 10
+    assert 0 < got < plain // 4                            # (10K rules: ~7x; 100K: ~24x)
     assert _native.ruleset_info(c.handle, "compressed") == 1 and _native.ruleset_info(big.handle, "compressed") == 0
     assert _native.ruleset_info(c.handle, "matchset_bytes") == got
-    g = golden("scan_r100000_s1_t20000.npz")
+    g = golden("scan_r10000_s1_t20000.npz")
     p = pfw.generate_traffic_device(pfw.TrafficProfile(count=20_000, seed=2), device=0)
     _native.set_tuning("algo", 2)
     np.testing.assert_array_equal(c.scan_range(p, 0, c.num_rules), g["first"])
     _native.set_tuning("ms_compress", 0)                 # compression off: over budget -> rule scan
-    c2 = compiled(golden_rules("r100000_s1"))
+    c2 = compiled(golden_rules("r10000_s1"))
     assert _native.lib().pfw_ruleset_matchset_bytes(c2.handle) == 0
+    # auto by size: 100K rules build compressed rows
+    _native.set_tuning("ms_compress", 2)
+    _native.set_tuning("matchset_budget_mb", 0)
+    assert _native.ruleset_info(compiled(golden_rules("r100000_s1")).handle, "compressed") == 1

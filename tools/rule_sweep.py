@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rules", default="1000,4096,10000,50000,100000,250000,500000,1000000")
     ap.add_argument("--rule-scan-max", type=int, default=1000000)
+    ap.add_argument("--compare-rows", action="store_true",
+                    help="also time the match-set scan with plain rows and with compressed rows forced")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -47,7 +49,15 @@ def main():
         row = {"rules": R, "packets": n, "create_s": round(create_s, 3),
                "matchset_mib": round(_native.lib().pfw_ruleset_matchset_bytes(c.handle) / 2**20, 1)}
         want = oracle.scan_range(rules, sub, 0, R)
-        for algo, key in ((0, "matchset"), (1, "rule_scan")):
+        variants = [(c, 0, "matchset"), (c, 1, "rule_scan")]
+        if args.compare_rows:
+            for cmpv, key in ((0, "plain"), (1, "compressed")):
+                _native.set_tuning("ms_compress", cmpv)
+                cv = pfw.CompiledRuleset.from_columns(rules, device=0)
+                if _native.lib().pfw_ruleset_matchset_bytes(cv.handle) > 0:
+                    variants.append((cv, 0, f"matchset_{key}"))
+            _native.set_tuning("ms_compress", 2)
+        for cc, algo, key in variants:
             if algo == 1 and R > args.rule_scan_max:
                 continue
             _native.set_tuning("algo", algo)
@@ -57,7 +67,7 @@ def main():
                 flush.fill_(1)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                c.scan_range_device(p, 0, R, first=first, stats=stats)
+                cc.scan_range_device(p, 0, R, first=first, stats=stats)
                 e1.record()
                 e1.synchronize()
                 t = e0.elapsed_time(e1)
@@ -69,7 +79,7 @@ def main():
             row["comparisons_per_packet"] = round(int(stats[0].item()) / n, 1)
         _native.set_tuning("algo", 0)
         print(json.dumps(row), flush=True)
-        del c
+        del c, variants
 
 
 if __name__ == "__main__":
