@@ -254,6 +254,8 @@ struct MsCmp {
     uint64_t ptr_off[4];
     const uint32_t *lines;    // distinct lines, 32 words each
     const uint32_t *loff;     // [4 * nblk]: first line of (dimension, block)
+    const uint16_t *head;     // rows x 8: the first 8 blocks' line indices, dense
+    uint64_t head_off[4];
 };
 template <bool SUM, bool CMP>
 struct MsArg {
@@ -422,8 +424,10 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
                     for (int d = 0; d < 4; d++) {
-                        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(u.ptr + u.ptr_off[d] +
-                                                                              (size_t)rr[d] * u.pstride + cab));
+                        // (whole-table scans start at block 0: the dense head array)
+                        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(
+                            cab == 0 ? u.head + u.head_off[d] + (size_t)rr[d] * 8
+                                     : u.ptr + u.ptr_off[d] + (size_t)rr[d] * u.pstride + cab));
                         const uint32_t *lo = u.loff + d * u.nblk + cab;  // (loff has 8 entries of slack)
                         const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
                         uint32_t *dst = &s_lnum[CMP ? warp : 0][CMP ? k * 32 + lane : 0][PFW_MS_PARK * d];
@@ -620,6 +624,7 @@ void ms_free(MatchSet *m) {
     if (m->d_lines) cudaFree(m->d_lines);
     if (m->d_loff) cudaFree(m->d_loff);
     if (m->d_ptr_all) cudaFree(m->d_ptr_all);
+    if (m->d_head_all) cudaFree(m->d_head_all);
     for (auto *b : m->d_sum)
         if (b) cudaFree(b);
     for (auto *b : m->d_ipb)
@@ -784,7 +789,7 @@ cudaError_t ms_compress_build(pfw_ruleset *h, MatchSet *m, int64_t n, const uint
     loff[(size_t)(4 * nblk)] = (uint32_t)desc.size();
     const int64_t pstride = ((nblk + 16 + 7) / 8) * 8;
     size_t need = desc.size() * 128;
-    for (int d = 0; d < 4; d++) need += (size_t)m->rows[d] * (size_t)pstride * 2;
+    for (int d = 0; d < 4; d++) need += (size_t)m->rows[d] * ((size_t)pstride + 8) * 2;
     if (need > budget) return cudaSuccess;  // over budget even compressed
     m->nblk = nblk;
     m->pstride = pstride;
@@ -805,6 +810,12 @@ cudaError_t ms_compress_build(pfw_ruleset *h, MatchSet *m, int64_t n, const uint
     }
     if (e == cudaSuccess) e = cudaMalloc(&m->d_ptr_all, (pent + 16) * 2);
     if (e == cudaSuccess) e = cudaMemset(m->d_ptr_all, 0, (pent + 16) * 2);
+    size_t hent = 0;
+    for (int d = 0; d < 4; d++) {
+        m->head_off[d] = hent;
+        hent += (size_t)m->rows[d] * 8;
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_head_all, (hent + 8) * 2);
     if (e == cudaSuccess) {
         ms_line_kernel<<<(unsigned)(h->sms * 8), MS_BLOCK>>>(d_desc, m->nlines, n, d_sb, d_sm, d_db, d_dm, d_slo,
                                                              d_shi, d_dlo, d_dhi, d_pr, d_clsp, m->d_lines);
@@ -815,7 +826,11 @@ cudaError_t ms_compress_build(pfw_ruleset *h, MatchSet *m, int64_t n, const uint
                                                            m->pstride);
             g_launches++;
         }
-        e = cudaGetLastError();
+        // the head array: each row's first 8 indices, dense (one strided copy per dimension)
+        for (int d = 0; d < 4 && e == cudaSuccess; d++)
+            e = cudaMemcpy2D(m->d_head_all + m->head_off[d], 16, m->d_ptr_all + m->ptr_off[d],
+                             (size_t)m->pstride * 2, 16, (size_t)m->rows[d], cudaMemcpyDeviceToDevice);
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
     }
     for (void *q : {(void *)d_bnd, (void *)d_boff, (void *)d_desc})
@@ -996,11 +1011,12 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
                 for (auto *&q : m->d_bits) q = nullptr;
             } else {  // optional: keep the plain rows
                 cudaGetLastError();
-                for (void *q : {(void *)m->d_lines, (void *)m->d_loff, (void *)m->d_ptr_all})
+                for (void *q : {(void *)m->d_lines, (void *)m->d_loff, (void *)m->d_ptr_all, (void *)m->d_head_all})
                     if (q) cudaFree(q);
                 m->d_lines = nullptr;
                 m->d_loff = nullptr;
                 m->d_ptr_all = nullptr;
+                m->d_head_all = nullptr;
                 m->cmp = false;
             }
         }
@@ -1026,7 +1042,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
         for (int d = 0; d < 4; d++) plain += (size_t)m->rows[d] * (size_t)m->wp * 4;
         m->bytes -= plain;
         m->bytes += ((size_t)m->nlines * 32 + 4 * 32) * 4 + (size_t)(4 * m->nblk + 1) * 4;
-        for (int d = 0; d < 4; d++) m->bytes += (size_t)m->rows[d] * (size_t)m->pstride * 2;
+        for (int d = 0; d < 4; d++) m->bytes += (size_t)m->rows[d] * ((size_t)m->pstride + 8) * 2;
     }
     h->ms = m;
     return PFW_OK;
@@ -1064,6 +1080,8 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     for (int d = 0; d < 4; d++) uc.ptr_off[d] = m->ptr_off[d];
     uc.lines = m->d_lines;
     uc.loff = m->d_loff;
+    uc.head = m->d_head_all;
+    for (int d = 0; d < 4; d++) uc.head_off[d] = m->head_off[d];
     void (*kern)(ScanParams, MsView, MsNoSum) = nullptr;
     void (*kern_s)(ScanParams, MsView, MsSum) = nullptr;
     void (*kern_c)(ScanParams, MsView, MsCmp) = nullptr;

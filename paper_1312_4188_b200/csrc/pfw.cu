@@ -168,6 +168,8 @@ struct MatchSet {
     uint32_t *d_lines = nullptr;    // distinct lines, 32 words each
     uint32_t *d_loff = nullptr;     // [4 * nblk]: first line of (d, block)
     int64_t nlines = 0;
+    uint16_t *d_head_all = nullptr; // rows x 8: the first 8 blocks' line indices, dense (L2-resident)
+    uint64_t head_off[4] = {};
 };
 
 struct pfw_ruleset {
