@@ -357,7 +357,12 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
     constexpr int LPB = PFW_MS_LPB, BATCH = 32 * LPB;  // packets per warp batch
     __shared__ uint4 s_off[CMP ? 1 : MS_BLOCK / 32][CMP ? 1 : BATCH];  // per warp: row offsets (plain rows)
     __shared__ uint4 s_row[(SUM || CMP) ? MS_BLOCK / 32 : 1][BATCH];  // per warp: row indices (SUM / CMP)
-    __shared__ uint32_t s_lnum[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][4 * PFW_MS_PARK];  // CMP: line numbers, 8 blocks x 4 dims (u32)
+    __shared__ uint32_t s_lnum[CMP ? MS_BLOCK / 32 : 1][CMP ? BATCH : 1][4 * PFW_MS_PARK];
+    // SUM && CMP: each packet's first PFW_MS_PARK candidate blocks (AND-summary
+    // bits) -- their block numbers here, their line numbers in s_lnum -- and
+    // the count (bit 7: more candidates follow the parked ones)
+    __shared__ uint16_t s_cb[(SUM && CMP) ? MS_BLOCK / 32 : 1][(SUM && CMP) ? BATCH : 1][PFW_MS_PARK];
+    __shared__ uint8_t s_nc[(SUM && CMP) ? MS_BLOCK / 32 : 1][(SUM && CMP) ? BATCH : 1];  // CMP: line numbers, 8 blocks x 4 dims (u32)
     __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match of the batch's packets
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
@@ -418,7 +423,41 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         make_uint4(r.x * wp + cbeg + t.off[0], r.y * wp + cbeg + t.off[1], r.z * wp + cbeg + t.off[2],
                                    r.w * wp + cbeg + t.off[3]);
                 if (SUM || CMP) s_row[(SUM || CMP) ? warp : 0][k * 32 + lane] = r;
-                if constexpr (CMP) {
+                if constexpr (SUM && CMP) {
+                    // lane-parallel (one packet per lane): the packet's candidate
+                    // blocks in [blk0, blast] -- set bits of the AND of its four
+                    // summary rows -- and the line numbers of the first
+                    // PFW_MS_PARK of them, so the group loop just walks the list
+                    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+                    const uint32_t kb0 = cbeg / 32u, kb1 = whi / 32u;
+                    uint32_t *dst = &s_lnum[CMP ? warp : 0][CMP ? k * 32 + lane : 0][0];
+                    uint16_t *cbl = &s_cb[(SUM && CMP) ? warp : 0][(SUM && CMP) ? k * 32 + lane : 0][0];
+                    int nc = 0, more = 0;
+                    for (uint32_t w = kb0 / 32u; w <= kb1 / 32u && !more; w++) {
+                        uint32_t a = __ldg(u.sum[0] + (size_t)r.x * u.sw + w) & __ldg(u.sum[1] + (size_t)r.y * u.sw + w) &
+                                     __ldg(u.sum[2] + (size_t)r.z * u.sw + w) & __ldg(u.sum[3] + (size_t)r.w * u.sw + w);
+                        const int rel0 = (int)kb0 - 32 * (int)w, rel1 = (int)kb1 - 32 * (int)w;
+                        a &= rel0 <= 0 ? 0xFFFFFFFFu : (rel0 >= 32 ? 0u : (0xFFFFFFFFu << rel0));
+                        a &= rel1 < 0 ? 0u : (rel1 >= 31 ? 0xFFFFFFFFu : ((2u << rel1) - 1u));
+                        while (a) {
+                            if (nc == PFW_MS_PARK) {
+                                more = 1;
+                                break;
+                            }
+                            const uint32_t b = 32u * w + (uint32_t)(__ffs(a) - 1);
+                            a &= a - 1u;
+                            cbl[nc] = (uint16_t)b;
+#pragma unroll
+                            for (int d = 0; d < 4; d++) {
+                                const uint16_t ix = b < 8u ? __ldg(u.head + u.head_off[d] + (size_t)rr[d] * 8 + b)
+                                                           : __ldg(u.ptr + u.ptr_off[d] + (size_t)rr[d] * u.pstride + b);
+                                dst[PFW_MS_PARK * d + nc] = __ldg(u.loff + d * u.nblk + b) + ix;
+                            }
+                            nc++;
+                        }
+                    }
+                    s_nc[(SUM && CMP) ? warp : 0][(SUM && CMP) ? k * 32 + lane : 0] = (uint8_t)(nc | (more << 7));
+                } else if constexpr (CMP) {
                     // absolute line numbers (loff + index) of the 8 blocks from
                     // the 8-aligned block at or below the first, per dimension
                     const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
@@ -452,6 +491,9 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
             uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0;
             uint32_t scand = 0;  // SUM: candidate blocks after the current one (this lane's 32)
             unsigned nrd = 0;    // SUM: block reads of this lane's group (counted on lane gl == 0)
+            int ck = 0;          // SUM && CMP: index into the packet's parked candidate list
+            bool fb = false;     // SUM && CMP: past the parked candidates (in-loop summary search)
+            bool fbload = false; // SUM && CMP: load the summaries this iteration (switching to fb)
             const uint32_t blk0 = cbeg / 32u, blast = whi / 32u;  // SUM: first / last block
             if (pj >= 0) {
                 const uint4 o = s_off[CMP ? 0 : warp][CMP ? 0 : pj];
@@ -465,7 +507,22 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 uint32_t x[V], any = 0u;
 #pragma unroll
                 for (int v = 0; v < V; v++) x[v] = 0u;
-                if constexpr (SUM) {
+                if constexpr (SUM && CMP) {
+                    if (act && fbload) {
+                        // past the parked candidates: the AND-summary after the last one
+                        scand = 0u;
+                        if ((uint32_t)gl < u.sw) {
+                            const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
+                            scand = __ldg(u.sum[0] + (size_t)rw.x * u.sw + gl) &
+                                    __ldg(u.sum[1] + (size_t)rw.y * u.sw + gl) &
+                                    __ldg(u.sum[2] + (size_t)rw.z * u.sw + gl) &
+                                    __ldg(u.sum[3] + (size_t)rw.w * u.sw + gl);
+                            const int rel0 = (int)(blk0 + (uint32_t)s) - 32 * gl, rel1 = (int)blast - 32 * gl;
+                            scand &= rel0 < 0 ? 0xFFFFFFFFu : (rel0 >= 31 ? 0u : (0xFFFFFFFFu << (rel0 + 1)));
+                            scand &= rel1 < 0 ? 0u : (rel1 >= 31 ? 0xFFFFFFFFu : ((2u << rel1) - 1u));
+                        }
+                    }
+                } else if constexpr (SUM) {
                     if (act && s == 0) {
                         // the packet's first step: its AND-summary, restricted
                         // to the blocks after this one, up to the window's last
@@ -483,11 +540,37 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         }
                     }
                 }
-                if (SUM && act && gl == 0) nrd++;
+                // this iteration reads lines (SUM && CMP: a parked candidate, or a
+                // fallback step; not the summary-only switching iteration)
+                const int pnc = (SUM && CMP && act) ? (int)s_nc[(SUM && CMP) ? warp : 0][(SUM && CMP) ? pj : 0] : 0;
+                const bool rd = act && (!(SUM && CMP) || (fb ? !fbload : ck < (pnc & 0x7F)));
+                if (SUM && rd && gl == 0) nrd++;
                 PFW_CHECK(!act || (pj < nv && (CMP || (uint64_t)max(max(o0, o1), max(o2, o3)) + V <= t.words)));
-                if (act) {
+                if (rd) {
                     MsStep<V> st;
-                    if constexpr (CMP) {
+                    if constexpr (SUM && CMP) {
+                        uint32_t q0, q1, q2, q3, b;
+                        if (!fb) {  // the next parked candidate
+                            b = s_cb[(SUM && CMP) ? warp : 0][(SUM && CMP) ? pj : 0][ck];
+                            const uint32_t *sp = &s_lnum[CMP ? warp : 0][CMP ? pj : 0][0];
+                            q0 = sp[ck];
+                            q1 = sp[PFW_MS_PARK + ck];
+                            q2 = sp[2 * PFW_MS_PARK + ck];
+                            q3 = sp[3 * PFW_MS_PARK + ck];
+                            s = (int)(b - blk0);
+                        } else {    // in-loop summary search: line numbers from global memory
+                            b = blk0 + (uint32_t)s;
+                            const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
+                            q0 = __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
+                            q1 = __ldg(u.loff + u.nblk + b) + __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
+                            q2 = __ldg(u.loff + 2 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
+                            q3 = __ldg(u.loff + 3 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
+                        }
+                        PFW_CHECK(b >= blk0 && b <= blast);
+                        const uint32_t *l = u.lines + lv;
+                        st.load(l + ((size_t)q0 << 5), l + ((size_t)q1 << 5), l + ((size_t)q2 << 5),
+                                l + ((size_t)q3 << 5));
+                    } else if constexpr (CMP) {
                         const uint32_t b = cbeg / 32u + (uint32_t)s;  // this step's block
                         const int j = (int)(b - cab);
                         uint32_t q0, q1, q2, q3;  // absolute line numbers
@@ -540,14 +623,25 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 }
                 bool done = act && (found || s + 1 >= nsteps);
                 int ns = s + 1;  // next step (SUM: the next candidate block)
-                if constexpr (SUM) {
+                bool sw_fb = false;  // SUM && CMP: switch to the in-loop summary search
+                if constexpr (SUM && CMP) {
+                    if (!fb) {
+                        // walking the parked list: done, next parked, or switch
+                        const int nc = pnc & 0x7F, more = pnc >> 7;
+                        done = act && (found || (ck + 1 >= nc && !more));
+                        sw_fb = act && !done && ck + 1 >= nc;  // (more candidates after the parked ones)
+                    }
+                }
+                // (SUM && CMP: only while some group of the warp is past its parked candidates)
+                if (SUM && (!CMP || __any_sync(0xFFFFFFFFu, fb))) {
                     // next candidate block of the groups still searching
-                    const uint32_t cm = (act && !found) ? scand : 0u;
+                    const bool fbs = !CMP || fb;  // groups in the in-loop summary search
+                    const uint32_t cm = (act && !found && fbs) ? scand : 0u;
                     const uint32_t cbits = (__ballot_sync(0xFFFFFFFFu, cm != 0u) >> gbase) & GMASK;
                     const int nb = __shfl_sync(0xFFFFFFFFu, 32 * gl + __ffs(cm) - 1,
                                                gbase + (__ffs(cbits) - 1) * (cbits != 0u));
-                    done = act && (found || cbits == 0u);
-                    if (!done && act) {
+                    if (fbs) done = act && (found || cbits == 0u);
+                    if (fbs && !done && act) {
                         ns = nb - (int)blk0;
                         const int rel = nb - 32 * gl;  // drop candidates up to nb
                         scand &= rel < 0 ? 0xFFFFFFFFu : (rel >= 31 ? 0u : (0xFFFFFFFFu << (rel + 1)));
@@ -559,6 +653,9 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                     const int np = next + __popc(dmask & ((1u << gbase) - 1u));
                     pj = np < nv ? np : -1;
                     s = 0;
+                    ck = 0;
+                    fb = false;
+                    fbload = false;
                     if (pj >= 0) {
                         const uint4 o = s_off[CMP ? 0 : warp][CMP ? 0 : pj];
                         o0 = o.x + lv;
@@ -567,7 +664,19 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         o3 = o.w + lv;
                     }
                 } else if (act) {
-                    if constexpr (SUM) {
+                    if constexpr (SUM && CMP) {
+                        if (!fb) {
+                            if (sw_fb) {
+                                fb = true;      // next iteration: load the summaries after block blk0 + s
+                                fbload = true;
+                            } else {
+                                ck++;
+                            }
+                        } else {
+                            fbload = false;
+                            s = ns;
+                        }
+                    } else if constexpr (SUM) {
                         const uint32_t adv = (uint32_t)(ns - s) * STEP;
                         s = ns;
                         o0 += adv;

@@ -829,3 +829,25 @@ def test_compressed_rows_when_plain_exceeds_budget():
     _native.set_tuning("ms_compress", 2)
     _native.set_tuning("matchset_budget_mb", 0)
     assert _native.ruleset_info(compiled(golden_rules("r100000_s1")).handle, "compressed") == 1
+
+
+def test_summary_candidates_past_the_parked_ones():
+    """Summary scan over compressed rows with more candidate blocks than the
+    lookup phase parks (random rules: nearly every block is a candidate), so
+    late-matching and default-deny packets continue with the in-loop summary
+    search; whole and partial windows, counters."""
+    _native.set_tuning("ms_summary", 1)
+    _native.set_tuning("ms_compress", 1)
+    rules = oracle.gen_ruleset(12_000, 91, wp=0.05)          # few wildcards: late / no matches
+    pk = oracle.gen_traffic_uniform(8000, 92)
+    c = compiled(rules)
+    assert _native.ruleset_info(c.handle, "summaries") == 1 and _native.ruleset_info(c.handle, "compressed") == 1
+    _native.set_tuning("algo", 2)
+    for lo, hi in ((0, 12_000), (1, 11_999), (700, 9000), (6 * 1024 - 3, 12_000), (11_000, 11_001)):
+        np.testing.assert_array_equal(c.scan_range(dev_pkts(pk), lo, hi), oracle.scan_range(rules, pk, lo, hi))
+    want = oracle.scan_range(rules, pk, 0, 12_000)
+    assert (want < 0).any() and (want > 7 * 1024).any()       # the fallback path is exercised
+    res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=3)).run_arrays(c, dev_pkts(pk))
+    first, comps, total, mx = oracle.engine_run(rules, pk, "function", 3)
+    np.testing.assert_array_equal(res.first, first)
+    np.testing.assert_array_equal(res.comparisons, comps)

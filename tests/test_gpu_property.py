@@ -104,7 +104,7 @@ def test_random_boundary_cases_bit_exact(case, mode, fp, shape, summary):
 
 
 @settings(max_examples=max(EXAMPLES // 3, 10), deadline=None, suppress_health_check=list(HealthCheck))
-@given(seed=st.integers(0, 2**31 - 1), R=st.integers(1025, 6000), wp=st.floats(0.05, 0.6),
+@given(seed=st.integers(0, 2**31 - 1), R=st.integers(1025, 12000), wp=st.floats(0.02, 0.6),
        cluster=st.floats(0.0, 0.95), mode=st.sampled_from(["plain", "compressed"]),
        summary=st.sampled_from([0, 1]), lo_f=st.floats(0.0, 1.0), len_f=st.floats(0.0, 1.0))
 def test_multi_block_rulesets_bit_exact(seed, R, wp, cluster, mode, summary, lo_f, len_f):
