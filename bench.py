@@ -235,7 +235,8 @@ def main() -> int:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--graph", action="store_true",
                     help="capture one step (all pass launches) in a CUDA graph and replay it")
-    ap.add_argument("--e2e-chunk", type=int, default=1 << 22, help="packets per H2D/scan/D2H chunk")
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 23,
+                    help="packets per H2D/scan/D2H chunk (ramped down at both ends of the call)")
     ap.add_argument("--algo", type=int, default=-1,
                     help="0 auto (match sets when built), 1 rule-by-rule scan, 2 match sets")
     ap.add_argument("--ms-words", type=int, default=0, help="match-set scan: words per lane per step (1, 2, 4)")
@@ -541,7 +542,8 @@ def main() -> int:
                "h2d_frac": round(n * 13 / e2e_s / 1e9 / link["h2d_gbs"], 4),
                "link_peak_source": link["source"],
                "api": f"pfw_classify_host_columns (C-ABI, the reference's PacketArrays columns in "
-                      f"pinned host memory, {args.e2e_chunk}-packet chunks, copy-in / 2x compute / "
+                      f"pinned host memory, {args.e2e_chunk}-packet chunks ramped 1/8-1/4-1/2 at both ends, "
+                      "copy-in / 2x compute / "
                       "copy-out streams, 3 slots)"}
 
     cpu = None

@@ -331,7 +331,7 @@ class CompiledRuleset:
             _ptr(stats), st), "pfw_scan_range_columns")
         return first
 
-    def classify_host_columns(self, cols: dict, chunk: int = 1 << 22):
+    def classify_host_columns(self, cols: dict, chunk: int = 1 << 23):
         """End-to-end over HOST columns (numpy; pinned memory overlaps the copies):
         returns (first int64 with -1 for default deny, verdict bool, [sum, max] comps)."""
         n = len(cols["proto"])

@@ -851,3 +851,19 @@ def test_summary_candidates_past_the_parked_ones():
     first, comps, total, mx = oracle.engine_run(rules, pk, "function", 3)
     np.testing.assert_array_equal(res.first, first)
     np.testing.assert_array_equal(res.comparisons, comps)
+
+
+@pytest.mark.parametrize("n", [917_504, 2_000_001, 3_145_731])
+def test_classify_host_ramped_chunk_schedule(n):
+    """pfw_classify_host_columns with a chunk small enough that the ramped
+    schedule (1/4, 1/2 chunks at both ends, full chunks between) engages:
+    identical to the device-resident scan, verdicts and stats included."""
+    rules = oracle.gen_ruleset(4096, 1)
+    c = compiled(rules)
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=5), device=0)
+    dev_first = first_to_host(c.scan_range_device(p, 0, 4096))
+    f, v, st = c.classify_host_columns(p.columns(), chunk=1 << 18)
+    np.testing.assert_array_equal(f, dev_first)
+    np.testing.assert_array_equal(v, np.where(dev_first >= 0, rules["action_accept"][np.maximum(dev_first, 0)], False))
+    comps = oracle.sequential_comparisons(dev_first, 4096)
+    assert st.tolist() == [int(comps.sum()), int(comps.max())]
