@@ -29,6 +29,9 @@ constexpr int MS_BLOCK = 256;
 #ifndef PFW_MS_MINB
 #define PFW_MS_MINB 5  // resident blocks per SM the scan is register-limited to
 #endif
+#ifndef PFW_MS_MINB_SC
+#define PFW_MS_MINB_SC 4  // the summary scan over compressed rows (two candidates per step)
+#endif
 #ifndef PFW_MS_PARK
 #define PFW_MS_PARK 6  // compressed rows: blocks of line numbers parked per packet and dimension (1..8)
 #endif
@@ -348,7 +351,7 @@ struct MsStep<1> {
 // in shared memory; a step reads those lines (beyond the 8 blocks the index
 // comes from global memory).
 template <int MODE, int G, int V, bool WIN, bool SUM = false, bool CMP = false>
-__global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
+__global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_MS_MINB)
     ms_scan_kernel(ScanParams p, MsView t, typename MsArg<SUM, CMP>::type u) {
     static_assert(!(SUM || CMP) || G * V == 32, "summary / compressed blocks are one step");
     constexpr int P = 32 / G;                      // packets in flight per warp
@@ -546,11 +549,16 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 const bool rd = act && (!(SUM && CMP) || (fb ? !fbload : ck < (pnc & 0x7F)));
                 if (SUM && rd && gl == 0) nrd++;
                 PFW_CHECK(!act || (pj < nv && (CMP || (uint64_t)max(max(o0, o1), max(o2, o3)) + V <= t.words)));
+                uint32_t x2[V], any2 = 0u;  // SUM && CMP list walk: the second candidate of this step
+                bool two = false;
+                int s2 = 0;
+#pragma unroll
+                for (int v = 0; v < V; v++) x2[v] = 0u;
                 if (rd) {
                     MsStep<V> st;
                     if constexpr (SUM && CMP) {
                         uint32_t q0, q1, q2, q3, b;
-                        if (!fb) {  // the next parked candidate
+                        if (!fb) {  // the next parked candidate(s): two per step when there are
                             b = s_cb[(SUM && CMP) ? warp : 0][(SUM && CMP) ? pj : 0][ck];
                             const uint32_t *sp = &s_lnum[CMP ? warp : 0][CMP ? pj : 0][0];
                             q0 = sp[ck];
@@ -558,6 +566,26 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                             q2 = sp[2 * PFW_MS_PARK + ck];
                             q3 = sp[3 * PFW_MS_PARK + ck];
                             s = (int)(b - blk0);
+                            two = ck + 1 < (pnc & 0x7F);
+                            if (two) {
+                                if (gl == 0) nrd++;  // (a second block read this step)
+                                const uint32_t b2 = s_cb[(SUM && CMP) ? warp : 0][(SUM && CMP) ? pj : 0][ck + 1];
+                                s2 = (int)(b2 - blk0);
+                                MsStep<V> st2;
+                                const uint32_t *l2 = u.lines + lv;
+                                st2.load(l2 + ((size_t)sp[ck + 1] << 5), l2 + ((size_t)sp[PFW_MS_PARK + ck + 1] << 5),
+                                         l2 + ((size_t)sp[2 * PFW_MS_PARK + ck + 1] << 5),
+                                         l2 + ((size_t)sp[3 * PFW_MS_PARK + ck + 1] << 5));
+#pragma unroll
+                                for (int v = 0; v < V; v++) {
+                                    x2[v] = st2.w[0][v] & st2.w[1][v] & st2.w[2][v] & st2.w[3][v];
+                                    if (WIN) {
+                                        if (s2 == 0) x2[v] &= mfirst[v];
+                                        if (s2 == nsteps - 1) x2[v] &= mlast[v];
+                                    }
+                                    any2 |= x2[v];
+                                }
+                            }
                         } else {    // in-loop summary search: line numbers from global memory
                             b = blk0 + (uint32_t)s;
                             const uint4 rw = s_row[(SUM || CMP) ? warp : 0][pj];
@@ -603,8 +631,22 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                         any |= x[v];
                     }
                 }
-                const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
-                const uint32_t gbits = (bal >> gbase) & GMASK;
+                unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
+                uint32_t gbits = (bal >> gbase) & GMASK;
+                if constexpr (SUM && CMP) {
+                    // a group whose first candidate of the step has no match takes
+                    // the second one's (its blocks are later: still the lowest)
+                    const unsigned bal2 = __ballot_sync(0xFFFFFFFFu, any2 != 0u && gbits == 0u);
+                    const uint32_t gbits2 = (bal2 >> gbase) & GMASK;
+                    if (gbits2) {
+                        gbits = gbits2;
+                        s = s2;
+#pragma unroll
+                        for (int v = 0; v < V; v++) x[v] = x2[v];
+                    }
+                    bal |= bal2;
+                    if (two && !gbits2 && gbits == 0u) s = s2;  // (the last block this step read)
+                }
                 const bool found = gbits != 0u;  // (idle groups have no bits)
                 if (bal) {  // warp-uniform: some group found its packet's first match
                     // this lane's lowest set bit: first non-zero word, its lowest bit
@@ -627,9 +669,9 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                 if constexpr (SUM && CMP) {
                     if (!fb) {
                         // walking the parked list: done, next parked, or switch
-                        const int nc = pnc & 0x7F, more = pnc >> 7;
-                        done = act && (found || (ck + 1 >= nc && !more));
-                        sw_fb = act && !done && ck + 1 >= nc;  // (more candidates after the parked ones)
+                        const int nc = pnc & 0x7F, more = pnc >> 7, nxt = ck + (two ? 2 : 1);
+                        done = act && (found || (nxt >= nc && !more));
+                        sw_fb = act && !done && nxt >= nc;  // (more candidates after the parked ones)
                     }
                 }
                 // (SUM && CMP: only while some group of the warp is past its parked candidates)
@@ -670,7 +712,7 @@ __global__ void __launch_bounds__(MS_BLOCK, PFW_MS_MINB)
                                 fb = true;      // next iteration: load the summaries after block blk0 + s
                                 fbload = true;
                             } else {
-                                ck++;
+                                ck += two ? 2 : 1;
                             }
                         } else {
                             fbload = false;
