@@ -60,6 +60,17 @@ def _worker(rank, world, port, q):
         c.scan_partition_accumulate(p, lo, hi, first, comps, stats)
         parallel.function_parallel_combine(first, comps, stats)
         out["allreduce"] = ((0, n), first_to_host(first), comps.cpu().numpy(), stats.cpu().numpy())
+        # per-rank rule shards (each rank uploads only its partition): fused and all-reduce
+        shard = c.shard(lo, hi)
+        fused = parallel.FusedFunctionParallel(shard, n, scatter=False)
+        f_sh, c_sh = fused.run(p)
+        out["shard_fused"] = (first_to_host(f_sh), c_sh.cpu().numpy())
+        fused.close()
+        first.fill_(2**31 - 1)
+        comps.zero_()
+        shard.scan_partition_accumulate(p, 0, shard.num_rules, first, comps, None)
+        parallel.function_parallel_combine(first, comps, None)
+        out["shard_allreduce"] = (first_to_host(first), comps.cpu().numpy())
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -98,3 +109,32 @@ def test_function_parallel_multiprocess_one_gpu(world):
         np.testing.assert_array_equal(cm, want_comps)
         total, mx, _ = g[f"function_{world}_stats"].tolist()
         assert st.tolist() == [total, mx]
+        for key in ("shard_fused", "shard_allreduce"):
+            f, cm = res[r][key]
+            np.testing.assert_array_equal(f, want_first)
+            np.testing.assert_array_equal(cm, want_comps)
+
+
+@pytest.mark.parametrize("config", ["data", "function"])
+def test_bench_two_ranks_shared_gpu(config):
+    """bench.py under torchrun with 2 ranks sharing the one GPU (PFW_SHARE_GPU=1:
+    gloo collectives, a functional check of the N>1 path): one JSON line from
+    rank 0 with the whole-job packet count and the rank layout."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, PFW_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--config", config, "--packets", str(1 << 20), "--steps", "3", "--warmup", "3",
+           "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=ROOT, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    if config == "data":
+        assert d["scaling"] == "weak" and d["config"]["packets"] == 2 << 20 and d["e2e"]["value"] > 0
+    else:
+        assert d["config"]["rules_per_gpu"] == [0, 50_000]
