@@ -1753,6 +1753,14 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     if (n == 0) return PFW_OK;
     if ((!h_pkts && !hc) || !h_first) return set_err(PFW_ERR_INVALID, "null host buffer");
     if (chunk <= 0) chunk = 1 << 23;
+    // at least ~8 chunks per call (>= 256K packets each), so that smaller
+    // batches pipeline too: a single chunk runs copy-in, scan and copy-out
+    // one after the other
+    {
+        int64_t c8 = n / 8;
+        if (c8 < (1 << 18)) c8 = 1 << 18;
+        if (chunk > c8) chunk = c8;
+    }
     if (chunk > n) chunk = n;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
