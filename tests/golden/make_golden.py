@@ -19,6 +19,14 @@ Every fixture records the reference call that produced it.  The fixtures pin
                     function-parallel / hybrid models (parafw/engines.py:260-369)
 * adversarial.npz -- the SURVEY 8(d) adversarial 50K-rule recipe, built with
                     the reference generator, and its first-match indices.
+* worst_case.json -- generate_traffic(WORST_CASE) packet lists, including
+                    rulesets that force the uncovered-port fallback
+                    (parafw/traffic.py:161-191)
+* parsers.json    -- load_ruleset / load_traffic on the edge inputs of
+                    parser_cases.py: the columns, or the exact error message
+                    (parafw/model.py:233-331, parafw/traffic.py:259-297)
+
+    python tests/golden/make_golden.py [--only worst_case,parsers]
 
 Large arrays are stored as sha256 digests plus a head slice so the fixtures
 stay small; the oracle regenerates them and compares digests.
@@ -41,11 +49,18 @@ from parafw.engines import EngineConfig, ExecutionModel, Engine  # noqa: E402
 from parafw.model import Action, CidrMatcher, PortRange, Protocol, Rule, Ruleset  # noqa: E402
 from parafw.rng import Xorshift64Star, derive_seed  # noqa: E402
 from parafw.traffic import (  # noqa: E402
+    MatchMode,
     RulesetGenParams,
+    TrafficFormatError,
     TrafficProfile,
     generate_ruleset,
     generate_traffic,
+    load_traffic,
 )
+from parafw.model import RuleParseError, load_ruleset  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import parser_cases  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 RULE_FIELDS = ("proto", "src_base", "src_mask", "sport_lo", "sport_hi",
@@ -279,15 +294,120 @@ def gen_adversarial():
          max_worker_comparisons=np.int64(st.max_worker_comparisons))
 
 
+def _complement_rules(base: int, plen: int, dport: PortRange) -> list:
+    """DROP tcp rules whose src prefixes cover every address outside base/plen."""
+    out = []
+    for k in range(1, plen + 1):
+        bit = 1 << (32 - k)
+        out.append(Rule(Action.DROP, Protocol.TCP, CidrMatcher((base ^ bit) & ~(bit - 1), k), PortRange(0, 65535),
+                        CidrMatcher(0, 0), dport))
+    return out
+
+
+# (name, ruleset builder, profile kwargs)
+WORST_CASES = [
+    # every TCP candidate matches unless dport == 80: every packet takes the fallback
+    ("dport_gap_s5", lambda: Ruleset((
+        Rule(Action.ACCEPT, Protocol.TCP, CidrMatcher(0, 0), PortRange(0, 65535), CidrMatcher(0, 0), PortRange(0, 79)),
+        Rule(Action.ACCEPT, Protocol.TCP, CidrMatcher(0, 0), PortRange(0, 65535), CidrMatcher(0, 0),
+             PortRange(81, 65535)))), dict(count=12, seed=5)),
+    # acceptance probability 2^-13: about 30% of packets exhaust 10000 attempts
+    ("src13_s3", lambda: Ruleset(tuple(_complement_rules(0x0A000000, 13, PortRange(1, 65535)))),
+     dict(count=40, seed=3)),
+    ("src13_s11_udp", lambda: Ruleset(tuple(_complement_rules(0x0A000000, 13, PortRange(1, 65535))) + (
+        Rule(Action.ACCEPT, Protocol.UDP, CidrMatcher(0, 0), PortRange(0, 65535), CidrMatcher(0, 0),
+             PortRange(0, 65535)),)), dict(count=30, seed=11)),
+    # random rulesets: rejection only
+    ("r2048_s21_w15_s4", lambda: generate_ruleset(RulesetGenParams(2048, seed=21, wildcard_probability=0.15)),
+     dict(count=300, seed=4)),
+    ("r1000_s1_s9_ports", lambda: generate_ruleset(RulesetGenParams(1000, seed=1)),
+     dict(count=200, seed=9, sport_range=PortRange(1000, 2999), dport_range=PortRange(7, 65000))),
+]
+
+
+def _profile_meta(prof):
+    return dict(count=prof.count, seed=prof.seed, proto=int(prof.proto),
+                src=[prof.src_subnet.base, prof.src_subnet.prefix_len],
+                dst=[prof.dst_subnet.base, prof.dst_subnet.prefix_len],
+                sport=[prof.sport_range.lo, prof.sport_range.hi], dport=[prof.dport_range.lo, prof.dport_range.hi])
+
+
+def gen_worst_case():
+    import json
+    from parafw.model import format_rule
+    out = {}
+    for name, build, kw in WORST_CASES:
+        rs = build()
+        prof = TrafficProfile(match_mode=MatchMode.WORST_CASE, **kw)
+        t = time.time()
+        pk = generate_traffic(prof, rs)
+        out[name] = {"rules": [format_rule(r) for r in rs], "profile": _profile_meta(prof),
+                     "packets": [[p.id, int(p.proto), p.src_ip, p.src_port, p.dst_ip, p.dst_port] for p in pk]}
+        print(f"  worst case {name}: {len(pk)} packets in {time.time() - t:.1f}s")
+    # the reference's error when no non-matching packet exists
+    rs = Ruleset((Rule(Action.DROP, Protocol.ANY, CidrMatcher(0, 0), PortRange(0, 65535), CidrMatcher(0, 0),
+                       PortRange(0, 65535)),))
+    try:
+        generate_traffic(TrafficProfile(3, seed=1, match_mode=MatchMode.WORST_CASE), rs)
+        err = None
+    except Exception as exc:  # TrafficGenerationError
+        err = str(exc)
+    out["_impossible"] = {"rules": [format_rule(r) for r in rs], "error": err}
+    path = os.path.join(OUT, "worst_case.json")
+    with open(path, "w") as fh:
+        json.dump(out, fh, indent=0)
+    print(f"wrote worst_case.json: {os.path.getsize(path)} bytes")
+
+
+def gen_parsers():
+    import json
+    import tempfile
+    res = {"rules": [], "traffic": []}
+    with tempfile.TemporaryDirectory() as d:
+        for text in parser_cases.RULE_TEXTS:
+            path = os.path.join(d, "rules.txt")
+            with open(path, "wb") as fh:
+                fh.write(text.encode())
+            try:
+                c = compile_ruleset(load_ruleset(path))
+                res["rules"].append({"columns": {f: getattr(c, f).astype(np.int64).tolist() for f in RULE_FIELDS}})
+            except RuleParseError as exc:
+                res["rules"].append({"error": str(exc).replace(path, "{path}")})
+        for body in parser_cases.TRAFFIC_BODIES:
+            path = os.path.join(d, "t.csv")
+            with open(path, "wb") as fh:
+                fh.write((parser_cases.TRAFFIC_HEADER + body).encode())
+            try:
+                pk = load_traffic(path)
+                res["traffic"].append({"packets": [[p.id, int(p.proto), p.src_ip, p.src_port, p.dst_ip, p.dst_port]
+                                                   for p in pk]})
+            except TrafficFormatError as exc:
+                res["traffic"].append({"error": str(exc).replace(path, "{path}")})
+    path = os.path.join(OUT, "parsers.json")
+    with open(path, "w") as fh:
+        json.dump(res, fh)
+    print(f"wrote parsers.json: {os.path.getsize(path)} bytes")
+
+
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="", help="comma-separated subset: rng,rules,scans,engines,adversarial,"
+                                               "worst_case,parsers")
+    only = set(filter(None, ap.parse_args().only.split(",")))
     t0 = time.time()
-    gen_rng()
-    rules, traffic = {}, {}
-    gen_rulesets(rules)
-    gen_traffic(traffic)
-    gen_scans(rules, traffic)
-    gen_engines(rules, traffic)
-    gen_adversarial()
+    if not only:
+        gen_rng()
+        rules, traffic = {}, {}
+        gen_rulesets(rules)
+        gen_traffic(traffic)
+        gen_scans(rules, traffic)
+        gen_engines(rules, traffic)
+        gen_adversarial()
+    if not only or "worst_case" in only:
+        gen_worst_case()
+    if not only or "parsers" in only:
+        gen_parsers()
     print(f"done in {time.time() - t0:.1f}s")
 
 

@@ -4,14 +4,25 @@ identical columns / records on canonical files, and on every malformed or
 non-canonical input the exact reference behaviour (via the Python path)."""
 from __future__ import annotations
 
+import json
+import os
+import sys
+
 import numpy as np
 import pytest
 
+from conftest import GOLDEN
 from paper_1312_4188_b200 import (Packet, Protocol, RuleParseError, RulesetGenParams, TrafficFormatError,
                                   generate_ruleset, load_ruleset, load_traffic, save_ruleset, save_traffic)
 from paper_1312_4188_b200.classifier import RULE_COLUMNS, PacketArrays, _rule_columns
 from paper_1312_4188_b200.fileio import format_results, load_ruleset_columns, parse_traffic
 from paper_1312_4188_b200.rng import Xorshift64Star
+
+sys.path.insert(0, GOLDEN)
+from parser_cases import RULE_TEXTS, TRAFFIC_BODIES, TRAFFIC_HEADER  # noqa: E402
+
+with open(os.path.join(GOLDEN, "parsers.json")) as _fh:
+    PARSERS = json.load(_fh)  # the reference's load_ruleset / load_traffic on each case (make_golden.py)
 
 
 def test_rules_native_equals_python(tmp_path):
@@ -24,16 +35,7 @@ def test_rules_native_equals_python(tmp_path):
         np.testing.assert_array_equal(got[f], want[f])
 
 
-@pytest.mark.parametrize("text", [
-    "# header\n\nACCEPT tcp 10.1.2.3/8 * * 80  # web\n  DROP any * * * *\r\nACCEPT udp 1.2.3.4/32 5-6 0.0.0.0/0 00080-65535\n",
-    "ACCEPT icmp * 1000 192.168.0.0/16 *",  # no trailing newline
-    "ACCEPT tcp +10.0.0.0/8 * * *\n",  # non-canonical -> python path (error)
-    "ACCEPT tcp 10.0.0.0/08 * * +80\n",  # '+80' valid for int(): python path accepts
-    "ACCEPT tcp 010.0.0.0/8 * * *\n", "ACCEPT tcp 10.0.0.0/33 * * *\n", "ACCEPT tcp * 90-80 * *\n",
-    "ACCEPT tcp * * *\n", "PERMIT tcp * * * *\n", "ACCEPT gre * * * *\n", "ACCEPT tcp * 70000 * *\n",
-    "ACCEPT tcp * 80- * *\n", "ACCEPT tcp * -5 * *\n", "ACCEPT tcp 1.2.3/8 * * *\n",
-    "ACCEPT tcp * * * 80\rDROP any * * * *\n",
-])
+@pytest.mark.parametrize("text", RULE_TEXTS)
 def test_rules_edge_cases_match_python(tmp_path, text):
     path = tmp_path / "r.txt"
     path.write_bytes(text.encode())
@@ -69,17 +71,10 @@ def test_traffic_native_equals_python(tmp_path):
     np.testing.assert_array_equal(rec, ref)
 
 
-HDR = "id,proto,src_ip,src_port,dst_ip,dst_port\n"
+HDR = TRAFFIC_HEADER
 
 
-@pytest.mark.parametrize("body", [
-    "1,tcp,1.2.3.4,5,6.7.8.9,10\r\n\n2,udp,0.0.0.0,0,255.255.255.255,65535",
-    "-3,tcp,1.2.3.4,5,6.7.8.9,10\n",  # negative id: int() accepts -> python path
-    " 4,tcp,1.2.3.4, 5,6.7.8.9,10\n",  # spaces: int() accepts -> python path
-    '"5",tcp,1.2.3.4,5,6.7.8.9,10\n',  # quoted field: csv accepts -> python path
-    "6,any,1.2.3.4,5,6.7.8.9,10\n", "7,tcp,1.2.3.4,70000,6.7.8.9,10\n", "8,tcp,1.2.3,5,6.7.8.9,10\n",
-    "9,tcp,1.2.3.4,5,6.7.8.9\n", "x,tcp,1.2.3.4,5,6.7.8.9,10\n", "10,tcp,1.2.3.4,5,6.7.8.9,10,11\n",
-])
+@pytest.mark.parametrize("body", TRAFFIC_BODIES)
 def test_traffic_edge_cases_match_python(tmp_path, body):
     path = tmp_path / "t.csv"
     path.write_bytes((HDR + body).encode())
@@ -109,3 +104,39 @@ def test_format_results():
                          np.array([1, 0, 0], np.uint8))
     assert out.decode() == "0,ACCEPT,3\n17,DROP,-\n5,DROP,0\n"
     assert format_results(np.zeros(0, np.int64), np.zeros(0, np.uint32), np.zeros(0, np.uint8)) == b""
+
+
+@pytest.mark.parametrize("k", range(len(RULE_TEXTS)))
+def test_rules_edge_cases_equal_reference(tmp_path, k):
+    """Python and native readers against the reference's own load_ruleset output."""
+    path = tmp_path / "rules.txt"
+    path.write_bytes(RULE_TEXTS[k].encode())
+    want = PARSERS["rules"][k]
+    for load in (lambda q: _rule_columns(load_ruleset(q)), load_ruleset_columns):
+        if "error" in want:
+            with pytest.raises(RuleParseError) as got:
+                load(path)
+            assert str(got.value) == want["error"].replace("{path}", str(path))
+        else:
+            got = load(path)
+            for f in RULE_COLUMNS:
+                assert np.asarray(got[f]).astype(np.int64).tolist() == want["columns"][f], f
+
+
+@pytest.mark.parametrize("k", range(len(TRAFFIC_BODIES)))
+def test_traffic_edge_cases_equal_reference(tmp_path, k):
+    path = tmp_path / "t.csv"
+    path.write_bytes((TRAFFIC_HEADER + TRAFFIC_BODIES[k]).encode())
+    want = PARSERS["traffic"][k]
+    if "error" in want:
+        for load in (load_traffic, parse_traffic):
+            with pytest.raises(TrafficFormatError) as got:
+                load(path)
+            assert str(got.value) == want["error"].replace("{path}", str(path))
+        return
+    got = [[p.id, int(p.proto), p.src_ip, p.src_port, p.dst_ip, p.dst_port] for p in load_traffic(path)]
+    assert got == want["packets"]
+    ids, rec = parse_traffic(path)
+    nat = [[int(i), int(r[3]), int(r[0]), int(r[2] >> 16), int(r[1]), int(r[2] & 0xFFFF)]
+           for i, r in zip(ids.tolist(), rec)]
+    assert nat == want["packets"]
