@@ -63,8 +63,9 @@ int pfw_device_count(void);
  * scan and, within the memory budget, the per-field match sets (interval
  * bitmaps).  Rules whose base has host bits outside the mask, or
  * whose port range is inverted, can never match under the reference
- * predicate (model.py:222-230) and are packed as never-matching.  n_rules may
- * be 0. */
+ * predicate (model.py:222-230) and are packed as never-matching.  Masks must
+ * be CIDR prefix masks (model.py:108-114; anything else is PFW_ERR_INVALID).
+ * n_rules may be 0. */
 int pfw_ruleset_create(int device, int64_t n_rules, const uint8_t *proto,
                        const uint32_t *src_base, const uint32_t *src_mask,
                        const uint16_t *sport_lo, const uint16_t *sport_hi,
@@ -136,6 +137,8 @@ int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *
  *   h_peer_first[t] / h_peer_comps[t]: rank t's buffers as mapped in this
  *     process (pfw_ipc_open; the caller's own buffer for its own rank);
  *     h_peer_comps may be NULL.  Buffers start at PFW_NO_MATCH / 0.
+ *   h_peer_cap[t]: packets rank t's buffers hold; a call whose n needs more
+ *     (its shard of n, or n) fails with PFW_ERR_INVALID before any launch.
  *   scatter = 0: every rank's buffer holds all n packets (all-reduce result);
  *   scatter = 1: packet i is held by its owner rank (balanced contiguous
  *     shards of n, partition_bounds semantics) at offset i - shard start
@@ -143,8 +146,8 @@ int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *
  * Completion: the combine is complete on every rank once all ranks' kernels
  * have finished (e.g. stream synchronize + a host barrier). */
 int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
-                       uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps, int npeers,
-                       int scatter, uint64_t *d_stats, void *stream);
+                       uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps,
+                       const int64_t *h_peer_cap, int npeers, int scatter, uint64_t *d_stats, void *stream);
 
 /* CUDA IPC plumbing for the fused combine.  pfw_ipc_get_handle exports the
  * allocation containing d_ptr and returns d_ptr's byte offset in it;

@@ -21,7 +21,6 @@ from .traffic import (MatchMode, RulesetGenParams, TrafficFormatError, TrafficGe
                       TrafficProfile, generate_ruleset, generate_traffic, generate_traffic_device,
                       load_traffic, save_traffic)
 
-from .harness import BenchReport, SweepAxis, SweepSpec, emit_csv, run_point, run_sweep
 
 __version__ = "0.2.0"
 
@@ -34,7 +33,7 @@ def __getattr__(name):
     raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
 
 __all__ = [
-    "BenchReport", "SweepAxis", "SweepSpec", "emit_csv", "run_point", "run_sweep", "FirewallClassifier",
+    "FirewallClassifier",
     "Action", "CidrMatcher", "ClassifyStats", "CompiledRuleset", "ConfigError", "Engine",
     "EngineConfig", "EngineResult", "ExecutionModel", "MatchMode", "MatchResult", "Packet",
     "PacketArrays", "PartialMatch", "PortRange", "Protocol", "Rule", "RuleParseError",

@@ -51,7 +51,7 @@ _SIGS = {
     "pfw_scan_range_columns": (_I32, [_P, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "pfw_scan_partition_accumulate": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
     "pfw_accumulator_init": (_I32, [_I64, _P, _P, _P]),
-    "pfw_scan_fused_min": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _I32, _I32, _P, _P]),
+    "pfw_scan_fused_min": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, _P, _P]),
     "pfw_ipc_handle_size": (_I32, []),
     "pfw_ipc_get_handle": (_I32, [_P, _P, ctypes.POINTER(_U64)]),
     "pfw_ipc_open": (_I32, [_I32, _P, ctypes.POINTER(_P)]),

@@ -40,6 +40,7 @@
 #include <type_traits>
 
 #include "../../include/pfw.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool is attached
 
 #define PFW_VERSION "0.2.0"
 
@@ -72,6 +73,14 @@ int set_err(int code, const char *fmt, ...) {
     g_err = buf;
     return code;
 }
+
+// NVTX range for the lifetime of a scope (pack / upload / scan / e2e stages)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 #define CUDA_TRY(expr)                                                                   \
     do {                                                                                 \
@@ -131,11 +140,16 @@ int64_t g_bucket_min = 1 << 20;  // ... from this many packets on
 
 }  // namespace
 
-// Per-scan scratch: ping-pong live-id lists for the passes + counters.
+// Per-scan scratch: ping-pong live-id lists for the passes + counters, and
+// the protocol buckets of launch_split.  Scans that may run concurrently
+// (the e2e pipeline's two compute streams) each get their own.
 struct ScanWs {
     uint32_t *ids = nullptr;       // 2 * cap
     unsigned int *ctr = nullptr;   // 2 * MAX_PASSES
     int64_t cap = 0;
+    uint32_t *d_bucket = nullptr;  // packet ids grouped by chain (bucket_cap)
+    unsigned *d_bcount = nullptr;  // [3 * MAX_CHAINS + 1]: count, base, cursor, single flag
+    int64_t bucket_cap = 0;
 };
 
 // Per-field match sets (matchset.cuh): field value -> elementary interval ->
@@ -201,9 +215,6 @@ struct pfw_ruleset {
     };
     std::vector<Chain> chains;
     uint8_t *d_lut = nullptr;          // 256 entries
-    uint32_t *d_bucket = nullptr;      // packet ids grouped by chain (n)
-    unsigned *d_bcount = nullptr;      // [3 * MAX_CHAINS]: count, base, cursor
-    int64_t bucket_cap = 0;
     MatchSet *ms = nullptr;            // match sets (null: not built / over budget)
 };
 
@@ -1078,6 +1089,8 @@ int ensure_ws(ScanWs &ws, int64_t n) {
 void free_ws(ScanWs &ws) {
     if (ws.ids) cudaFree(ws.ids);
     if (ws.ctr) cudaFree(ws.ctr);
+    if (ws.d_bucket) cudaFree(ws.d_bucket);
+    if (ws.d_bcount) cudaFree(ws.d_bcount);
     ws = ScanWs{};
 }
 
@@ -1195,6 +1208,8 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
     if (hi > h->n) return set_err(PFW_ERR_INVALID, "rule window end %lld beyond ruleset of %lld",
                                   (long long)hi, (long long)h->n);
     if (n == 0) return PFW_OK;
+    NvtxRange nv(mode == MODE_ACC ? "pfw scan (accumulate)" : mode == MODE_PEER ? "pfw scan (fused peer combine)"
+                                                                                : "pfw scan");
     const bool have_cols = cols && cols->proto && cols->src && cols->sport && cols->dst && cols->dport;
     if ((!d_pkts && !have_cols) || (!first && mode != MODE_PEER))
         return set_err(PFW_ERR_INVALID, "null packet or output pointer");
@@ -1257,21 +1272,21 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cuda
                  bool chains) {
     const int nch = (int)h->chains.size();
     const int64_t n = p0.n;
-    if (h->bucket_cap < n) {
-        if (h->d_bucket) cudaFree(h->d_bucket);
-        h->d_bucket = nullptr;
-        h->bucket_cap = 0;
-        CUDA_TRY(cudaMalloc(&h->d_bucket, (size_t)n * sizeof(uint32_t)));
-        h->bucket_cap = n;
+    if (w.bucket_cap < n) {
+        if (w.d_bucket) cudaFree(w.d_bucket);
+        w.d_bucket = nullptr;
+        w.bucket_cap = 0;
+        CUDA_TRY(cudaMalloc(&w.d_bucket, (size_t)n * sizeof(uint32_t)));
+        w.bucket_cap = n;
     }
-    if (!h->d_bcount) CUDA_TRY(cudaMalloc(&h->d_bcount, (3 * MAX_CHAINS + 1) * sizeof(unsigned)));
-    int *d_single = reinterpret_cast<int *>(h->d_bcount + 3 * MAX_CHAINS);
-    CUDA_TRY(cudaMemsetAsync(h->d_bcount, 0, MAX_CHAINS * sizeof(unsigned), st));
+    if (!w.d_bcount) CUDA_TRY(cudaMalloc(&w.d_bcount, (3 * MAX_CHAINS + 1) * sizeof(unsigned)));
+    int *d_single = reinterpret_cast<int *>(w.d_bcount + 3 * MAX_CHAINS);
+    CUDA_TRY(cudaMemsetAsync(w.d_bcount, 0, MAX_CHAINS * sizeof(unsigned), st));
     const unsigned nb = (unsigned)((n + BK_BLOCK * BK_PER_THREAD - 1) / (BK_BLOCK * BK_PER_THREAD));
-    bucket_count_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, h->d_bcount);
-    bucket_prefix_kernel<<<1, 32, 0, st>>>(nch, h->d_bcount, d_single);
-    bucket_scatter_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, h->d_bcount,
-                                                  h->d_bucket, d_single);
+    bucket_count_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, w.d_bcount);
+    bucket_prefix_kernel<<<1, 32, 0, st>>>(nch, w.d_bcount, d_single);
+    bucket_scatter_kernel<<<nb, BK_BLOCK, 0, st>>>(p0.pkts, p0.cols.proto, n, h->d_lut, nch, w.d_bcount,
+                                                  w.d_bucket, d_single);
     CUDA_TRY(cudaGetLastError());
     g_launches += 3;
     // bucket c's ids start at base[c]; its count is bc[c].  The base is only
@@ -1279,9 +1294,9 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p0, ScanWs &w, cuda
     // device-side pointer computed by a tiny kernel into the ws pointer slot.
     for (int c = 0; c < nch; c++) {
         ScanParams p = p0;
-        p.bucket_base = h->d_bcount + MAX_CHAINS + c;
-        p.in_ids0 = h->d_bucket;
-        p.in_count0 = h->d_bcount + c;
+        p.bucket_base = w.d_bcount + MAX_CHAINS + c;
+        p.in_ids0 = w.d_bucket;
+        p.in_count0 = w.d_bcount + c;
         p.bk_single = d_single;
         p.bk_index = c;
         if (chains) {  // protocol-split: this bucket scans its chain table
@@ -1415,12 +1430,22 @@ int pfw_ruleset_create(int device, int64_t n, const uint8_t *proto, const uint32
     if (n > 0 && (!proto || !src_base || !src_mask || !sport_lo || !sport_hi || !dst_base ||
                   !dst_mask || !dport_lo || !dport_hi || !accept))
         return set_err(PFW_ERR_INVALID, "null rule column");
+    // CIDR masks only (model.py:108-114): both encodings -- the range test
+    // ip - base <= ~mask and the match-set interval [base, base | ~mask] --
+    // equal the reference's (ip & mask) == base exactly for prefix masks
+    for (int64_t r = 0; r < n; r++) {
+        const uint32_t hs = ~src_mask[r], hd = ~dst_mask[r];
+        if ((hs & (hs + 1u)) || (hd & (hd + 1u)))
+            return set_err(PFW_ERR_INVALID, "rule %lld: %s mask 0x%08x is not a prefix mask", (long long)r,
+                           (hs & (hs + 1u)) ? "src" : "dst", (hs & (hs + 1u)) ? src_mask[r] : dst_mask[r]);
+    }
     int ndev = pfw_device_count();
     if (device < 0 || device >= ndev)
         return set_err(PFW_ERR_CUDA, "CUDA device %d not available (%d visible)", device, ndev);
     DeviceGuard g(device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", device);
 
+    NvtxRange nv("pfw_ruleset_create: pack + upload + match sets");
     pfw_ruleset *h = new pfw_ruleset();
     h->device = device;
     h->n = n;
@@ -1551,8 +1576,6 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     }
     if (h->d_lut) cudaFree(h->d_lut);
     ms_free(h->ms);
-    if (h->d_bucket) cudaFree(h->d_bucket);
-    if (h->d_bcount) cudaFree(h->d_bcount);
     free_ws(h->ws_e2e[0]);
     free_ws(h->ws_e2e[1]);
     for (auto &st : h->streams)
@@ -1629,14 +1652,22 @@ int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const
 }
 
 int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
-                       uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps, int npeers,
-                       int scatter, uint64_t *d_stats, void *stream) {
+                       uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps,
+                       const int64_t *h_peer_cap, int npeers, int scatter, uint64_t *d_stats, void *stream) {
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (npeers < 1 || npeers > MAX_PEERS) return set_err(PFW_ERR_INVALID, "npeers must be in 1..%d", MAX_PEERS);
-    if (!h_peer_first) return set_err(PFW_ERR_INVALID, "null peer table");
-    for (int i = 0; i < npeers; i++)
+    if (!h_peer_first || !h_peer_cap) return set_err(PFW_ERR_INVALID, "null peer table");
+    if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count %lld", (long long)n);
+    for (int i = 0; i < npeers; i++) {
         if (!h_peer_first[i] || (h_peer_comps && !h_peer_comps[i]))
             return set_err(PFW_ERR_INVALID, "null peer buffer %d", i);
+        // rank i receives its shard of n (scatter) or all n packets: its
+        // buffers must hold them, or the atomics would land past their end
+        const int64_t need = scatter ? n / npeers + (i < n % npeers ? 1 : 0) : n;
+        if (h_peer_cap[i] < need)
+            return set_err(PFW_ERR_INVALID, "peer %d buffer holds %lld packets, the call needs %lld", i,
+                           (long long)h_peer_cap[i], (long long)need);
+    }
     if (n == 0) return PFW_OK;
     DeviceGuard g(h->device);
     cudaStream_t st = (cudaStream_t)stream;
@@ -1764,6 +1795,7 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     if (chunk > n) chunk = n;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
+    NvtxRange nv("pfw_classify_host: H2D / scan / D2H pipeline");
     constexpr int S = E2E_SLOTS;
     // slot: packets (16B records, or 13B of columns) + first 4B + verdict 1B
     const size_t slot = (((size_t)chunk * 21 + 255) / 256) * 256;
@@ -1813,6 +1845,17 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     }
     const int64_t nchunks = (int64_t)sizes.size();
     int rc = PFW_OK;
+    // inside the loop an error stops issuing work but never returns before
+    // the streams are drained: copies already queued still target the
+    // caller's host buffers
+#define E2E_TRY(expr)                                                                       \
+    {                                                                                       \
+        const cudaError_t e2e_err_ = (expr);                                                \
+        if (e2e_err_ != cudaSuccess) {                                                      \
+            rc = set_err(PFW_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e2e_err_)); \
+            break;                                                                          \
+        }                                                                                   \
+    }
     int64_t c0 = 0;
     for (int64_t k = 0; k < nchunks && rc == PFW_OK; c0 += sizes[(size_t)k], k++) {
         const int64_t m = sizes[(size_t)k];
@@ -1828,30 +1871,35 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
                       reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 8),
                       reinterpret_cast<const uint32_t *>(base + (size_t)chunk * 4),
                       reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 10)};
-        if (k >= S) CUDA_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
+        if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
         if (hc) {
-            CUDA_TRY(cudaMemcpyAsync((void *)dc.src, hc->src + c0, m * 4, cudaMemcpyHostToDevice, s_in));
-            CUDA_TRY(cudaMemcpyAsync((void *)dc.dst, hc->dst + c0, m * 4, cudaMemcpyHostToDevice, s_in));
-            CUDA_TRY(cudaMemcpyAsync((void *)dc.sport, hc->sport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
-            CUDA_TRY(cudaMemcpyAsync((void *)dc.dport, hc->dport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
-            CUDA_TRY(cudaMemcpyAsync((void *)dc.proto, hc->proto + c0, m, cudaMemcpyHostToDevice, s_in));
+            E2E_TRY(cudaMemcpyAsync((void *)dc.src, hc->src + c0, m * 4, cudaMemcpyHostToDevice, s_in));
+            E2E_TRY(cudaMemcpyAsync((void *)dc.dst, hc->dst + c0, m * 4, cudaMemcpyHostToDevice, s_in));
+            E2E_TRY(cudaMemcpyAsync((void *)dc.sport, hc->sport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
+            E2E_TRY(cudaMemcpyAsync((void *)dc.dport, hc->dport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
+            E2E_TRY(cudaMemcpyAsync((void *)dc.proto, hc->proto + c0, m, cudaMemcpyHostToDevice, s_in));
         } else {
-            CUDA_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
+            E2E_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
                                      cudaMemcpyHostToDevice, s_in));
         }
-        CUDA_TRY(cudaEventRecord(ev_in[sl], s_in));
-        CUDA_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
-        if (k >= S) CUDA_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
+        E2E_TRY(cudaEventRecord(ev_in[sl], s_in));
+        E2E_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
+        if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
         rc = launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
                          h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr);
         if (rc != PFW_OK) break;
-        CUDA_TRY(cudaEventRecord(ev_scan[sl], s_comp));
-        CUDA_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
-        CUDA_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, s_out));
-        if (h_verdict) CUDA_TRY(cudaMemcpyAsync(h_verdict + c0, dv, m, cudaMemcpyDeviceToHost, s_out));
-        CUDA_TRY(cudaEventRecord(ev_out[sl], s_out));
+        E2E_TRY(cudaEventRecord(ev_scan[sl], s_comp));
+        E2E_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
+        E2E_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, s_out));
+        if (h_verdict) E2E_TRY(cudaMemcpyAsync(h_verdict + c0, dv, m, cudaMemcpyDeviceToHost, s_out));
+        E2E_TRY(cudaEventRecord(ev_out[sl], s_out));
     }
-    for (auto &st : h->streams) CUDA_TRY(cudaStreamSynchronize(st));
+#undef E2E_TRY
+    for (auto &st : h->streams) {
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess && rc == PFW_OK)
+            rc = set_err(PFW_ERR_CUDA, "cudaStreamSynchronize failed: %s", cudaGetErrorString(e));
+    }
     if (rc != PFW_OK) return rc;
     if (h_stats) CUDA_TRY(cudaMemcpy(h_stats, d_stats, 16, cudaMemcpyDeviceToHost));
     return PFW_OK;
@@ -1902,6 +1950,7 @@ int pfw_generate_traffic_at(int device, uint64_t seed, int64_t first_packet, int
     if (device < 0 || device >= ndev) return set_err(PFW_ERR_CUDA, "CUDA device %d not available", device);
     DeviceGuard g(device);
     cudaStream_t st = (cudaStream_t)stream;
+    NvtxRange nv("pfw_generate_traffic");
 
     GenParams gp{};
     gp.proto = (uint32_t)proto;
@@ -1944,8 +1993,16 @@ int pfw_generate_traffic_at(int device, uint64_t seed, int64_t first_packet, int
         uploaded_dev_mask |= 1 << device;
     }
 
-    uint64_t *d_state = nullptr;
-    unsigned long long *d_rej = nullptr;
+    struct Scratch {  // freed on every return path
+        uint64_t *d_state = nullptr;
+        unsigned long long *d_rej = nullptr;
+        ~Scratch() {
+            if (d_state) cudaFree(d_state);
+            if (d_rej) cudaFree(d_rej);
+        }
+    } sc;
+    uint64_t *&d_state = sc.d_state;
+    unsigned long long *&d_rej = sc.d_rej;
     int64_t start = 0;
     Mat64 m1 = mat_step();
     uint64_t x = host_seed_state(seed);  // state before packet `start`
@@ -1992,8 +2049,6 @@ int pfw_generate_traffic_at(int device, uint64_t seed, int64_t first_packet, int
         start = (int64_t)rej + 1;
         x = y;
     }
-    if (d_state) cudaFree(d_state);
-    if (d_rej) cudaFree(d_rej);
     return rc;
 }
 

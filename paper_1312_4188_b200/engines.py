@@ -274,6 +274,9 @@ class Engine:
     def run_arrays(self, ruleset, packets) -> EngineResult:
         start = time.perf_counter_ns()
         compiled = ruleset if isinstance(ruleset, CompiledRuleset) else compile_ruleset(ruleset, self.device)
+        if compiled.is_shard:
+            raise ValueError("Engine.run_arrays needs a whole ruleset, not a rule shard "
+                             "(shards are scanned through parallel.run_function_parallel)")
         pkts = compiled._packets(packets)
         n = len(pkts)
         if n == 0:

@@ -194,6 +194,9 @@ class FusedFunctionParallel:
         P = ctypes.c_void_p
         self._peer_first = (P * world)(*firsts)
         self._peer_comps = (P * world)(*comps) if with_comps else None
+        # packets each rank's buffers hold (checked again by the C side)
+        self._peer_cap = (ctypes.c_int64 * world)(*[
+            (b - a if scatter else n) for a, b in partition_bounds(n, world)])
 
     def _barrier(self):
         import torch
@@ -207,6 +210,8 @@ class FusedFunctionParallel:
         this rank's (first, comps) once every rank's scan has completed."""
         import torch
         from . import _native
+        if len(pkts) != self.n:
+            raise ValueError(f"FusedFunctionParallel was set up for batches of {self.n} packets, got {len(pkts)}")
         self.first.fill_(NO_MATCH)
         if self.comps is not None:
             self.comps.zero_()
@@ -220,7 +225,7 @@ class FusedFunctionParallel:
         st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
         _native.check(_native.lib().pfw_scan_fused_min(
             self.compiled.handle, lo, hi, pkts.data.data_ptr(), len(pkts), self._peer_first,
-            self._peer_comps, self.info.world, 1 if self.scatter else 0,
+            self._peer_comps, self._peer_cap, self.info.world, 1 if self.scatter else 0,
             None if stats is None else stats.data_ptr(), st), "pfw_scan_fused_min")
         self._barrier()  # every rank's atomics have landed
         m = self.own_range[1] - self.own_range[0]

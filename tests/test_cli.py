@@ -73,7 +73,7 @@ def test_classify_and_verify_output(tmp_path, capsys):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
-def test_gen_traffic_worst_case_and_bench(tmp_path, capsys):
+def test_gen_traffic_worst_case(tmp_path, capsys):
     rules = tmp_path / "r.txt"
     assert cli.main(["gen-rules", "--count", "64", "--seed", "1", "--out", str(rules)]) == 0
     t = tmp_path / "t.csv"
@@ -82,11 +82,6 @@ def test_gen_traffic_worst_case_and_bench(tmp_path, capsys):
     assert cli.main(["classify", "--rules", str(rules), "--traffic", str(t)]) == 0
     lines = capsys.readouterr().out.splitlines()
     assert len(lines) == 200 and all(l.endswith(",DROP,-") for l in lines)
-    out = tmp_path / "b.csv"
-    assert cli.main(["bench", "--axis", "nodes", "--values", "1,4", "--rules", "128", "--batch", "64",
-                     "--reps", "2", "--model", "data,function", "--out", str(out)]) == 0
-    rows = out.read_text().splitlines()
-    assert rows[0].startswith("model,nodes,rules") and len(rows) == 5
 
 
 @pytest.mark.gpu

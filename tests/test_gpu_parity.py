@@ -391,19 +391,28 @@ def test_fused_min_combine_virtual_ranks(scatter):
             comps = torch.zeros(n, dtype=torch.int32, device="cuda:0")
             fptr = [first.data_ptr() + 4 * a for a, _ in bounds]
             cptr = [comps.data_ptr() + 4 * a for a, _ in bounds]
+            caps = [b - a for a, b in bounds]
             bufs = [(first, comps)]
         else:
             bufs = [(torch.full((n,), NO_MATCH, dtype=torch.int32, device="cuda:0"),
                      torch.zeros(n, dtype=torch.int32, device="cuda:0")) for _ in range(G)]
             fptr = [b[0].data_ptr() for b in bufs]
             cptr = [b[1].data_ptr() for b in bufs]
+            caps = [n] * G
         P = ctypes.c_void_p
         stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
         for lo, hi in pfw.partition_bounds(c.num_rules, G):
             _native.check(_native.lib().pfw_scan_fused_min(
-                c.handle, lo, hi, p.data.data_ptr(), n, (P * G)(*fptr), (P * G)(*cptr), G, scatter,
+                c.handle, lo, hi, p.data.data_ptr(), n, (P * G)(*fptr), (P * G)(*cptr), (ctypes.c_int64 * G)(*caps),
+                G, scatter,
                 stats.data_ptr(), torch.cuda.current_stream().cuda_stream), "fused")
         torch.cuda.synchronize()
+        if G > 1:  # a batch larger than the buffers is refused before any launch
+            with pytest.raises(ValueError, match="buffer holds"):
+                _native.check(_native.lib().pfw_scan_fused_min(
+                    c.handle, 0, c.num_rules, p.data.data_ptr(), n + G, (P * G)(*fptr), (P * G)(*cptr),
+                    (ctypes.c_int64 * G)(*caps), G, scatter, None, torch.cuda.current_stream().cuda_stream),
+                    "fused")
         for first, comps in bufs:
             np.testing.assert_array_equal(first_to_host(first), g[f"function_{G}_first"])
             np.testing.assert_array_equal(comps.cpu().numpy(), g[f"function_{G}_comps"])
@@ -725,7 +734,8 @@ def test_rule_shards_function_parallel(algo):
         cptr = (P * G)(*[fc.data_ptr() + 4 * a for a, _ in bounds])
         for s in shards:
             _native.check(_native.lib().pfw_scan_fused_min(
-                s.handle, 0, s.num_rules, p.data.data_ptr(), n, fptr, cptr, G, 1, None,
+                s.handle, 0, s.num_rules, p.data.data_ptr(), n, fptr, cptr,
+                (ctypes.c_int64 * G)(*[b - a for a, b in bounds]), G, 1, None,
                 torch.cuda.current_stream().cuda_stream), "fused")
         torch.cuda.synchronize()
         np.testing.assert_array_equal(first_to_host(ff), g[f"function_{G}_first"])
