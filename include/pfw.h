@@ -35,6 +35,8 @@ extern "C" {
 #endif
 
 #define PFW_NO_MATCH 0x7FFFFFFFu
+/* pfw_classify_host_ex flags */
+#define PFW_HOST_FIRST_MINUS1 1u /* unmatched packets get first = 0xFFFFFFFF (int32 -1, scan_range's value) */
 #define PFW_MAX_RULES 0x7FFFFFFE
 
 enum {
@@ -149,6 +151,11 @@ int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pk
                        uint32_t *const *h_peer_first, uint32_t *const *h_peer_comps,
                        const int64_t *h_peer_cap, int npeers, int scatter, uint64_t *d_stats, void *stream);
 
+/* In-process multi-GPU fused combine (Engine(devices=...)): let `device`'s
+ * kernels access `peer`'s memory directly over NVLink (cudaDeviceEnablePeerAccess);
+ * already enabled, or device == peer, is success. */
+int pfw_peer_enable(int device, int peer);
+
 /* CUDA IPC plumbing for the fused combine.  pfw_ipc_get_handle exports the
  * allocation containing d_ptr and returns d_ptr's byte offset in it;
  * pfw_ipc_open maps a peer's allocation (NVLink peer access) and returns its
@@ -176,11 +183,23 @@ int pfw_classify_host(pfw_ruleset_t h, const void *h_pkts, int64_t n, uint32_t *
                       uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk);
 
 /* pfw_classify_host for the reference's column layout (PacketArrays):
- * copies 13 bytes per packet (five column copies per chunk), no host packing. */
+ * copies 13 bytes per packet (five column copies per chunk), no host packing.
+ * Both host entry points take pinned or pageable buffers: pageable ones are
+ * staged through a per-handle pinned ring by a host thread pool, chunk by
+ * chunk, overlapping the device copies and scans. */
 int pfw_classify_host_columns(pfw_ruleset_t h, const uint8_t *h_proto, const uint32_t *h_src_ip,
                               const uint16_t *h_src_port, const uint32_t *h_dst_ip,
                               const uint16_t *h_dst_port, int64_t n, uint32_t *h_first,
                               uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk);
+
+/* Either entry point with flags: h_pkts (16-byte records) non-NULL selects
+ * the record layout, otherwise the five columns are read.  flags:
+ * PFW_HOST_FIRST_MINUS1 writes -1 for unmatched packets, so h_first is the
+ * reference's scan_range result (classifier.py:146-162) as int32. */
+int pfw_classify_host_ex(pfw_ruleset_t h, const void *h_pkts, const uint8_t *h_proto,
+                         const uint32_t *h_src_ip, const uint16_t *h_src_port, const uint32_t *h_dst_ip,
+                         const uint16_t *h_dst_port, int64_t n, uint32_t *h_first, uint8_t *h_verdict,
+                         uint64_t *h_stats, int64_t chunk, uint32_t flags);
 
 /* Bit-exact UNIFORM traffic generation on the device.  Replaces
  * generate_traffic(TrafficProfile(...)) with match_mode UNIFORM

@@ -8,7 +8,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "pfw.cu")
 SRC_HOST = os.path.join(PKG, "csrc", "hostio.cpp")
-HEADERS = [os.path.join(PKG, "csrc", "matchset.cuh")]
+HEADERS = [os.path.join(PKG, "csrc", "matchset.cuh"), os.path.join(PKG, "csrc", "hostpool.h")]
 LIB = os.path.join(PKG, "libpfw.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -15,6 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PFW_LIB") or os.path.join(PKG, "libpfw.so")  # PFW_LIB: experiment builds
 
 NO_MATCH = 0x7FFFFFFF  # PFW_NO_MATCH
+HOST_FIRST_MINUS1 = 1  # PFW_HOST_FIRST_MINUS1
 PFW_OK, PFW_ERR_INVALID, PFW_ERR_CUDA, PFW_ERR_NOMEM, PFW_ERR_GENERATION = range(5)
 
 
@@ -52,6 +53,7 @@ _SIGS = {
     "pfw_scan_partition_accumulate": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
     "pfw_accumulator_init": (_I32, [_I64, _P, _P, _P]),
     "pfw_scan_fused_min": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, _P, _P]),
+    "pfw_peer_enable": (_I32, [_I32, _I32]),
     "pfw_ipc_handle_size": (_I32, []),
     "pfw_ipc_get_handle": (_I32, [_P, _P, ctypes.POINTER(_U64)]),
     "pfw_ipc_open": (_I32, [_I32, _P, ctypes.POINTER(_P)]),
@@ -60,6 +62,7 @@ _SIGS = {
     "pfw_combine_min": (_I32, [_P, _I64, _I64, _P, _P]),
     "pfw_classify_host": (_I32, [_P, _P, _I64, _P, _P, _P, _I64]),
     "pfw_classify_host_columns": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I64]),
+    "pfw_classify_host_ex": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _U32]),
     "pfw_generate_traffic": (_I32, [_I32, _U64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,
                                     _I32, _I32, _P, _P]),
     "pfw_generate_traffic_at": (_I32, [_I32, _U64, _I64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,

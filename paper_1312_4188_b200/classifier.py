@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes
 import time
 import weakref
+from collections.abc import Sequence as _SequenceABC
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -40,6 +41,7 @@ from .model import Action, MatchResult, Packet, Protocol, Ruleset
 __all__ = [
     "ClassifyStats",
     "CompiledRuleset",
+    "MatchResults",
     "PacketArrays",
     "classify",
     "classify_batch_sequential",
@@ -96,6 +98,93 @@ def classify(ruleset: Ruleset, packet: Packet) -> MatchResult:
     return MatchResult(Action.ACCEPT if compiled.action_accept[idx] else Action.DROP, idx, idx + 1)
 
 
+class MatchResults(_SequenceABC):
+    """Array-backed, lazy ``list[MatchResult]`` (classifier.py:175-185 without
+    building N objects): ``results[i]`` is a MatchResult made on access from
+    the first-match index array (-1 = default deny), the per-packet
+    comparison counts and the ruleset's action column.  Compares equal to a
+    list of the same MatchResults (the reference returns a list), so
+    ``results == expected`` and ``results == []`` behave as in the reference.
+
+    ``comparisons=None`` means the sequential / data-parallel count
+    ``first + 1`` or ``num_rules`` (classifier.py:200), derived on access."""
+
+    __slots__ = ("first", "_comps", "_accept", "_num_rules")
+
+    def __init__(self, first, comparisons, action_accept, num_rules: int) -> None:
+        self.first = np.asarray(first)
+        self._comps = None if comparisons is None else np.asarray(comparisons)
+        self._accept = action_accept
+        self._num_rules = int(num_rules)
+
+    @property
+    def comparisons(self) -> np.ndarray:
+        if self._comps is None:
+            f = self.first.astype(np.int64)
+            self._comps = np.where(f >= 0, f + 1, self._num_rules)
+        return self._comps
+
+    @property
+    def verdict_accept(self) -> np.ndarray:
+        f = self.first
+        hit = f >= 0
+        out = np.zeros(len(f), dtype=np.bool_)
+        out[hit] = np.asarray(self._accept)[f[hit]]
+        return out
+
+    def __len__(self) -> int:
+        return int(self.first.shape[0])
+
+    def _make(self, idx: int, comps: int) -> MatchResult:
+        if idx < 0:
+            return MatchResult(Action.DROP, None, comps)
+        return MatchResult(Action.ACCEPT if self._accept[idx] else Action.DROP, idx, comps)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            c = None if self._comps is None else self._comps[i]
+            return MatchResults(self.first[i], c, self._accept, self._num_rules)
+        n = len(self)
+        i = int(i)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("MatchResults index out of range")
+        f = int(self.first[i])
+        c = int(self._comps[i]) if self._comps is not None else (f + 1 if f >= 0 else self._num_rules)
+        return self._make(f, c)
+
+    def __iter__(self):
+        step = 1 << 16
+        for a in range(0, len(self), step):
+            fs = self.first[a:a + step].tolist()
+            cs = self.comparisons[a:a + step].tolist()
+            for f, c in zip(fs, cs):
+                yield self._make(f, c)
+
+    def tolist(self) -> list[MatchResult]:
+        return list(iter(self))
+
+    def __eq__(self, other) -> bool:
+        if isinstance(other, MatchResults):
+            return (len(self) == len(other) and np.array_equal(self.first, other.first)
+                    and np.array_equal(self.comparisons, other.comparisons)
+                    and np.array_equal(self.verdict_accept, other.verdict_accept))
+        if isinstance(other, (list, tuple)):
+            return len(self) == len(other) and all(a == b for a, b in zip(self, other))
+        return NotImplemented
+
+    def __ne__(self, other):
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    __hash__ = None
+
+    def __repr__(self) -> str:
+        head = ", ".join(repr(r) for r in self[:3])
+        return f"MatchResults([{head}{', ...' if len(self) > 3 else ''}], n={len(self)})"
+
+
 # ----------------------------------------------------------------- packets
 
 class PacketArrays:
@@ -130,6 +219,14 @@ class PacketArrays:
         out[:, 2] = (np.asarray(src_port, dtype=np.uint32) << 16) | np.asarray(dst_port, dtype=np.uint32)
         out[:, 3] = np.asarray(proto, dtype=np.uint32)
         return out
+
+    @staticmethod
+    def unpack_host(records: np.ndarray) -> dict:
+        """Inverse of pack_host: the five reference columns of [n, 4] records."""
+        rec = np.asarray(records, dtype=np.uint32).reshape(-1, 4)
+        return {"proto": rec[:, 3].astype(np.uint8), "src_ip": rec[:, 0].copy(),
+                "src_port": (rec[:, 2] >> 16).astype(np.uint16), "dst_ip": rec[:, 1].copy(),
+                "dst_port": (rec[:, 2] & 0xFFFF).astype(np.uint16)}
 
     @classmethod
     def from_host_records(cls, records: np.ndarray, device: int | None = None) -> "PacketArrays":
@@ -331,20 +428,52 @@ class CompiledRuleset:
             _ptr(stats), st), "pfw_scan_range_columns")
         return first
 
-    def classify_host_columns(self, cols: dict, chunk: int = 1 << 23):
-        """End-to-end over HOST columns (numpy; pinned memory overlaps the copies):
-        returns (first int64 with -1 for default deny, verdict bool, [sum, max] comps)."""
-        n = len(cols["proto"])
-        arrs = [np.ascontiguousarray(cols[f], dtype=d) for f, d in zip(PACKET_COLUMNS, _PACKET_DTYPES)]
-        first = np.empty(n, dtype=np.uint32)
-        verdict = np.empty(n, dtype=np.uint8)
+    def classify_host(self, packets, chunk: int = 1 << 23, out=None):
+        """End-to-end first match over HOST packets, returned in host memory.
+
+        ``packets``: a dict of the reference's PacketArrays columns (numpy:
+        proto, src_ip, src_port, dst_ip, dst_port; classifier.py:62-95), or an
+        (n, 4) uint32 array of 16-byte records.  Pinned inputs are copied by
+        DMA directly; pageable ones are staged chunk by chunk through the
+        handle's pinned ring by the native host thread pool -- either way
+        host copies, device copies and scans overlap (pfw_classify_host_ex).
+
+        Returns (first int32 [-1 = default deny], verdict bool, stats int64
+        [sum, max] of the sequential comparison counts).  The outputs live in
+        pinned memory from torch's caching host allocator (reused across
+        calls), so results land by DMA with no staging copy; ``out`` = (first
+        int32, verdict uint8 or bool) host arrays to write instead."""
+        torch = _torch()
+        if isinstance(packets, dict):
+            arrs = [np.ascontiguousarray(packets[f], dtype=d) for f, d in zip(PACKET_COLUMNS, _PACKET_DTYPES)]
+            n = len(arrs[0])
+            for f, a in zip(PACKET_COLUMNS, arrs):
+                if len(a) != n:
+                    raise ValueError(f"packet column {f} has {len(a)} entries, expected {n}")
+            rec_ptr, col_ptrs = None, [a.ctypes.data for a in arrs]
+        else:
+            rec = np.ascontiguousarray(packets, dtype=np.uint32).reshape(-1, 4)
+            arrs = [rec]
+            n = rec.shape[0]
+            rec_ptr, col_ptrs = rec.ctypes.data, [None] * 5
+        if out is None:
+            first = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+            verdict = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy().view(np.bool_)
+        else:
+            first, verdict = out
+            if first.dtype != np.int32 or verdict.dtype.itemsize != 1 or len(first) != n or len(verdict) != n \
+                    or not first.flags.c_contiguous or not verdict.flags.c_contiguous:
+                raise ValueError("out must be contiguous (int32[n], uint8/bool[n]) host arrays")
         stats = np.zeros(2, dtype=np.uint64)
-        check(_native.lib().pfw_classify_host_columns(self._h, *[a.ctypes.data for a in arrs], n,
-                                                      first.ctypes.data, verdict.ctypes.data,
-                                                      stats.ctypes.data, chunk), "pfw_classify_host_columns")
-        f = first.astype(np.int64)
-        f[f == NO_MATCH] = -1
-        return f, verdict.astype(np.bool_), stats.astype(np.int64)
+        check(_native.lib().pfw_classify_host_ex(self._h, rec_ptr, *col_ptrs, n, first.ctypes.data,
+                                                 verdict.ctypes.data, stats.ctypes.data, chunk,
+                                                 _native.HOST_FIRST_MINUS1), "pfw_classify_host_ex")
+        return first, verdict, stats.astype(np.int64)
+
+    def classify_host_columns(self, cols: dict, chunk: int = 1 << 23):
+        """classify_host over the five columns, first as int64 (scan_range's dtype)."""
+        f, v, st = self.classify_host(cols, chunk)
+        return f.astype(np.int64), v.copy(), st
 
     def scan_partition_accumulate(self, pkts: PacketArrays, lo: int, hi: int, first, comps, stats=None,
                                   stream: int | None = None) -> None:
@@ -376,18 +505,10 @@ class CompiledRuleset:
     def first_match(self, packet: Packet) -> int:
         return int(self.scan_range([packet], 0, self.num_rules)[0])
 
-    def build_results(self, first: np.ndarray, comparisons: np.ndarray) -> list[MatchResult]:
-        """MatchResults from first-match indices and counts (classifier.py:175-185)."""
-        accept = self.action_accept
-        acc, drop = Action.ACCEPT, Action.DROP
-        out = []
-        append = out.append
-        for idx, comps in zip(first.tolist(), comparisons.tolist()):
-            if idx < 0:
-                append(MatchResult(drop, None, comps))
-            else:
-                append(MatchResult(acc if accept[idx] else drop, idx, comps))
-        return out
+    def build_results(self, first: np.ndarray, comparisons) -> MatchResults:
+        """MatchResults from first-match indices and counts (classifier.py:175-185),
+        array-backed: MatchResult objects are made only when accessed."""
+        return MatchResults(first, comparisons, self.action_accept, self.num_rules)
 
 
 def first_to_host(first) -> np.ndarray:

@@ -40,7 +40,8 @@
 #include <type_traits>
 
 #include "../../include/pfw.h"
-#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool is attached
+#include <nvtx3/nvToolsExt.h>
+#include "hostpool.h"  // header-only NVTX v3: ranges cost nothing unless a tool is attached
 
 #define PFW_VERSION "0.2.0"
 
@@ -198,6 +199,8 @@ struct pfw_ruleset {
     // e2e workspace
     void *d_ws = nullptr;
     size_t ws_bytes = 0;
+    void *h_stage = nullptr;       // pinned staging ring for pageable e2e buffers (same slots as d_ws)
+    size_t stage_bytes = 0;
     cudaStream_t streams[4] = {};  // e2e copy-in, compute x2 (alternating chunks), copy-out
     cudaEvent_t events[3 * 3] = {};                          // e2e per-slot in / scan / out
     ScanWs ws;         // default (calls on the caller's stream)
@@ -263,6 +266,7 @@ struct ScanParams {
     unsigned long long *blocks_read;  // match-set scan with summaries: block reads (null = not counted)
     int tile;
     uint32_t one;  // runtime 1: keeps ptxas from folding x*1+c into IADD3
+    uint32_t nomatch_out;  // MODE_WRITE: first[] value of an unmatched packet (PFW_NO_MATCH, or -1 for host views)
     uint32_t index_base;  // rule shard: reported indices are index_base + local position
     // MODE_PEER (fused function-parallel combine): result buffers of every
     // rank, reached over NVLink through CUDA IPC mappings
@@ -308,7 +312,7 @@ __device__ __forceinline__ void emit_result(const ScanParams &p, uint32_t id, ui
             }
         }
     } else {
-        p.first[id] = f;
+        p.first[id] = f != PFW_NO_MATCH ? f : p.nomatch_out;
         if (p.comps) p.comps[id] = c;
         if (p.verdict) p.verdict[id] = (fl != PFW_NO_MATCH) ? p.accept[fl] : (uint8_t)0;
     }
@@ -1198,7 +1202,7 @@ int launch_split(pfw_ruleset *h, int mode, const ScanParams &p, ScanWs &w, cudaS
 int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_pkts, int64_t n,
                 uint32_t *first, uint32_t *comps, uint8_t *verdict, uint64_t *stats,
                 cudaStream_t st, ScanWs *ws = nullptr, const ScanParams *peer = nullptr,
-                const PacketCols *cols = nullptr) {
+                const PacketCols *cols = nullptr, uint32_t nomatch_out = PFW_NO_MATCH) {
     const bool acc = mode == MODE_ACC;
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count %lld", (long long)n);
@@ -1233,6 +1237,7 @@ int launch_scan(pfw_ruleset *h, int mode, int64_t lo, int64_t hi, const void *d_
     p.stats = reinterpret_cast<unsigned long long *>(stats);
     p.tile = g_tile;
     p.one = 1;
+    p.nomatch_out = nomatch_out;
     p.index_base = (uint32_t)h->index_base;
     DeviceGuard g(h->device);
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
@@ -1568,6 +1573,7 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     if (h->d_rules) cudaFree(h->d_rules);
     if (h->d_accept) cudaFree(h->d_accept);
     if (h->d_ws) cudaFree(h->d_ws);
+    if (h->h_stage) cudaFreeHost(h->h_stage);
     free_ws(h->ws);
     if (h->d_peers) cudaFree(h->d_peers);
     for (auto &ch : h->chains) {
@@ -1689,6 +1695,25 @@ int pfw_scan_fused_min(pfw_ruleset_t h, int64_t lo, int64_t hi, const void *d_pk
                        &peer);
 }
 
+int pfw_peer_enable(int device, int peer) {
+    const int ndev = pfw_device_count();
+    if (device < 0 || device >= ndev || peer < 0 || peer >= ndev)
+        return set_err(PFW_ERR_INVALID, "device %d / peer %d outside the %d visible devices", device, peer, ndev);
+    if (device == peer) return PFW_OK;
+    int can = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return set_err(PFW_ERR_CUDA, "device %d cannot access device %d's memory (no P2P)", device, peer);
+    DeviceGuard g(device);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return PFW_OK;
+    }
+    if (e != cudaSuccess) return set_err(PFW_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", device, peer,
+                                         cudaGetErrorString(e));
+    return PFW_OK;
+}
+
 int pfw_ipc_handle_size(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 
 // cudaIpcGetMemHandle exports the whole allocation that contains d_ptr; a
@@ -1769,8 +1794,22 @@ int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d
     return PFW_OK;
 }
 
+// Host buffers the DMA engines can read / write directly (pinned or
+// registered, or managed); anything else is pageable and goes through the
+// handle's pinned staging ring.
+static bool host_is_pinned(const void *p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged || a.type == cudaMemoryTypeDevice;
+}
+
 static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketCols *hc, int64_t n,
-                              uint32_t *h_first, uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk) {
+                              uint32_t *h_first, uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk,
+                              uint32_t flags = 0) {
     // Three-stage pipeline over E2E_SLOTS buffer slots:
     //   copy-in stream   H2D chunk k into slot k%S     (waits: scan k-S done)
     //   compute streams  scan chunk k on stream k%2    (waits: H2D k done); two
@@ -1778,6 +1817,12 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     //                    while chunk k's small late passes finish
     //   copy-out stream  D2H results of chunk k        (waits: scan k done)
     // so H2D of later chunks, the scans and D2H of earlier chunks all overlap.
+    // Pageable caller buffers are staged through a pinned ring of the same S
+    // slots by the host thread pool (HostPool): chunk k's columns are copied
+    // into pinned memory while the GPU copies / scans earlier chunks, and a
+    // chunk's results are copied out once its D2H has landed -- DMA from
+    // pageable memory would otherwise stage synchronously and serialise the
+    // pipeline.
     if (!h) return set_err(PFW_ERR_INVALID, "null ruleset handle");
     if (n < 0) return set_err(PFW_ERR_INVALID, "negative packet count");
     if (h_stats) h_stats[0] = h_stats[1] = 0;
@@ -1797,6 +1842,20 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     if (!g.ok) return set_err(PFW_ERR_CUDA, "cudaSetDevice(%d) failed", h->device);
     NvtxRange nv("pfw_classify_host: H2D / scan / D2H pipeline");
     constexpr int S = E2E_SLOTS;
+    // which caller buffers need staging (inputs: records or the 5 columns)
+    const void *in_ptr[5] = {h_pkts, nullptr, nullptr, nullptr, nullptr};
+    size_t in_w[5] = {16, 0, 0, 0, 0};  // bytes per packet of each input buffer
+    int nin = 1;
+    if (hc) {
+        const void *q[5] = {hc->src, hc->dst, hc->sport, hc->dport, hc->proto};
+        const size_t w[5] = {4, 4, 2, 2, 1};
+        for (int i = 0; i < 5; i++) in_ptr[i] = q[i], in_w[i] = w[i];
+        nin = 5;
+    }
+    bool stage_in[5] = {}, any_in = false;
+    for (int i = 0; i < nin; i++) any_in |= stage_in[i] = !host_is_pinned(in_ptr[i]);
+    const bool stage_first = !host_is_pinned(h_first);
+    const bool stage_verd = h_verdict && !host_is_pinned(h_verdict);
     // slot: packets (16B records, or 13B of columns) + first 4B + verdict 1B
     const size_t slot = (((size_t)chunk * 21 + 255) / 256) * 256;
     const size_t need = S * slot + 256;
@@ -1806,6 +1865,13 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         h->ws_bytes = 0;
         CUDA_TRY(cudaMalloc(&h->d_ws, need));
         h->ws_bytes = need;
+    }
+    if ((any_in || stage_first || stage_verd) && h->stage_bytes < S * slot) {
+        if (h->h_stage) cudaFreeHost(h->h_stage);
+        h->h_stage = nullptr;
+        h->stage_bytes = 0;
+        CUDA_TRY(cudaHostAlloc(&h->h_stage, S * slot, cudaHostAllocPortable));
+        h->stage_bytes = S * slot;
     }
     for (auto &st : h->streams)
         if (!st) CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1844,6 +1910,27 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         }
     }
     const int64_t nchunks = (int64_t)sizes.size();
+    std::vector<int64_t> starts((size_t)nchunks + 1, 0);
+    for (int64_t k = 0; k < nchunks; k++) starts[(size_t)k + 1] = starts[(size_t)k] + sizes[(size_t)k];
+    HostPool &pool = HostPool::get();
+    char *hs = static_cast<char *>(h->h_stage);
+    // slot layout (device and staging alike): inputs at [0, 16*chunk) -- records,
+    // or columns src | dst | sport | dport | proto at 0, 4, 8, 10, 12 x chunk --,
+    // first at 16*chunk, verdict at 20*chunk
+    const size_t in_off[5] = {0, (size_t)chunk * 4, (size_t)chunk * 8, (size_t)chunk * 10, (size_t)chunk * 12};
+    int64_t drained = 0;  // chunks whose staged results have been copied out
+    auto drain = [&](int64_t upto) -> cudaError_t {  // copy staged results of chunks < upto out
+        for (; drained < upto; drained++) {
+            const int sl = (int)(drained % S);
+            const cudaError_t e = cudaEventSynchronize(ev_out[sl]);
+            if (e != cudaSuccess) return e;
+            const int64_t c0 = starts[(size_t)drained], m = sizes[(size_t)drained];
+            char *base = hs + sl * slot;
+            if (stage_first) pool.copy(h_first + c0, base + (size_t)chunk * 16, (size_t)m * 4);
+            if (stage_verd) pool.copy(h_verdict + c0, base + (size_t)chunk * 20, (size_t)m);
+        }
+        return cudaSuccess;
+    };
     int rc = PFW_OK;
     // inside the loop an error stops issuing work but never returns before
     // the streams are drained: copies already queued still target the
@@ -1856,43 +1943,62 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
             break;                                                                          \
         }                                                                                   \
     }
-    int64_t c0 = 0;
-    for (int64_t k = 0; k < nchunks && rc == PFW_OK; c0 += sizes[(size_t)k], k++) {
-        const int64_t m = sizes[(size_t)k];
+    for (int64_t k = 0; k < nchunks && rc == PFW_OK; k++) {
+        const int64_t c0 = starts[(size_t)k], m = sizes[(size_t)k];
         const int sl = (int)(k % S);
         cudaStream_t s_comp = h->streams[1 + (k & 1)];
         char *base = ws + sl * slot;
+        char *sbase = hs + sl * slot;
         uint4 *dp = reinterpret_cast<uint4 *>(base);
         uint32_t *df = reinterpret_cast<uint32_t *>(base + (size_t)chunk * 16);
         uint8_t *dv = reinterpret_cast<uint8_t *>(base + (size_t)chunk * 20);
-        // column layout inside the 16B/packet region: src | dst | sport | dport | proto
-        PacketCols dc{reinterpret_cast<const uint8_t *>(base + (size_t)chunk * 12),
-                      reinterpret_cast<const uint32_t *>(base),
-                      reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 8),
-                      reinterpret_cast<const uint32_t *>(base + (size_t)chunk * 4),
-                      reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 10)};
+        PacketCols dc{reinterpret_cast<const uint8_t *>(base + in_off[4]), reinterpret_cast<const uint32_t *>(base),
+                      reinterpret_cast<const uint16_t *>(base + in_off[2]),
+                      reinterpret_cast<const uint32_t *>(base + in_off[1]),
+                      reinterpret_cast<const uint16_t *>(base + in_off[3])};
         if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
-        if (hc) {
-            E2E_TRY(cudaMemcpyAsync((void *)dc.src, hc->src + c0, m * 4, cudaMemcpyHostToDevice, s_in));
-            E2E_TRY(cudaMemcpyAsync((void *)dc.dst, hc->dst + c0, m * 4, cudaMemcpyHostToDevice, s_in));
-            E2E_TRY(cudaMemcpyAsync((void *)dc.sport, hc->sport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
-            E2E_TRY(cudaMemcpyAsync((void *)dc.dport, hc->dport + c0, m * 2, cudaMemcpyHostToDevice, s_in));
-            E2E_TRY(cudaMemcpyAsync((void *)dc.proto, hc->proto + c0, m, cudaMemcpyHostToDevice, s_in));
-        } else {
-            E2E_TRY(cudaMemcpyAsync(dp, static_cast<const char *>(h_pkts) + c0 * 16, m * 16,
-                                     cudaMemcpyHostToDevice, s_in));
+        if (any_in) {
+            // the staging slot's previous H2D (chunk k - S) must have read it
+            if (k >= S) E2E_TRY(cudaEventSynchronize(ev_in[sl]));
+            for (int i = 0; i < nin; i++)
+                if (stage_in[i])
+                    pool.copy(sbase + in_off[i], static_cast<const char *>(in_ptr[i]) + (size_t)c0 * in_w[i],
+                              (size_t)m * in_w[i]);
         }
+        bool fail = false;
+        for (int i = 0; i < nin; i++) {
+            const char *src = stage_in[i] ? sbase + in_off[i]
+                                          : static_cast<const char *>(in_ptr[i]) + (size_t)c0 * in_w[i];
+            const cudaError_t e = cudaMemcpyAsync(base + in_off[i], src, (size_t)m * in_w[i],
+                                                  cudaMemcpyHostToDevice, s_in);
+            if (e != cudaSuccess) {
+                rc = set_err(PFW_ERR_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
+                fail = true;
+                break;
+            }
+        }
+        if (fail) break;
         E2E_TRY(cudaEventRecord(ev_in[sl], s_in));
         E2E_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
         if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
         rc = launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
-                         h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr);
+                         h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr,
+                         (flags & PFW_HOST_FIRST_MINUS1) ? 0xFFFFFFFFu : PFW_NO_MATCH);
         if (rc != PFW_OK) break;
         E2E_TRY(cudaEventRecord(ev_scan[sl], s_comp));
         E2E_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
-        E2E_TRY(cudaMemcpyAsync(h_first + c0, df, m * 4, cudaMemcpyDeviceToHost, s_out));
-        if (h_verdict) E2E_TRY(cudaMemcpyAsync(h_verdict + c0, dv, m, cudaMemcpyDeviceToHost, s_out));
+        // a staged output slot is reused by chunk k: chunk k - S's results
+        // must have been copied out of it first
+        if (stage_first || stage_verd) E2E_TRY(drain(k - S + 1 > 0 ? k - S + 1 : 0));
+        E2E_TRY(cudaMemcpyAsync(stage_first ? reinterpret_cast<uint32_t *>(sbase + (size_t)chunk * 16) : h_first + c0,
+                                df, m * 4, cudaMemcpyDeviceToHost, s_out));
+        if (h_verdict)
+            E2E_TRY(cudaMemcpyAsync(stage_verd ? reinterpret_cast<uint8_t *>(sbase + (size_t)chunk * 20) : h_verdict + c0,
+                                    dv, m, cudaMemcpyDeviceToHost, s_out));
         E2E_TRY(cudaEventRecord(ev_out[sl], s_out));
+        // copy out what has landed meanwhile (keeps the host busy while the
+        // GPU works; never waits for the chunk just issued)
+        if ((stage_first || stage_verd) && k >= 1) E2E_TRY(drain(k - 1 > drained ? k - 1 : drained));
     }
 #undef E2E_TRY
     for (auto &st : h->streams) {
@@ -1901,6 +2007,10 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
             rc = set_err(PFW_ERR_CUDA, "cudaStreamSynchronize failed: %s", cudaGetErrorString(e));
     }
     if (rc != PFW_OK) return rc;
+    if (stage_first || stage_verd) {
+        const cudaError_t e = drain(nchunks);
+        if (e != cudaSuccess) return set_err(PFW_ERR_CUDA, "staged copy-out failed: %s", cudaGetErrorString(e));
+    }
     if (h_stats) CUDA_TRY(cudaMemcpy(h_stats, d_stats, 16, cudaMemcpyDeviceToHost));
     return PFW_OK;
 }
@@ -1919,6 +2029,18 @@ int pfw_classify_host_columns(pfw_ruleset_t h, const uint8_t *h_proto, const uin
         return set_err(PFW_ERR_INVALID, "null packet column");
     const PacketCols hc{h_proto, h_src_ip, h_src_port, h_dst_ip, h_dst_port};
     return classify_host_impl(h, nullptr, &hc, n, h_first, h_verdict, h_stats, chunk);
+}
+
+int pfw_classify_host_ex(pfw_ruleset_t h, const void *h_pkts, const uint8_t *h_proto, const uint32_t *h_src_ip,
+                         const uint16_t *h_src_port, const uint32_t *h_dst_ip, const uint16_t *h_dst_port,
+                         int64_t n, uint32_t *h_first, uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk,
+                         uint32_t flags) {
+    if (flags & ~(uint32_t)PFW_HOST_FIRST_MINUS1) return set_err(PFW_ERR_INVALID, "unknown flags 0x%x", flags);
+    if (h_pkts) return classify_host_impl(h, h_pkts, nullptr, n, h_first, h_verdict, h_stats, chunk, flags);
+    if (n > 0 && (!h_proto || !h_src_ip || !h_src_port || !h_dst_ip || !h_dst_port))
+        return set_err(PFW_ERR_INVALID, "null packet column");
+    const PacketCols hc{h_proto, h_src_ip, h_src_port, h_dst_ip, h_dst_port};
+    return classify_host_impl(h, nullptr, &hc, n, h_first, h_verdict, h_stats, chunk, flags);
 }
 
 int pfw_generate_traffic(int device, uint64_t seed, int64_t n, int proto, uint32_t src_base,

@@ -36,8 +36,8 @@ from typing import Iterable, Sequence
 import numpy as np
 
 from . import _native
-from .classifier import (ClassifyStats, CompiledRuleset, PacketArrays, classify_batch_sequential,
-                         compile_ruleset, first_to_host)
+from .classifier import (NO_MATCH, ClassifyStats, CompiledRuleset, MatchResults, PacketArrays,
+                         classify_batch_sequential, compile_ruleset, first_to_host)
 from .model import Action, MatchResult, Packet, Rule, Ruleset
 
 __all__ = [
@@ -80,6 +80,8 @@ class EngineConfig:
 
     ``nodes``: packet chunks (data), rule partitions (function) or rule lanes
     (hybrid); it defines the function/hybrid comparison counters.
+    ``gpus``: how many GPUs the Engine shards over (results and counters do
+    not depend on it).
     ``batch_size``/``executor``/``max_workers`` are validated as in the
     reference and otherwise ignored (the GPU replaces the pool).
     """
@@ -89,8 +91,11 @@ class EngineConfig:
     batch_size: int = 4096
     executor: str = "process"
     max_workers: int | None = None
+    gpus: int = 1  # GPUs one Engine drives (packet shards / rule shards; see Engine)
 
     def __post_init__(self) -> None:
+        if not 1 <= self.gpus <= 64:
+            raise ConfigError(f"gpus must be within 1..64, got {self.gpus}")
         if not 1 <= self.nodes <= MAX_NODES:
             raise ConfigError(f"nodes must be within 1..{MAX_NODES}, got {self.nodes}")
         if self.batch_size < 1:
@@ -211,33 +216,112 @@ def combine_partition_matches(local_first, num_rules: int):
     return first_to_host(out)
 
 
-@dataclass(frozen=True)
 class EngineResult:
-    """Array form of one run: no per-packet objects (the large-batch fast path)."""
+    """Array form of one run: no per-packet objects (the large-batch fast path).
 
-    first: np.ndarray        # int64, -1 = default deny
-    comparisons: np.ndarray  # int64 per packet
-    verdict_accept: np.ndarray  # bool per packet
-    stats: ClassifyStats
+    ``first``: matched rule index per packet, -1 = default deny (int32 from
+    the host path, int64 otherwise); ``verdict_accept``: bool per packet;
+    ``comparisons``: per-packet comparison counts -- given by the kernels for
+    the function-parallel / hybrid models, derived on first access for the
+    sequential / data-parallel ones (``first + 1`` or R, classifier.py:200);
+    ``stats``: ClassifyStats."""
+
+    __slots__ = ("first", "verdict_accept", "stats", "_comps", "_num_rules")
+
+    def __init__(self, first, comparisons, verdict_accept, stats: ClassifyStats, num_rules: int | None = None):
+        self.first = first
+        self.verdict_accept = verdict_accept
+        self.stats = stats
+        self._comps = comparisons
+        self._num_rules = num_rules
+        if comparisons is None and num_rules is None:
+            raise ValueError("EngineResult needs comparisons or num_rules")
+
+    @property
+    def comparisons(self) -> np.ndarray:
+        if self._comps is None:
+            f = np.asarray(self.first, dtype=np.int64)
+            self._comps = np.where(f >= 0, f + 1, self._num_rules)
+        return self._comps
+
+    def __len__(self) -> int:
+        return len(self.first)
+
+
+def _is_host_batch(packets) -> bool:
+    """Host packet batch for the e2e path: the reference's PacketArrays
+    columns as a dict of arrays, or (n, 4) uint32 records."""
+    if isinstance(packets, dict):
+        return True
+    return isinstance(packets, np.ndarray) and packets.ndim == 2 and packets.shape[1] == 4
+
+
+def _host_len(packets) -> int:
+    return len(packets["proto"]) if isinstance(packets, dict) else int(packets.shape[0])
+
+
+def _host_slice(packets, a: int, b: int):
+    if isinstance(packets, dict):
+        return {f: np.asarray(packets[f])[a:b] for f in ("proto", "src_ip", "src_port", "dst_ip", "dst_port")}
+    return packets[a:b]
+
+
+def _nvtx(name: str):
+    import torch
+    return torch.cuda.nvtx.range(name)
 
 
 class Engine:
-    """Reusable batch-synchronous runner for one EngineConfig on one GPU.
+    """Reusable batch-synchronous runner for one EngineConfig (engines.py:221-290).
 
-    Not reentrant (engines.py:221-228); rulesets are compiled once per object
-    and cached, packets are shared read-only.
+    Not reentrant (engines.py:221-228); rulesets are compiled once per
+    device and cached, packets are shared read-only.
+
+    GPUs: ``devices`` (or ``EngineConfig.gpus``, devices 0..gpus-1) -- one
+    process drives all of them, one stream per device:
+
+    * sequential / data-parallel: packets split into contiguous
+      ``partition_bounds(N, G)`` shards (engines.py:307), the ruleset
+      replicated on every device, no collective; host batches run the e2e
+      pipeline on every device at once (one host thread each).
+    * function-parallel / hybrid: the ``nodes`` rule partitions are grouped
+      into G contiguous runs, each device uploads only its run (a rule shard)
+      and scans the replicated packets against its partitions, combining
+      straight into the packet owners' result buffers with NVLink atomics
+      (the fused MIN / SUM epilogue, peer access within the process) --
+      engines.py:349-369 across devices with no separate collective.
     """
 
-    def __init__(self, config: EngineConfig, device: int | None = None) -> None:
+    def __init__(self, config: EngineConfig, device: int | None = None, devices=None) -> None:
         self.config = config
-        self.device = device
+        if devices is None:
+            if config.gpus > 1:
+                devices = list(range(config.gpus))
+            else:
+                devices = [device]
+        devices = list(devices)
+        if not devices:
+            raise ConfigError("devices must name at least one GPU")
+        if any(d is not None for d in devices):
+            _native.require_device()
+            have = _native.device_count()
+            for d in devices:
+                if d is not None and not 0 <= int(d) < have:
+                    raise ConfigError(f"GPU {d} requested but only {have} CUDA devices are visible")
+        self.devices = devices
+        self.device = devices[0]
+        self._copies: dict = {}
 
     @property
     def pool_width(self) -> int:
         return self.config.max_workers or os.cpu_count() or 1
 
+    @property
+    def gpus(self) -> int:
+        return len(self.devices)
+
     def close(self) -> None:
-        pass
+        self._copies.clear()
 
     def __enter__(self) -> "Engine":
         return self
@@ -245,9 +329,33 @@ class Engine:
     def __exit__(self, *exc) -> None:
         self.close()
 
+    def _dev(self, g: int) -> int:
+        d = self.devices[g]
+        if d is None:
+            import torch
+            _native.require_device()
+            return torch.cuda.current_device()
+        return int(d)
+
+    def _copy(self, compiled: CompiledRuleset, device: int, lo: int | None = None, hi: int | None = None):
+        """``compiled`` (or its rule shard [lo, hi)) uploaded on ``device``, cached."""
+        if lo is None and compiled.device == device:
+            return compiled
+        key = (id(compiled), device, lo, hi)
+        hit = self._copies.get(key)
+        if hit is not None and hit[0]() is compiled:
+            return hit[1]
+        if lo is None:
+            c = CompiledRuleset.from_columns(compiled.columns(), device=device)
+        else:
+            cols = {f: v[lo:hi] for f, v in compiled.columns().items()}
+            c = CompiledRuleset.from_columns(cols, device=device, shard=(lo, compiled.num_rules))
+        self._copies[key] = (weakref.ref(compiled), c)
+        return c
+
     # ------------------------------------------------------------- device
     def run_device(self, compiled: CompiledRuleset, pkts: PacketArrays, stream: int | None = None):
-        """Launch the configured model; returns device tensors
+        """Launch the configured model on one device; returns device tensors
         (first int32 [NO_MATCH = none], comps int32, stats int64 [sum, max_worker])."""
         import torch
         n = len(pkts)
@@ -272,37 +380,157 @@ class Engine:
 
     # -------------------------------------------------------------- arrays
     def run_arrays(self, ruleset, packets) -> EngineResult:
+        """The configured model over a packet batch, results as arrays.
+
+        ``packets``: a device ``PacketArrays``, a host batch (dict of the
+        reference's PacketArrays columns, or (n, 4) uint32 records -- pinned or
+        pageable numpy; the e2e pipeline copies, scans and returns results in
+        overlapped chunks) or a sequence of ``Packet``."""
         start = time.perf_counter_ns()
-        compiled = ruleset if isinstance(ruleset, CompiledRuleset) else compile_ruleset(ruleset, self.device)
+        compiled = ruleset if isinstance(ruleset, CompiledRuleset) else compile_ruleset(ruleset, self._dev(0))
         if compiled.is_shard:
             raise ValueError("Engine.run_arrays needs a whole ruleset, not a rule shard "
                              "(shards are scanned through parallel.run_function_parallel)")
-        pkts = compiled._packets(packets)
-        n = len(pkts)
+        R = compiled.num_rules
+        host = _is_host_batch(packets)
+        n = _host_len(packets) if host else len(packets)
         if n == 0:
             z = np.zeros(0, np.int64)
-            return EngineResult(z, z, np.zeros(0, np.bool_),
-                                ClassifyStats(0, 0, time.perf_counter_ns() - start, 0))
-        first, comps, stats = self.run_device(compiled, pkts)
-        first_h = first_to_host(first)
-        comps_h = comps.cpu().numpy().astype(np.int64)
-        st = stats.cpu().numpy()
+            return EngineResult(z, z, np.zeros(0, np.bool_), ClassifyStats(0, 0, time.perf_counter_ns() - start, 0))
+        model = self.config.model
+        seq = model in (ExecutionModel.SEQUENTIAL, ExecutionModel.DATA_PARALLEL)
+        if seq and host:
+            with _nvtx("Engine.run_arrays: e2e (host batch)"):
+                first, verdict, st = self._data_host(compiled, packets, n)
+            return EngineResult(first, None, verdict, ClassifyStats(int(st[0]), n, time.perf_counter_ns() - start,
+                                                                    int(st[1])), num_rules=R)
+        if host:
+            with _nvtx("Engine.run_arrays: upload"):
+                pk = packets if isinstance(packets, dict) else PacketArrays.unpack_host(packets)
+                pkts = PacketArrays.from_columns(*[pk[f] for f in ("proto", "src_ip", "src_port", "dst_ip",
+                                                                  "dst_port")], device=self._dev(0))
+        else:
+            with _nvtx("Engine.run_arrays: pack + upload"):
+                pkts = compiled._packets(packets) if self.gpus == 1 else (
+                    packets if isinstance(packets, PacketArrays) else PacketArrays.from_packets(packets, self._dev(0)))
+        if self.gpus > 1:
+            with _nvtx(f"Engine.run_arrays: {model.value} on {self.gpus} GPUs"):
+                first_h, comps_h, st = (self._data_multi(compiled, pkts) if seq
+                                        else self._function_multi(compiled, pkts))
+        else:
+            if compiled.device != pkts.device:
+                compiled = self._copy(compiled, pkts.device)
+            with _nvtx(f"Engine.run_arrays: {model.value} scan"):
+                first, comps, stats = self.run_device(compiled, pkts)
+            first_h = first_to_host(first)
+            comps_h = None if seq else comps.cpu().numpy().astype(np.int64)
+            st = stats.cpu().numpy()
         acc = np.zeros(n, dtype=np.bool_)
         hit = first_h >= 0
         acc[hit] = compiled.action_accept[first_h[hit]]
         return EngineResult(first_h, comps_h, acc,
-                            ClassifyStats(int(st[0]), n, time.perf_counter_ns() - start, int(st[1])))
+                            ClassifyStats(int(st[0]), n, time.perf_counter_ns() - start, int(st[1])), num_rules=R)
+
+    def _data_host(self, compiled, packets, n):
+        """Host batch, sequential / data-parallel: the e2e pipeline on every
+        device over its packet shard, outputs written in place."""
+        if self.gpus == 1:
+            dev = self._dev(0)
+            return self._copy(compiled, dev).classify_host(packets)
+        import torch
+        from concurrent.futures import ThreadPoolExecutor
+        first = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+        verdict = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy().view(np.bool_)
+        bounds = partition_bounds(n, self.gpus)
+        reps = [self._copy(compiled, self._dev(g)) for g in range(self.gpus)]
+
+        def shard(g):  # ctypes drops the GIL: the devices' pipelines run concurrently
+            a, b = bounds[g]
+            if b == a:
+                return np.zeros(2, np.int64)
+            return reps[g].classify_host(_host_slice(packets, a, b), out=(first[a:b], verdict[a:b]))[2]
+        with ThreadPoolExecutor(max_workers=self.gpus) as ex:
+            sts = list(ex.map(shard, range(self.gpus)))
+        return first, verdict, np.array([sum(int(x[0]) for x in sts), max(int(x[1]) for x in sts)], np.int64)
+
+    def _data_multi(self, compiled, pkts):
+        """Device batch, data-parallel over G devices: contiguous packet shards
+        (engines.py:307), replicated rules, no collective."""
+        import torch
+        bounds = partition_bounds(len(pkts), self.gpus)
+        outs = []
+        for g, (a, b) in enumerate(bounds):  # launches are asynchronous: the devices run concurrently
+            if b == a:
+                continue
+            dev = self._dev(g)
+            rep = self._copy(compiled, dev)
+            with torch.cuda.device(dev):
+                sub = PacketArrays(pkts.data[a:b].to(f"cuda:{dev}", non_blocking=True))
+                outs.append(self.run_device(rep, sub))
+        first = np.concatenate([first_to_host(f) for f, _, _ in outs])
+        st = [s.cpu().numpy() for _, _, s in outs]
+        return first, None, np.array([sum(int(x[0]) for x in st), max(int(x[1]) for x in st)], np.int64)
+
+    def _function_multi(self, compiled, pkts):
+        """Function-parallel / hybrid over G devices: device g owns a
+        contiguous run of the ``nodes`` rule partitions (its rule shard) and
+        scans the replicated packets against each of them; every scan's
+        epilogue folds its per-packet first match (atomicMin) and per-task
+        comparisons (atomicAdd) straight into the owner device's result
+        buffers over NVLink (packet owners: partition_bounds(N, G))."""
+        import ctypes
+        import torch
+        n, G, R = len(pkts), self.gpus, compiled.num_rules
+        parts = [(lo, hi) for lo, hi in partition_bounds(R, self.config.nodes) if hi > lo]
+        groups = partition_bounds(len(parts), G)
+        owners = partition_bounds(n, G)
+        devs = [self._dev(g) for g in range(G)]
+        lib = _native.lib()
+        for d in set(devs):
+            for q in set(devs):
+                if d != q:
+                    _native.check(lib.pfw_peer_enable(d, q), "pfw_peer_enable")
+        firsts = [torch.full((max(b - a, 1),), NO_MATCH, dtype=torch.int32, device=f"cuda:{d}")
+                  for (a, b), d in zip(owners, devs)]
+        comps = [torch.zeros(max(b - a, 1), dtype=torch.int32, device=f"cuda:{d}") for (a, b), d in zip(owners, devs)]
+        stats = [torch.zeros(2, dtype=torch.int64, device=f"cuda:{d}") for d in devs]
+        replicas = {}
+        for d in set(devs):
+            replicas[d] = pkts if pkts.device == d else PacketArrays(pkts.data.to(f"cuda:{d}"))
+        for d in set(devs):
+            torch.cuda.synchronize(d)  # every owner buffer is initialised before any scan writes into it
+        P = ctypes.c_void_p
+        tf = (P * G)(*[t.data_ptr() for t in firsts])
+        tc = (P * G)(*[t.data_ptr() for t in comps])
+        caps = (ctypes.c_int64 * G)(*[b - a for a, b in owners])
+        for g, (ga, gb) in enumerate(groups):
+            if gb == ga:
+                continue
+            lo_g, hi_g = parts[ga][0], parts[gb - 1][1]
+            shard = self._copy(compiled, devs[g], lo_g, hi_g)
+            st = torch.cuda.current_stream(devs[g]).cuda_stream
+            for lo, hi in parts[ga:gb]:
+                _native.check(lib.pfw_scan_fused_min(shard.handle, lo - lo_g, hi - lo_g, replicas[devs[g]].data.data_ptr(),
+                                                     n, tf, tc, caps, G, 1, stats[g].data_ptr(), st),
+                              "pfw_scan_fused_min")
+        for d in set(devs):
+            torch.cuda.synchronize(d)
+        first = np.concatenate([first_to_host(f[:b - a]) for f, (a, b) in zip(firsts, owners)])
+        comp = np.concatenate([c[:b - a].cpu().numpy() for c, (a, b) in zip(comps, owners)]).astype(np.int64)
+        st = [s.cpu().numpy() for s in stats]
+        return first, comp, np.array([sum(int(x[0]) for x in st), max(int(x[1]) for x in st)], np.int64)
 
     # ----------------------------------------------------------- drop-in
-    def run(self, ruleset: Ruleset, packets: Sequence[Packet]) -> tuple[list[MatchResult], ClassifyStats]:
+    def run(self, ruleset: Ruleset, packets: Sequence[Packet]) -> tuple[MatchResults, ClassifyStats]:
         """Classify packets under the configured model (engines.py:260-290).
-        results[i] belongs to packets[i]."""
-        if self.config.model is ExecutionModel.SEQUENTIAL:
+        results[i] belongs to packets[i]; the results are an array-backed lazy
+        sequence of MatchResult (equal to the reference's list)."""
+        if self.config.model is ExecutionModel.SEQUENTIAL and self.gpus == 1:
             return classify_batch_sequential(ruleset, packets)
         start = time.perf_counter_ns()
-        compiled = compile_ruleset(ruleset, self.device)
+        compiled = compile_ruleset(ruleset, self._dev(0))
         res = self.run_arrays(compiled, packets)
-        results = compiled.build_results(res.first, res.comparisons) if len(res.first) else []
+        results = compiled.build_results(res.first, res._comps) if len(res.first) else []
         s = res.stats
         return results, ClassifyStats(s.total_comparisons, s.packets_processed,
                                       time.perf_counter_ns() - start, s.max_worker_comparisons)

@@ -50,3 +50,20 @@ def test_no_silent_cpu_fallback():
     pk = [pfw.Packet(0, pfw.Protocol.TCP, 1, 2, 3, 4)]
     with pytest.raises(_native.NativeUnavailable):
         pfw.classify_batch_sequential(rs, pk)
+
+
+def test_non_prefix_masks_are_rejected():
+    """Masks must be CIDR prefix masks (model.py:108-114); both encodings of
+    the CIDR test are exact only for those, so anything else is refused
+    before any device work (this runs without a GPU)."""
+    import ctypes
+    import numpy as np
+    lib = _native.load()
+    cols = [np.array([6], np.uint8), np.array([0x0A000000], np.uint32), np.array([0xFF00FF00], np.uint32),
+            np.array([0], np.uint16), np.array([65535], np.uint16), np.array([0], np.uint32),
+            np.array([0], np.uint32), np.array([0], np.uint16), np.array([65535], np.uint16),
+            np.array([1], np.uint8)]
+    h = ctypes.c_void_p()
+    rc = lib.pfw_ruleset_create(0, 1, *[c.ctypes.data for c in cols], ctypes.byref(h))
+    assert rc == _native.PFW_ERR_INVALID
+    assert "not a prefix mask" in _native.last_error()

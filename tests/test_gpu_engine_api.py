@@ -1,0 +1,122 @@
+"""The drop-in Engine API beyond one device and one layout:
+host batches through the e2e pipeline (pinned and pageable numpy, columns and
+records), the lazy MatchResult sequence, and one Engine driving several
+devices (``devices=`` / ``EngineConfig.gpus``) -- all bit-exact against the
+reference's golden results.
+
+Several-device runs use the same device listed more than once where only
+one GPU is visible: the shard / owner / fused-combine logic is identical
+(peer pointers are then local), so this checks it on any box; the
+``device_count() >= 2`` tests (tests/test_gpu_multidevice.py) cover real
+NVLink peers."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_rules, golden_traffic
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1312_4188_b200 as pfw  # noqa: E402
+from paper_1312_4188_b200 import _native  # noqa: E402
+from paper_1312_4188_b200.classifier import MatchResults  # noqa: E402
+from oracle import oracle  # noqa: E402
+from oracle.oracle import PKT_FIELDS  # noqa: E402
+
+
+def _pinned(cols):
+    out = {}
+    for f in PKT_FIELDS:
+        a = np.ascontiguousarray(cols[f])
+        t = torch.empty(a.shape, dtype={1: torch.uint8, 2: torch.int16, 4: torch.int32}[a.itemsize], pin_memory=True)
+        t.numpy().view(a.dtype)[:] = a
+        out[f] = t.numpy().view(a.dtype)
+    return out
+
+
+@pytest.mark.parametrize("layout", ["pageable", "pinned", "records"])
+def test_run_arrays_host_batch_equals_golden(layout):
+    g = golden("scan_oracle_r1000_t100000.npz")
+    c = pfw.CompiledRuleset.from_columns(golden_rules("r1000_s1"), device=0)
+    pk = golden_traffic("t100000_s2")
+    if layout == "pinned":
+        pk = _pinned(pk)
+    elif layout == "records":
+        pk = pfw.PacketArrays.pack_host(*[pk[f] for f in PKT_FIELDS])
+    eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.DATA_PARALLEL))
+    for _ in range(2):  # second call reuses the staging ring and pinned outputs
+        res = eng.run_arrays(c, pk)
+        np.testing.assert_array_equal(res.first, g["first"])
+        np.testing.assert_array_equal(res.verdict_accept, g["verdict"])
+        assert res.stats.total_comparisons == int(g["total_comparisons"]) == int(res.comparisons.sum())
+        assert res.stats.max_worker_comparisons == int(g["max_worker_comparisons"])
+
+
+def test_host_batch_staging_large_pageable():
+    # several chunks, pageable in and out: staged through the pinned ring
+    rules = oracle.gen_ruleset(1000, 1)
+    c = pfw.CompiledRuleset.from_columns(rules, device=0)
+    n = 3 << 20
+    pk = oracle.gen_traffic_uniform(n, 77)
+    want = oracle.scan_range(rules, pk, 0, 1000)
+    f, v, st = c.classify_host(pk, chunk=1 << 18)
+    np.testing.assert_array_equal(f, want)
+    np.testing.assert_array_equal(v, np.where(want >= 0, rules["action_accept"][np.maximum(want, 0)], False))
+    out_f = np.empty(n, np.int32)  # pageable outputs too
+    out_v = np.empty(n, np.uint8)
+    c.classify_host(pk, chunk=1 << 18, out=(out_f, out_v))
+    np.testing.assert_array_equal(out_f, want)
+
+
+def test_lazy_match_results_equal_reference_list():
+    rs = pfw.generate_ruleset(pfw.RulesetGenParams(170, seed=29, wildcard_probability=0.3))
+    packets = pfw.generate_traffic(pfw.TrafficProfile(count=350, seed=30))
+    for model in ("sequential", "data", "function", "hybrid"):
+        results, _ = pfw.run(rs, packets, pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=3))
+        assert isinstance(results, MatchResults)
+        eager = [pfw.classify(rs, p) for p in packets[:20]]
+        if model in ("sequential", "data"):
+            assert results[:20] == eager  # MatchResult objects made on access
+        assert len(results) == 350 and results[-1] == list(results)[-1]
+        assert results == results.tolist()
+
+
+@pytest.mark.parametrize("model", ["data", "function", "hybrid"])
+def test_engine_on_several_devices_equals_golden(model):
+    g = golden("engine_r503_t600.npz")
+    c = pfw.CompiledRuleset.from_columns(golden_rules("r503_s24_w30"), device=0)
+    cols = golden_traffic("t600_s25")
+    p = pfw.PacketArrays.from_columns(*[cols[f] for f in PKT_FIELDS], device=0)
+    for nodes in (1, 3, 8, 64):
+        for devices in ([0, 0], [0, 0, 0]):
+            eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=nodes), devices=devices)
+            for batch in (p, cols):
+                res = eng.run_arrays(c, batch)
+                key = f"{model}_{nodes}"
+                np.testing.assert_array_equal(res.first, g[f"{key}_first"])
+                np.testing.assert_array_equal(res.comparisons, g[f"{key}_comps"])
+                s = res.stats
+                assert [s.total_comparisons, s.max_worker_comparisons, s.packets_processed] == \
+                    g[f"{key}_stats"].tolist()
+
+
+def test_function_parallel_100k_rules_on_several_devices():
+    g = golden("engine_r100000_t2000.npz")
+    c = pfw.CompiledRuleset.from_columns(golden_rules("r100000_s1"), device=0)
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=2000, seed=2), device=0)
+    for nodes in (2, 8):
+        eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=nodes), devices=[0, 0])
+        res = eng.run_arrays(c, p)
+        np.testing.assert_array_equal(res.first, g[f"function_{nodes}_first"])
+        np.testing.assert_array_equal(res.comparisons, g[f"function_{nodes}_comps"])
+
+
+def test_gpus_beyond_visible_devices_is_config_error():
+    have = _native.device_count()
+    with pytest.raises(pfw.ConfigError, match="CUDA devices are visible"):
+        pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.DATA_PARALLEL, gpus=have + 1))

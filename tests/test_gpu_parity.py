@@ -494,6 +494,28 @@ def test_scan_range_columns_device_and_host():
     assert st.tolist() == [int(comps.sum()), int(comps.max())]
 
 
+def test_e2e_mixed_protocol_rule_scan_large_chunks():
+    """The e2e pipeline runs consecutive chunks on two compute streams; with
+    the rule-by-rule scan each chunk >= bucket_min is grouped by protocol
+    first.  Each stream has its own bucket scratch, so mixed-protocol chunks
+    scanned concurrently never see each other's buckets (9Mi packets,
+    protocols shuffled)."""
+    _native.set_tuning("algo", 1)
+    rules = oracle.gen_ruleset(1000, 1)
+    n = 9 << 20
+    parts = [oracle.gen_traffic_uniform(n // 3, 31 + k, proto=pr) for k, pr in enumerate((6, 17, 1))]
+    perm = np.random.default_rng(5).permutation(n)
+    pk = {f: np.concatenate([q[f] for q in parts])[perm] for f in PKT_FIELDS}
+    c = compiled(rules)
+    want = oracle.scan_range(rules, pk, 0, 1000)
+    for split in (0, 1):
+        _native.set_tuning("proto_split", split)
+        f, v, st = c.classify_host_columns(pk)
+        np.testing.assert_array_equal(f, want)
+    comps = oracle.sequential_comparisons(want, 1000)
+    assert st.tolist() == [int(comps.sum()), int(comps.max())]
+
+
 # --------------------------------------------- protocol-uniform tile fast path
 
 @pytest.mark.parametrize("proto", [1, 6, 17, 47, 0, 255])
