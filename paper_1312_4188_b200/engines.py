@@ -337,11 +337,14 @@ class Engine:
             return torch.cuda.current_device()
         return int(d)
 
-    def _copy(self, compiled: CompiledRuleset, device: int, lo: int | None = None, hi: int | None = None):
-        """``compiled`` (or its rule shard [lo, hi)) uploaded on ``device``, cached."""
-        if lo is None and compiled.device == device:
+    def _copy(self, compiled: CompiledRuleset, device: int, lo: int | None = None, hi: int | None = None,
+              slot: int = 0):
+        """``compiled`` (or its rule shard [lo, hi)) uploaded on ``device``, cached.
+        ``slot`` > 0 asks for a separate handle (handles are not reentrant: host
+        threads driving the same device concurrently each need their own)."""
+        if lo is None and compiled.device == device and slot == 0:
             return compiled
-        key = (id(compiled), device, lo, hi)
+        key = (id(compiled), device, lo, hi, slot)
         hit = self._copies.get(key)
         if hit is not None and hit[0]() is compiled:
             return hit[1]
@@ -442,7 +445,8 @@ class Engine:
         first = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
         verdict = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy().view(np.bool_)
         bounds = partition_bounds(n, self.gpus)
-        reps = [self._copy(compiled, self._dev(g)) for g in range(self.gpus)]
+        devs = [self._dev(g) for g in range(self.gpus)]
+        reps = [self._copy(compiled, d, slot=devs[:g].count(d)) for g, d in enumerate(devs)]
 
         def shard(g):  # ctypes drops the GIL: the devices' pipelines run concurrently
             a, b = bounds[g]

@@ -135,6 +135,9 @@ def test_bench_two_ranks_shared_gpu(config):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
     if config == "data":
-        assert d["scaling"] == "weak" and d["config"]["packets"] == 2 << 20 and d["e2e"]["value"] > 0
+        # strong by default (BASELINE configs[1]: the packets split over the ranks) + the weak record
+        assert d["scaling"] == "strong" and d["config"]["packets"] == 1 << 20 and d["e2e"]["value"] > 0
+        assert d["config"]["packets_per_gpu"] == 1 << 19
+        assert d["weak"]["packets"] == 2 << 20 and d["weak"]["value"] > 0
     else:
         assert d["config"]["rules_per_gpu"] == [0, 50_000]
