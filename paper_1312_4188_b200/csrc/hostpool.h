@@ -54,6 +54,30 @@ class HostPool {
         });
     }
 
+    // several copies as ONE job: every copy cut into pieces of at most ~2 MB,
+    // all pieces spread over the pool (one wake-up per batch of columns)
+    struct Copy {
+        void *dst;
+        const void *src;
+        size_t bytes;
+    };
+    void copy_many(const Copy *c, int nc) {
+        constexpr size_t PIECE = 2u << 20;
+        size_t total = 0;
+        for (int i = 0; i < nc; i++) total += c[i].bytes;
+        if (total == 0) return;
+        std::vector<Copy> pieces;
+        for (int i = 0; i < nc; i++)
+            for (size_t a = 0; a < c[i].bytes; a += PIECE)
+                pieces.push_back(Copy{static_cast<char *>(c[i].dst) + a, static_cast<const char *>(c[i].src) + a,
+                                      std::min(PIECE, c[i].bytes - a)});
+        if (pieces.size() == 1 || threads() == 0) {
+            for (const Copy &p : pieces) memcpy(p.dst, p.src, p.bytes);
+            return;
+        }
+        run((int)pieces.size(), [&](int i) { memcpy(pieces[(size_t)i].dst, pieces[(size_t)i].src, pieces[(size_t)i].bytes); });
+    }
+
     ~HostPool() {
         {
             std::lock_guard<std::mutex> l(mu_);

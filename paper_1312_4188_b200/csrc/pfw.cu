@@ -41,7 +41,8 @@
 
 #include "../../include/pfw.h"
 #include <nvtx3/nvToolsExt.h>
-#include "hostpool.h"  // header-only NVTX v3: ranges cost nothing unless a tool is attached
+#include "hostpool.h"
+#include <chrono>  // header-only NVTX v3: ranges cost nothing unless a tool is attached
 
 #define PFW_VERSION "0.2.0"
 
@@ -1419,6 +1420,11 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");
         g_ms_group = (int)value;
+    } else if (!strcmp(key, "ms_lean")) {
+        if (value < 0 || value > 3)
+            return set_err(PFW_ERR_INVALID, "ms_lean: 0 general kernel, 1 lean (8-lane groups), 2 lean (4-lane "
+                                            "groups, 256-bit loads), 3 auto");
+        g_ms_lean = (int)value;
     } else {
         return set_err(PFW_ERR_INVALID, "unknown tuning key '%s'", key);
     }
@@ -1797,6 +1803,10 @@ int pfw_combine_min(const uint32_t *d_rows, int64_t rows, int64_t n, uint32_t *d
 // Host buffers the DMA engines can read / write directly (pinned or
 // registered, or managed); anything else is pageable and goes through the
 // handle's pinned staging ring.
+static double host_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static bool host_is_pinned(const void *p) {
     if (!p) return true;
     cudaPointerAttributes a{};
@@ -1919,6 +1929,10 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     // first at 16*chunk, verdict at 20*chunk
     const size_t in_off[5] = {0, (size_t)chunk * 4, (size_t)chunk * 8, (size_t)chunk * 10, (size_t)chunk * 12};
     int64_t drained = 0;  // chunks whose staged results have been copied out
+    // PFW_E2E_TRACE=1: per-call host-side timing of the staging path (stderr)
+    static const bool trace = getenv("PFW_E2E_TRACE") != nullptr;
+    double t_wait = 0.0, t_copy = 0.0;
+    const double t_call = trace ? host_seconds() : 0.0;
     auto drain = [&](int64_t upto) -> cudaError_t {  // copy staged results of chunks < upto out
         for (; drained < upto; drained++) {
             const int sl = (int)(drained % S);
@@ -1926,8 +1940,11 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
             if (e != cudaSuccess) return e;
             const int64_t c0 = starts[(size_t)drained], m = sizes[(size_t)drained];
             char *base = hs + sl * slot;
-            if (stage_first) pool.copy(h_first + c0, base + (size_t)chunk * 16, (size_t)m * 4);
-            if (stage_verd) pool.copy(h_verdict + c0, base + (size_t)chunk * 20, (size_t)m);
+            HostPool::Copy cps[2];
+            int ncp = 0;
+            if (stage_first) cps[ncp++] = HostPool::Copy{h_first + c0, base + (size_t)chunk * 16, (size_t)m * 4};
+            if (stage_verd) cps[ncp++] = HostPool::Copy{h_verdict + c0, base + (size_t)chunk * 20, (size_t)m};
+            pool.copy_many(cps, ncp);
         }
         return cudaSuccess;
     };
@@ -1959,11 +1976,21 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
         if (any_in) {
             // the staging slot's previous H2D (chunk k - S) must have read it
+            const double tw0 = trace ? host_seconds() : 0.0;
             if (k >= S) E2E_TRY(cudaEventSynchronize(ev_in[sl]));
+            const double tw1 = trace ? host_seconds() : 0.0;
+            HostPool::Copy cps[5];
+            int ncp = 0;
             for (int i = 0; i < nin; i++)
                 if (stage_in[i])
-                    pool.copy(sbase + in_off[i], static_cast<const char *>(in_ptr[i]) + (size_t)c0 * in_w[i],
-                              (size_t)m * in_w[i]);
+                    cps[ncp++] = HostPool::Copy{sbase + in_off[i],
+                                                static_cast<const char *>(in_ptr[i]) + (size_t)c0 * in_w[i],
+                                                (size_t)m * in_w[i]};
+            pool.copy_many(cps, ncp);
+            if (trace) {
+                t_wait += tw1 - tw0;
+                t_copy += host_seconds() - tw1;
+            }
         }
         bool fail = false;
         for (int i = 0; i < nin; i++) {
@@ -2012,6 +2039,11 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         if (e != cudaSuccess) return set_err(PFW_ERR_CUDA, "staged copy-out failed: %s", cudaGetErrorString(e));
     }
     if (h_stats) CUDA_TRY(cudaMemcpy(h_stats, d_stats, 16, cudaMemcpyDeviceToHost));
+    if (trace)
+        fprintf(stderr, "pfw e2e: n=%lld chunks=%lld stage_in=%d stage_out=%d call %.2f ms, slot waits %.2f ms, "
+                        "staging copies %.2f ms (%d pool threads)\n", (long long)n, (long long)nchunks, (int)any_in,
+                (int)(stage_first || stage_verd), (host_seconds() - t_call) * 1e3, t_wait * 1e3, t_copy * 1e3,
+                pool.threads());
     return PFW_OK;
 }
 

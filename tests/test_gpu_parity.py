@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2)):
+                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3)):
         _native.set_tuning(k, v)
 
 
@@ -626,6 +626,38 @@ def test_match_set_step_shapes(group, words):
     test_ragged_sizes_and_empty()
     test_adversarial_recipe_sample()
     test_fused_min_combine_virtual_ranks(0)
+
+
+@pytest.mark.parametrize("lean", [0, 1, 2])
+def test_lean_whole_table_scan(lean):
+    """Whole-table scans over plain rows: the general kernel (0), the lean one
+    (1) and the lean one with L1 no-allocate row loads (2) are bit-exact
+    against the reference goldens, ragged batches and the full-size data
+    config's strided oracle sample."""
+    _native.set_tuning("algo", 2)
+    _native.set_tuning("ms_compress", 0)
+    _native.set_tuning("ms_lean", lean)
+    for name, rn, tn in (("oracle_r1000_t100000", "r1000_s1", "t100000_s2"), ("r2048_t1000", "r2048_s21_w15", "t1000_s22"),
+                         ("r300_t10000", "r300_s40_w30", "t10000_s41"), ("r64_t600", "r64_s30_w40", "t600_s25"),
+                         ("r1000_t3000icmp", "r1000_s1", "t3000_s11_icmp")):
+        test_scan_matches_reference_golden(name, rn, tn)
+    test_ragged_sizes_and_empty()
+    test_engine_models_match_reference_golden("data")
+    rules = golden_rules("r10000_s1")
+    c = compiled(rules)
+    n = 1 << 22
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=2), device=0)
+    comps = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    verdict = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+    first = first_to_host(c.scan_range_device(p, 0, 10_000, comps=comps, verdict=verdict, stats=stats))
+    idx = np.arange(0, n, 97)
+    sub = {f: v[idx] for f, v in p.columns().items()}
+    want = oracle.scan_range(rules, sub, 0, 10_000)
+    np.testing.assert_array_equal(first[idx], want)
+    cc = comps.cpu().numpy().astype(np.int64)
+    np.testing.assert_array_equal(cc, np.where(first >= 0, first + 1, 10_000))
+    assert stats.cpu().tolist() == [int(cc.sum()), int(cc.max())]
 
 
 def test_match_set_budget_falls_back_to_rule_scan():
