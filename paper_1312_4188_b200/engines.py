@@ -49,6 +49,7 @@ __all__ = [
 
 MAX_NODES = 512  # engines.py:59-61
 _EXECUTORS = ("process", "thread", "serial")
+_SHARDS = ("auto", "packets", "rules")
 
 
 class ConfigError(ValueError):
@@ -81,7 +82,13 @@ class EngineConfig:
     ``nodes``: packet chunks (data), rule partitions (function) or rule lanes
     (hybrid); it defines the function/hybrid comparison counters.
     ``gpus``: how many GPUs the Engine shards over (results and counters do
-    not depend on it).
+    not depend on it).  ``shard``: how the function-parallel / hybrid models
+    use them -- "rules" gives each GPU a contiguous run of the ``nodes``
+    partitions (the model's own decomposition, combined by the fused NVLink
+    MIN / SUM), "packets" gives each GPU a packet shard and the whole
+    partition loop (no combine; the model's speculative per-partition work
+    then stays per GPU instead of growing with the GPU count); "auto" picks
+    packets.  Results and counters are identical.
     ``batch_size``/``executor``/``max_workers`` are validated as in the
     reference and otherwise ignored (the GPU replaces the pool).
     """
@@ -92,10 +99,13 @@ class EngineConfig:
     executor: str = "process"
     max_workers: int | None = None
     gpus: int = 1  # GPUs one Engine drives (packet shards / rule shards; see Engine)
+    shard: str = "auto"  # function / hybrid over several GPUs: "rules", "packets" or "auto" (= packets)
 
     def __post_init__(self) -> None:
         if not 1 <= self.gpus <= 64:
             raise ConfigError(f"gpus must be within 1..64, got {self.gpus}")
+        if self.shard not in _SHARDS:
+            raise ConfigError(f"shard must be one of {_SHARDS}, got {self.shard!r}")
         if not 1 <= self.nodes <= MAX_NODES:
             raise ConfigError(f"nodes must be within 1..{MAX_NODES}, got {self.nodes}")
         if self.batch_size < 1:
@@ -284,12 +294,14 @@ class Engine:
       ``partition_bounds(N, G)`` shards (engines.py:307), the ruleset
       replicated on every device, no collective; host batches run the e2e
       pipeline on every device at once (one host thread each).
-    * function-parallel / hybrid: the ``nodes`` rule partitions are grouped
-      into G contiguous runs, each device uploads only its run (a rule shard)
-      and scans the replicated packets against its partitions, combining
-      straight into the packet owners' result buffers with NVLink atomics
-      (the fused MIN / SUM epilogue, peer access within the process) --
-      engines.py:349-369 across devices with no separate collective.
+    * function-parallel / hybrid, shard="rules": the ``nodes`` rule
+      partitions are grouped into G contiguous runs, each device uploads
+      only its run (a rule shard) and scans the replicated packets against
+      its partitions, combining straight into the packet owners' result
+      buffers with NVLink atomics (the fused MIN / SUM epilogue, peer access
+      within the process) -- engines.py:349-369 across devices with no
+      separate collective.  shard="packets" (and "auto"): packet shards as
+      for data-parallel, each device running all partitions.
     """
 
     def __init__(self, config: EngineConfig, device: int | None = None, devices=None) -> None:
@@ -418,8 +430,9 @@ class Engine:
                     packets if isinstance(packets, PacketArrays) else PacketArrays.from_packets(packets, self._dev(0)))
         if self.gpus > 1:
             with _nvtx(f"Engine.run_arrays: {model.value} on {self.gpus} GPUs"):
-                first_h, comps_h, st = (self._data_multi(compiled, pkts) if seq
-                                        else self._function_multi(compiled, pkts))
+                by_rules = not seq and self.config.shard == "rules"
+                first_h, comps_h, st = (self._function_multi(compiled, pkts) if by_rules
+                                        else self._data_multi(compiled, pkts, with_comps=not seq))
         else:
             if compiled.device != pkts.device:
                 compiled = self._copy(compiled, pkts.device)
@@ -457,9 +470,11 @@ class Engine:
             sts = list(ex.map(shard, range(self.gpus)))
         return first, verdict, np.array([sum(int(x[0]) for x in sts), max(int(x[1]) for x in sts)], np.int64)
 
-    def _data_multi(self, compiled, pkts):
-        """Device batch, data-parallel over G devices: contiguous packet shards
-        (engines.py:307), replicated rules, no collective."""
+    def _data_multi(self, compiled, pkts, with_comps: bool = False):
+        """Device batch over G devices as contiguous packet shards
+        (engines.py:307), replicated rules, no collective: the data-parallel
+        model, or any model with shard="packets" (each device runs the
+        model's whole launch sequence on its shard)."""
         import torch
         bounds = partition_bounds(len(pkts), self.gpus)
         outs = []
@@ -472,8 +487,9 @@ class Engine:
                 sub = PacketArrays(pkts.data[a:b].to(f"cuda:{dev}", non_blocking=True))
                 outs.append(self.run_device(rep, sub))
         first = np.concatenate([first_to_host(f) for f, _, _ in outs])
+        comps = np.concatenate([c.cpu().numpy() for _, c, _ in outs]).astype(np.int64) if with_comps else None
         st = [s.cpu().numpy() for _, _, s in outs]
-        return first, None, np.array([sum(int(x[0]) for x in st), max(int(x[1]) for x in st)], np.int64)
+        return first, comps, np.array([sum(int(x[0]) for x in st), max(int(x[1]) for x in st)], np.int64)
 
     def _function_multi(self, compiled, pkts):
         """Function-parallel / hybrid over G devices: device g owns a

@@ -93,8 +93,9 @@ def test_engine_on_several_devices_equals_golden(model):
     cols = golden_traffic("t600_s25")
     p = pfw.PacketArrays.from_columns(*[cols[f] for f in PKT_FIELDS], device=0)
     for nodes in (1, 3, 8, 64):
-        for devices in ([0, 0], [0, 0, 0]):
-            eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=nodes), devices=devices)
+        for devices, shard in (([0, 0], "rules"), ([0, 0, 0], "rules"), ([0, 0], "packets"), ([0, 0, 0], "auto")):
+            eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=nodes, shard=shard),
+                             devices=devices)
             for batch in (p, cols):
                 res = eng.run_arrays(c, batch)
                 key = f"{model}_{nodes}"
@@ -109,8 +110,9 @@ def test_function_parallel_100k_rules_on_several_devices():
     g = golden("engine_r100000_t2000.npz")
     c = pfw.CompiledRuleset.from_columns(golden_rules("r100000_s1"), device=0)
     p = pfw.generate_traffic_device(pfw.TrafficProfile(count=2000, seed=2), device=0)
-    for nodes in (2, 8):
-        eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=nodes), devices=[0, 0])
+    for nodes, shard in ((2, "rules"), (8, "rules"), (8, "packets")):
+        eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.FUNCTION_PARALLEL, nodes=nodes, shard=shard),
+                         devices=[0, 0])
         res = eng.run_arrays(c, p)
         np.testing.assert_array_equal(res.first, g[f"function_{nodes}_first"])
         np.testing.assert_array_equal(res.comparisons, g[f"function_{nodes}_comps"])

@@ -119,12 +119,13 @@ def test_engine_drives_two_devices(model):
     c = pfw.CompiledRuleset.from_columns(golden_rules("r503_s24_w30"), device=0)
     cols = golden_traffic("t600_s25")
     p = pfw.PacketArrays.from_columns(*[cols[f] for f in PKT_FIELDS], device=0)
-    eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=8, gpus=2))
-    assert eng.devices == [0, 1]
-    for batch in (p, cols):
-        res = eng.run_arrays(c, batch)
-        np.testing.assert_array_equal(res.first, g[f"{model}_8_first"])
-        np.testing.assert_array_equal(res.comparisons, g[f"{model}_8_comps"])
+    for shard in ("rules", "packets"):
+        eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=8, gpus=2, shard=shard))
+        assert eng.devices == [0, 1]
+        for batch in (p, cols):
+            res = eng.run_arrays(c, batch)
+            np.testing.assert_array_equal(res.first, g[f"{model}_8_first"])
+            np.testing.assert_array_equal(res.comparisons, g[f"{model}_8_comps"])
 
 
 def test_bench_spawns_nccl_ranks():

@@ -159,6 +159,11 @@ def test_config_validation():
         EngineConfig(model=ExecutionModel.HYBRID, executor="gpu")
     with pytest.raises(ConfigError):
         EngineConfig(model=ExecutionModel.HYBRID, max_workers=0)
+    with pytest.raises(ConfigError, match="gpus"):
+        EngineConfig(model=ExecutionModel.HYBRID, gpus=0)
+    with pytest.raises(ConfigError, match="shard"):
+        EngineConfig(model=ExecutionModel.HYBRID, shard="nodes")
+    assert EngineConfig(model=ExecutionModel.FUNCTION_PARALLEL, gpus=8, shard="rules").gpus == 8
     with pytest.raises(ConfigError):
         ExecutionModel.from_key("quantum")
     assert ExecutionModel.from_key("hybrid") is ExecutionModel.HYBRID
