@@ -54,6 +54,7 @@ constexpr int64_t MS_CMP_MIN_RULES = 24576;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
+int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
 
 struct MsBuildArgs {
@@ -1181,6 +1182,14 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     }
     MatchSet *m = new MatchSet();
     m->wp = (((n + 31) / 32 + 127) / 128) * 128;  // whole 4-word-per-lane steps
+    if (g_ms_odd_rows && !(g_ms_compress == 1)) {
+        // rows an odd number of 128-byte lines long: the rows' leading lines
+        // (where most scans end) then spread over every L2 slice-hash pattern
+        // instead of only multiples of 512 bytes; shapes whose step does not
+        // divide the row scan with the window masks
+        m->wp = (((n + 31) / 32 + 31) / 32) * 32;
+        if ((m->wp / 32) % 2 == 0) m->wp += 32;
+    }
     m->sp_rows = (int64_t)bsp.size();
     m->rows[MSD_SRC] = (int64_t)bs.size();
     m->rows[MSD_DST] = (int64_t)bd.size();
@@ -1399,7 +1408,9 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     void (*kern)(ScanParams, MsView, MsNoSum) = nullptr;
     void (*kern_s)(ScanParams, MsView, MsSum) = nullptr;
     void (*kern_c)(ScanParams, MsView, MsCmp) = nullptr;
-    const bool win = !(p.lo == 0 && p.hi == h->n);
+    // (rows not a whole number of steps long: mask the last step's words)
+    const bool win = !(p.lo == 0 && p.hi == h->n) ||
+                     (m->wp % ((int64_t)(g_ms_group ? g_ms_group : (h->n > 16384 && !m->cmp ? 16 : 8)) * g_ms_words)) != 0;
     // auto: 8 lanes (4 packets in flight, 1024-rule steps) while the rows'
     // leading lines fit in L2; 16 lanes (2048-rule steps, fewer iterations)
     // for large plain rulesets whose scans run long and mostly miss L2

@@ -1420,6 +1420,8 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");
         g_ms_group = (int)value;
+    } else if (!strcmp(key, "ms_odd_rows")) {
+        g_ms_odd_rows = value != 0;
     } else if (!strcmp(key, "ms_lean")) {
         if (value < 0 || value > 3)
             return set_err(PFW_ERR_INVALID, "ms_lean: 0 general kernel, 1 lean (8-lane groups), 2 lean (4-lane "
