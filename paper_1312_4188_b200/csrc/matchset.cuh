@@ -54,6 +54,7 @@ constexpr int64_t MS_CMP_MIN_RULES = 24576;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
+int g_ms_prefetch = 0;         // lean kernel over 16-byte records: cp.async pipeline of packets + lookup entries (measured 3-4% slower: off)
 int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
 
@@ -403,12 +404,12 @@ __global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_
             v[k] = make_uint4(0u, 0u, 0u, 0u);
             if (i < n) {
                 if (p.pkts) {
-                    v[k] = __ldg(p.pkts + i);
+                    v[k] = __ldcs(p.pkts + i);  // streamed once: evict-first in L2 (the tables stay)
                 } else {
-                    v[k].x = __ldg(p.cols.src + i);
-                    v[k].y = __ldg(p.cols.dst + i);
-                    v[k].z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
-                    v[k].w = __ldg(p.cols.proto + i);
+                    v[k].x = __ldcs(p.cols.src + i);
+                    v[k].y = __ldcs(p.cols.dst + i);
+                    v[k].z = ((uint32_t)__ldcs(p.cols.sport + i) << 16) | (uint32_t)__ldcs(p.cols.dport + i);
+                    v[k].w = __ldcs(p.cols.proto + i);
                 }
             }
         }
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_
             if (i < n) {
                 const uint32_t res = s_res[warp][k * 32 + lane];
                 PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
-                emit_result<MODE>(p, (uint32_t)i, res, span, st_sum, st_max);
+                emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
             }
         }
         __syncwarp();
@@ -813,13 +814,41 @@ __device__ __forceinline__ void ms_load_rows(const uint32_t *a, const uint32_t *
 //  * G = 4: each lane loads 32 bytes per row (256-bit loads), so one load
 //    instruction per row serves 8 packets per warp (8 steps per iteration).
 // Results are identical (same lowest set bit of the same AND).
-template <int MODE, int G>
+// cp.async (LDGSTS) helpers: global -> shared without registers
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Lookup-table entries of one packet, gathered by cp.async one batch ahead
+struct MsLk {
+    uint2 ipc[2];    // src / dst: [first, end) boundary index of the packet's /16 block
+    uint32_t port[2];  // sport / dport -> interval
+};
+
+template <int MODE, int G, bool PF>
 __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
     ms_lean_kernel(ScanParams p, MsView t, uint32_t zoff) {
     constexpr int V = 32 / G, P = 32 / G;
     constexpr uint32_t STEP = 32;  // words per step (one line per row)
     __shared__ uint4 s_off[MS_BLOCK / 32][32];
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];
+    // PF (16-byte records): a two-batch software pipeline of async copies --
+    // while batch j's step loop runs, the packets of batch j+2 and the lookup
+    // table entries of batch j+1 land in shared memory, so a batch's lookup
+    // phase waits only for the (rare) boundary search
+    __shared__ uint4 s_pk[PF ? MS_BLOCK / 32 : 1][PF ? 2 : 1][32];
+    __shared__ MsLk s_lk[PF ? MS_BLOCK / 32 : 1][PF ? 2 : 1][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const uint32_t lv = (uint32_t)gl * V;
@@ -835,28 +864,84 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
     unsigned long long st_sum = 0;
     unsigned st_max = 0;
 
-    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
+    // PF: gather batch jb's lookup entries (its packets already in s_pk[.][buf])
+    auto issue_lookups = [&](int64_t bb, int buf) {
+        if (bb + lane < n) {
+            const uint4 v = s_pk[PF ? warp : 0][PF ? buf : 0][lane];
+            MsLk *d = &s_lk[PF ? warp : 0][PF ? buf : 0][lane];
+            cp_async8(&d->ipc[0], t.ipc[0] + (v.x >> 16));
+            cp_async8(&d->ipc[1], t.ipc[1] + (v.y >> 16));
+            cp_async4(&d->port[0], t.port[0] + (v.z >> 16));
+            cp_async4(&d->port[1], t.port[1] + (v.z & 0xFFFFu));
+        }
+    };
+    auto issue_packets = [&](int64_t bb, int buf) {
+        if (bb + lane < n) cp_async16(&s_pk[PF ? warp : 0][PF ? buf : 0][lane], p.pkts + bb + lane);
+    };
+    if (PF) {  // prologue: packets of the first two batches, lookups of the first
+        issue_packets(gw * 32, 0);
+        issue_packets(gw * 32 + nw * 32, 1);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        issue_lookups(gw * 32, 0);
+        cp_async_commit();
+    }
+    int buf = 0;
+    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32, buf ^= 1) {
         const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
         const int64_t i = b0 + lane;
+        if (PF) {
+            cp_async_wait_all();
+            __syncwarp();
+        }
         if (i < n) {
             uint4 v;
-            if (p.pkts) {
-                v = __ldg(p.pkts + i);
+            uint4 r;
+            if (PF) {
+                v = s_pk[PF ? warp : 0][PF ? buf : 0][lane];
+                const MsLk lk = s_lk[PF ? warp : 0][PF ? buf : 0][lane];
+                uint32_t rr[2];
+#pragma unroll
+                for (int d = 0; d < 2; d++) {  // ms_ip_row with the /16 entry already here
+                    const uint32_t ip = d ? v.y : v.x;
+                    uint32_t lo = lk.ipc[d].x, hi = lk.ipc[d].y;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (__ldg(t.ipb[d] + mid) <= ip) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    rr[d] = lo - 1;
+                }
+                r = make_uint4(rr[0], rr[1], (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + lk.port[0],
+                               lk.port[1]);
             } else {
-                v.x = __ldg(p.cols.src + i);
-                v.y = __ldg(p.cols.dst + i);
-                v.z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
-                v.w = __ldg(p.cols.proto + i);
+                if (p.pkts) {
+                    v = __ldcs(p.pkts + i);  // streamed once: evict-first in L2 (the tables stay)
+                } else {
+                    v.x = __ldcs(p.cols.src + i);
+                    v.y = __ldcs(p.cols.dst + i);
+                    v.z = ((uint32_t)__ldcs(p.cols.sport + i) << 16) | (uint32_t)__ldcs(p.cols.dport + i);
+                    v.w = __ldcs(p.cols.proto + i);
+                }
+                r = make_uint4(
+                    ms_ip_row(t.ipb[0], t.ipc[0], v.x), ms_ip_row(t.ipb[1], t.ipc[1], v.y),
+                    (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
+                    __ldg(t.port[1] + (v.z & 0xFFFFu)));
             }
-            const uint4 r = make_uint4(
-                ms_ip_row(t.ipb[0], t.ipc[0], v.x), ms_ip_row(t.ipb[1], t.ipc[1], v.y),
-                (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
-                __ldg(t.port[1] + (v.z & 0xFFFFu)));
             PFW_CHECK(r.x < t.nrows[0] && r.y < t.nrows[1] && r.z < t.nrows[2] && r.w < t.nrows[3]);
             s_off[warp][lane] = make_uint4(r.x * wp + t.off[0], r.y * wp + t.off[1], r.z * wp + t.off[2],
                                            r.w * wp + t.off[3]);
         }
         s_res[warp][lane] = PFW_NO_MATCH;
+        if (PF) {
+            // next batch's lookups (its packets landed with the wait above),
+            // then the batch after next's packets into the buffer just read
+            __syncwarp();
+            issue_lookups(b0 + nw * 32, buf ^ 1);
+            issue_packets(b0 + 2 * nw * 32, buf);
+            cp_async_commit();
+        }
         __syncwarp();
         if (nsteps > 0) {
             // group state: packet pj of the batch (-1: idle, reading the zero
@@ -916,7 +1001,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
         if (i < n) {
             const uint32_t res = s_res[warp][lane];
             PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
-            emit_result<MODE>(p, (uint32_t)i, res, span, st_sum, st_max);
+            emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
         }
         __syncwarp();
     }
@@ -1446,7 +1531,9 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     // general kernel is kept there)
     const int lean = g_ms_lean == 3 ? (h->n <= 8192 ? 2 : 0) : g_ms_lean;
     if (lean && kern && !win && grp == 8 && g_ms_words == 4)
-        kern_l = lean == 2 ? ms_lean_kernel<MODE, 4> : ms_lean_kernel<MODE, 8>;
+        kern_l = (g_ms_prefetch && p.pkts)
+                     ? (lean == 2 ? ms_lean_kernel<MODE, 4, true> : ms_lean_kernel<MODE, 8, true>)
+                     : (lean == 2 ? ms_lean_kernel<MODE, 4, false> : ms_lean_kernel<MODE, 8, false>);
     int occ = g_ctas_per_sm;
     if (occ <= 0) {
         if (kern_l) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_l, MS_BLOCK, 0));

@@ -284,7 +284,7 @@ enum { MODE_WRITE = 0, MODE_ACC = 1, MODE_PEER = 2 };
 // comparisons / verdict (MODE_WRITE), accumulates a function-parallel
 // partition (MODE_ACC), or combines straight into the ranks' buffers
 // (MODE_PEER); span = window length (comparisons of an unmatched packet).
-template <int MODE>
+template <int MODE, bool CS = false>
 __device__ __forceinline__ void emit_result(const ScanParams &p, uint32_t id, uint32_t f, uint32_t span,
                                             unsigned long long &st_sum, unsigned &st_max) {
     const uint32_t c = (f != PFW_NO_MATCH) ? (uint32_t)(f - p.win_lo + 1) : span;
@@ -313,9 +313,21 @@ __device__ __forceinline__ void emit_result(const ScanParams &p, uint32_t id, ui
             }
         }
     } else {
-        p.first[id] = f != PFW_NO_MATCH ? f : p.nomatch_out;
-        if (p.comps) p.comps[id] = c;
-        if (p.verdict) p.verdict[id] = (fl != PFW_NO_MATCH) ? p.accept[fl] : (uint8_t)0;
+        const uint32_t fo = f != PFW_NO_MATCH ? f : p.nomatch_out;
+        const uint8_t vo = (fl != PFW_NO_MATCH) ? p.accept[fl] : (uint8_t)0;
+        if (CS) {
+            // match-set scans write each packet's results once, in packet
+            // order: streaming stores (evict-first in L2), so the output
+            // stream does not push the tables out (the rule scan's scattered
+            // per-pass writes keep the default policy: partial sectors)
+            __stcs(p.first + id, fo);
+            if (p.comps) __stcs(p.comps + id, c);
+            if (p.verdict) __stcs(reinterpret_cast<signed char *>(p.verdict + id), (signed char)vo);
+        } else {
+            p.first[id] = fo;
+            if (p.comps) p.comps[id] = c;
+            if (p.verdict) p.verdict[id] = vo;
+        }
     }
     st_sum += c;
     st_max = max(st_max, c);
@@ -1420,6 +1432,8 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");
         g_ms_group = (int)value;
+    } else if (!strcmp(key, "ms_prefetch")) {
+        g_ms_prefetch = value != 0;
     } else if (!strcmp(key, "ms_odd_rows")) {
         g_ms_odd_rows = value != 0;
     } else if (!strcmp(key, "ms_lean")) {
