@@ -156,9 +156,15 @@ class FusedFunctionParallel:
         dev = f"cuda:{self.device}"
         self.own_range = packet_shard(n, self.info) if scatter else (0, n)
         m = self.own_range[1] - self.own_range[0]
+        # two result buffer sets, used by alternate calls: a call writes one
+        # set (reset during the previous call) and resets the other before its
+        # completion barrier, so every call needs a single host barrier.
         # never allocate 0 bytes: IPC needs a real allocation on every rank
-        self.first = torch.full((max(m, 1),), NO_MATCH, dtype=torch.int32, device=dev)
-        self.comps = torch.zeros(max(m, 1), dtype=torch.int32, device=dev) if with_comps else None
+        self._first = [torch.full((max(m, 1),), NO_MATCH, dtype=torch.int32, device=dev) for _ in range(2)]
+        self._comps = [torch.zeros(max(m, 1), dtype=torch.int32, device=dev) for _ in range(2)] \
+            if with_comps else [None, None]
+        self._k = 0
+        torch.cuda.synchronize(self.device)
         lib = _native.lib()
         hs = lib.pfw_ipc_handle_size()
 
@@ -168,35 +174,47 @@ class FusedFunctionParallel:
             _native.check(lib.pfw_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)), "pfw_ipc_get_handle")
             return buf.raw, off.value
 
-        mine = (handle(self.first), handle(self.comps) if with_comps else None)
+        mine = [(handle(self._first[k]), handle(self._comps[k]) if with_comps else None) for k in range(2)]
         world = self.info.world
         if world > 1:
             allh = [None] * world
-            dist.all_gather_object(allh, mine, group=group)
+            dist.all_gather_object(allh, mine, group=group)  # (also the initial barrier)
         else:
             allh = [mine]
         self._opened = []
-        firsts, comps = [], []
-        for t, (hf, hc) in enumerate(allh):
-            if t == self.info.rank:
-                firsts.append(self.first.data_ptr())
-                comps.append(self.comps.data_ptr() if with_comps else None)
-                continue
-            for hnd, out in ((hf, firsts), (hc, comps)):
-                if hnd is None:
-                    out.append(None)
-                    continue
-                raw, off = hnd
-                base = ctypes.c_void_p()
-                _native.check(lib.pfw_ipc_open(self.device, raw, ctypes.byref(base)), "pfw_ipc_open")
-                self._opened.append(base.value)
-                out.append(base.value + off)
         P = ctypes.c_void_p
-        self._peer_first = (P * world)(*firsts)
-        self._peer_comps = (P * world)(*comps) if with_comps else None
+        self._peer_first, self._peer_comps = [], []
+        for k in range(2):
+            firsts, comps = [], []
+            for t, sets in enumerate(allh):
+                hf, hc = sets[k]
+                if t == self.info.rank:
+                    firsts.append(self._first[k].data_ptr())
+                    comps.append(self._comps[k].data_ptr() if with_comps else None)
+                    continue
+                for hnd, out in ((hf, firsts), (hc, comps)):
+                    if hnd is None:
+                        out.append(None)
+                        continue
+                    raw, off = hnd
+                    base = ctypes.c_void_p()
+                    _native.check(lib.pfw_ipc_open(self.device, raw, ctypes.byref(base)), "pfw_ipc_open")
+                    self._opened.append(base.value)
+                    out.append(base.value + off)
+            self._peer_first.append((P * world)(*firsts))
+            self._peer_comps.append((P * world)(*comps) if with_comps else None)
         # packets each rank's buffers hold (checked again by the C side)
         self._peer_cap = (ctypes.c_int64 * world)(*[
             (b - a if scatter else n) for a, b in partition_bounds(n, world)])
+
+    @property
+    def first(self):
+        """This rank's first-match buffer of the latest call."""
+        return self._first[(self._k - 1) % 2]
+
+    @property
+    def comps(self):
+        return self._comps[(self._k - 1) % 2]
 
     def _barrier(self):
         import torch
@@ -206,16 +224,15 @@ class FusedFunctionParallel:
             dist.barrier(group=self.group)
 
     def run(self, pkts, stats=None, stream: int | None = None):
-        """Reset, scan this rank's rule shard with the fused combine, and return
-        this rank's (first, comps) once every rank's scan has completed."""
+        """Scan this rank's rule shard with the fused combine and return this
+        rank's (first, comps) once every rank's scan has completed.  The
+        returned tensors are views of an internal buffer set: valid until
+        the next call (which resets them for the call after it)."""
         import torch
         from . import _native
         if len(pkts) != self.n:
             raise ValueError(f"FusedFunctionParallel was set up for batches of {self.n} packets, got {len(pkts)}")
-        self.first.fill_(NO_MATCH)
-        if self.comps is not None:
-            self.comps.zero_()
-        self._barrier()  # nobody writes into a buffer before its owner reset it
+        k = self._k % 2
         # a rule-shard handle holds exactly this rank's rules (local window,
         # global indices); a whole-ruleset handle scans this rank's window
         if getattr(self.compiled, "is_shard", False):
@@ -224,12 +241,19 @@ class FusedFunctionParallel:
             lo, hi = rule_shard(self.compiled.num_rules, self.info)
         st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
         _native.check(_native.lib().pfw_scan_fused_min(
-            self.compiled.handle, lo, hi, pkts.data.data_ptr(), len(pkts), self._peer_first,
-            self._peer_comps, self._peer_cap, self.info.world, 1 if self.scatter else 0,
+            self.compiled.handle, lo, hi, pkts.data.data_ptr(), len(pkts), self._peer_first[k],
+            self._peer_comps[k], self._peer_cap, self.info.world, 1 if self.scatter else 0,
             None if stats is None else stats.data_ptr(), st), "pfw_scan_fused_min")
-        self._barrier()  # every rank's atomics have landed
+        # reset the other set (the previous call's results) for the next call;
+        # the barrier below orders it before any rank's next-call atomics
+        with torch.cuda.stream(torch.cuda.ExternalStream(st, device=self.device)):
+            self._first[k ^ 1].fill_(NO_MATCH)
+            if self._comps[k ^ 1] is not None:
+                self._comps[k ^ 1].zero_()
+        self._barrier()  # every rank's atomics into set k have landed
+        self._k += 1
         m = self.own_range[1] - self.own_range[0]
-        return self.first[:m], (self.comps[:m] if self.comps is not None else None)
+        return self._first[k][:m], (self._comps[k][:m] if self._comps[k] is not None else None)
 
     def close(self):
         from . import _native

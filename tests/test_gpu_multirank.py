@@ -46,8 +46,12 @@ def _worker(rank, world, port, q):
         # fused, reduce-scatter and all-reduce layouts
         for scatter in (True, False):
             fused = parallel.FusedFunctionParallel(c, n, scatter=scatter)
-            first, comps = fused.run(p)
-            out[("fused", scatter)] = (fused.own_range, first_to_host(first), comps.cpu().numpy())
+            for _ in range(3):  # one barrier per call: alternate buffer sets, reset one call ahead
+                first, comps = fused.run(p)
+                got = (fused.own_range, first_to_host(first), comps.cpu().numpy())
+                if ("fused", scatter) in out:
+                    assert all(np.array_equal(a, b) for a, b in zip(got[1:], out[("fused", scatter)][1:]))
+                out[("fused", scatter)] = got
             fused.close()
         # separate all-reduce combine (gloo here, NCCL on a multi-GPU box)
         import torch

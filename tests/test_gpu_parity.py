@@ -426,9 +426,12 @@ def test_fused_function_parallel_single_rank_class():
     c = compiled(golden_rules("r100000_s1"))
     p = pfw.generate_traffic_device(pfw.TrafficProfile(count=2000, seed=2), device=0)
     fused = FusedFunctionParallel(c, len(p))
-    first, comps = fused.run(p)
-    np.testing.assert_array_equal(first_to_host(first), g["function_1_first"])
-    np.testing.assert_array_equal(comps.cpu().numpy(), g["function_1_comps"])
+    for _ in range(3):  # alternate buffer sets: each call's set was reset by the previous call
+        first, comps = fused.run(p)
+        np.testing.assert_array_equal(first_to_host(first), g["function_1_first"])
+        np.testing.assert_array_equal(comps.cpu().numpy(), g["function_1_comps"])
+    with pytest.raises(ValueError, match="batches of"):
+        fused.run(p.slice(0, 100))
     fused.close()
 
 
