@@ -54,6 +54,7 @@ constexpr int64_t MS_CMP_MIN_RULES = 24576;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
+int g_ms_lean_cmp = 0;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane
 int g_ms_prefetch = 0;         // lean kernel over 16-byte records: cp.async pipeline of packets + lookup entries (measured 3-4% slower: off)
 int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
@@ -772,6 +773,13 @@ __global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_
     }
 }
 
+// base + 4 * off as one IMAD.WIDE (base: a 64-bit per-lane register)
+__device__ __forceinline__ const uint32_t *ms_word_ptr(const uint32_t *base, uint32_t off) {
+    const uint32_t *r;
+    asm("mad.wide.u32 %0, %1, 4, %2;" : "=l"(r) : "r"(off), "l"(base));
+    return r;
+}
+
 // The four rows' V words of one step for this lane: 128-bit loads (V = 4)
 // or Blackwell's 256-bit loads (V = 8, LDG.E.ENL2.256), all four in flight
 // together.
@@ -836,13 +844,15 @@ struct MsLk {
     uint32_t port[2];  // sport / dport -> interval
 };
 
-template <int MODE, int G, bool PF>
-__global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
+template <int MODE, int G, int V, bool PF, int MINB>
+__global__ void __launch_bounds__(MS_BLOCK, MINB)
     ms_lean_kernel(ScanParams p, MsView t, uint32_t zoff) {
-    constexpr int V = 32 / G, P = 32 / G;
-    constexpr uint32_t STEP = 32;  // words per step (one line per row)
-    __shared__ uint4 s_off[MS_BLOCK / 32][32];
+    constexpr int P = 32 / G;
+    constexpr uint32_t STEP = (uint32_t)G * V;  // words per step (G*V = 32: one line per row)
+    static_assert(V % 4 == 0 && 128 % STEP == 0, "4 or 8 words per lane; steps divide the 128-word row unit");
+    __shared__ uint4 s_off[MS_BLOCK / 32][33];  // [32]: the zero line (idle groups)
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];
+    __shared__ uint4 s_x[MS_BLOCK / 32][32][V / 4];  // per packet: the finding lane's AND words
     // PF (16-byte records): a two-batch software pipeline of async copies --
     // while batch j's step loop runs, the packets of batch j+2 and the lookup
     // table entries of batch j+1 land in shared memory, so a batch's lookup
@@ -861,6 +871,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
     const int nsteps = p.lo >= p.hi ? 0 : (int)((uint32_t)((p.hi - 1) >> 5) / STEP) + 1;
     const uint32_t wp = (uint32_t)t.wp;
     const uint32_t *bits = t.bits0;
+    if (lane == 0) s_off[warp][32] = make_uint4(zoff, zoff, zoff, zoff);
     unsigned long long st_sum = 0;
     unsigned st_max = 0;
 
@@ -947,10 +958,11 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
             // group state: packet pj of the batch (-1: idle, reading the zero
             // line), step s, the four rows' word offsets at this lane's words
             // (s_off holds each packet's row offsets; a lane adds its own lv)
+            // (s_off[warp][32] is the zero line's offset: idle groups point there)
             int pj = grp < nv ? grp : -1;
             int next = P;  // next packet to hand out; every group idle <=> next == nv + P
             int s = 0;
-            uint4 o = pj >= 0 ? s_off[warp][pj] : make_uint4(zoff, zoff, zoff, zoff);
+            uint4 o = s_off[warp][pj >= 0 ? pj : 32];
             o.x += lv;
             o.y += lv;
             o.z += lv;
@@ -968,16 +980,14 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
                 const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
                 const unsigned gbits = (bal >> gbase) & ((1u << G) - 1u);
                 // the group's lowest lane with a set bit holds the packet's
-                // first match: its first non-zero word, that word's lowest bit
-                // (computed by every lane, stored by that one: no divergence)
-                uint32_t wsel = x[V - 1], widx = V - 1;
+                // first match: it parks its words and their position; the
+                // bit itself is resolved after the loop, one packet per lane
+                // (a 32-lane select chain instead of one per iteration)
+                if (any != 0u && (gbits & below) == 0u) {
+                    s_res[warp][pj] = (uint32_t)s * STEP + lv;  // word index of x[0]
 #pragma unroll
-                for (int k = V - 2; k >= 0; k--) {
-                    wsel = x[k] ? x[k] : wsel;
-                    widx = x[k] ? (uint32_t)k : widx;
+                    for (int k = 0; k < V; k += 4) s_x[warp][pj][k / 4] = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
                 }
-                const uint32_t cand = ((uint32_t)s * STEP + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
-                if (any != 0u && (gbits & below) == 0u) s_res[warp][pj] = cand;
                 const bool act = pj >= 0;
                 const bool done = act && (gbits != 0u || s + 1 >= nsteps);
                 const unsigned dm = __ballot_sync(0xFFFFFFFFu, done && gl == 0);
@@ -985,14 +995,169 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
                 // next packet (its rank among the finished groups), an active
                 // one advances one step, an idle one stays on the zero line
                 const int np = next + __popc(dm & groups_below);
-                const uint4 q = s_off[warp][np & 31];
                 const bool take = np < nv;
+                const uint4 q = s_off[warp][take ? np : 32];
                 const uint32_t adv = act ? STEP : 0u;
-                o.x = done ? (take ? q.x : zoff) + lv : o.x + adv;
-                o.y = done ? (take ? q.y : zoff) + lv : o.y + adv;
-                o.z = done ? (take ? q.z : zoff) + lv : o.z + adv;
-                o.w = done ? (take ? q.w : zoff) + lv : o.w + adv;
+                o.x = done ? q.x + lv : o.x + adv;
+                o.y = done ? q.y + lv : o.y + adv;
+                o.z = done ? q.z + lv : o.z + adv;
+                o.w = done ? q.w + lv : o.w + adv;
                 s = done ? 0 : s + (act ? 1 : 0);
+                pj = done ? (take ? np : -1) : pj;
+                next += __popc(dm);
+            }
+        }
+        __syncwarp();
+        if (i < n) {
+            uint32_t res = s_res[warp][lane];
+            if (res != PFW_NO_MATCH) {  // the parked words' first non-zero word, its lowest bit
+                uint32_t x[V];
+#pragma unroll
+                for (int k = 0; k < V; k += 4) {
+                    const uint4 q4 = s_x[warp][lane][k / 4];
+                    x[k] = q4.x;
+                    x[k + 1] = q4.y;
+                    x[k + 2] = q4.z;
+                    x[k + 3] = q4.w;
+                }
+                uint32_t wsel = x[V - 1], widx = V - 1;
+#pragma unroll
+                for (int k = V - 2; k >= 0; k--) {
+                    wsel = x[k] ? x[k] : wsel;
+                    widx = x[k] ? (uint32_t)k : widx;
+                }
+                res = (res + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
+            }
+            PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
+            emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
+        }
+        __syncwarp();
+    }
+    if (p.stats) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            st_sum += __shfl_xor_sync(0xFFFFFFFFu, st_sum, o);
+            st_max = max(st_max, __shfl_xor_sync(0xFFFFFFFFu, st_max, o));
+        }
+        if (lane == 0) {
+            if (st_sum) atomicAdd(&p.stats[0], st_sum);
+            if (st_max) atomicMax(&p.stats[1], (unsigned long long)st_max);
+        }
+    }
+}
+
+// Lean scan of whole-table windows over COMPRESSED rows (large rulesets, the
+// function-parallel config): the lean kernel's step loop, where a step's four
+// lines are line numbers instead of row offsets.  The lookup phase parks each
+// packet's absolute line numbers (loff[d][b] + index) for its first MS_LEAN_PARK
+// blocks in shared memory, from the dense head array (one 16-byte load per
+// dimension); a step takes its block's four line numbers with one shared
+// 16-byte load; blocks past the parked ones (rare: most scans end in the first
+// two or three) read the index from global memory.  Idle groups read the zero
+// line after the last distinct line.
+#ifndef MS_LEAN_PARK
+#define MS_LEAN_PARK 4
+#endif
+template <int MODE, int G>
+__global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
+    ms_lean_cmp_kernel(ScanParams p, MsView t, MsCmp u, uint32_t zline) {
+    constexpr int V = 32 / G, P = 32 / G, K = MS_LEAN_PARK;
+    static_assert(K >= 1 && K <= 8, "1..8 parked blocks (the head array holds 8)");
+    __shared__ uint4 s_ln[MS_BLOCK / 32][32][K];  // per packet: line numbers of blocks 0..K-1 (x..w = dimension)
+    __shared__ uint4 s_row[MS_BLOCK / 32][32];    // per packet: its four rows (blocks >= K)
+    __shared__ uint32_t s_res[MS_BLOCK / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / G, gl = lane % G, gbase = grp * G;
+    const uint32_t lv = (uint32_t)gl * V;
+    const unsigned below = (1u << gl) - 1u;
+    const unsigned groups_below = (1u << gbase) - 1u;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    const int64_t n = p.n;
+    const uint32_t span = (uint32_t)(p.win_hi > p.win_lo ? p.win_hi - p.win_lo : 0);
+    const int nsteps = p.lo >= p.hi ? 0 : (int)((uint32_t)((p.hi - 1) >> 5) / 32u) + 1;  // blocks
+    const uint32_t *lines = u.lines;
+    const uint4 zq = make_uint4(zline, zline, zline, zline);
+    unsigned long long st_sum = 0;
+    unsigned st_max = 0;
+
+    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
+        const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
+        const int64_t i = b0 + lane;
+        if (i < n) {
+            uint4 v;
+            if (p.pkts) {
+                v = __ldcs(p.pkts + i);
+            } else {
+                v.x = __ldcs(p.cols.src + i);
+                v.y = __ldcs(p.cols.dst + i);
+                v.z = ((uint32_t)__ldcs(p.cols.sport + i) << 16) | (uint32_t)__ldcs(p.cols.dport + i);
+                v.w = __ldcs(p.cols.proto + i);
+            }
+            const uint32_t rr[4] = {ms_ip_row(t.ipb[0], t.ipc[0], v.x), ms_ip_row(t.ipb[1], t.ipc[1], v.y),
+                                    (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
+                                    __ldg(t.port[1] + (v.z & 0xFFFFu))};
+            PFW_CHECK(rr[0] < t.nrows[0] && rr[1] < t.nrows[1] && rr[2] < t.nrows[2] && rr[3] < t.nrows[3]);
+            s_row[warp][lane] = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+            uint32_t ln[4][K];
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(u.head + u.head_off[d] + (size_t)rr[d] * 8));
+                const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int j = 0; j < K; j++)
+                    ln[d][j] = __ldg(u.loff + d * u.nblk + j) + ((qq[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+            }
+#pragma unroll
+            for (int j = 0; j < K; j++) s_ln[warp][lane][j] = make_uint4(ln[0][j], ln[1][j], ln[2][j], ln[3][j]);
+        }
+        s_res[warp][lane] = PFW_NO_MATCH;
+        __syncwarp();
+        if (nsteps > 0) {
+            int pj = grp < nv ? grp : -1;
+            int next = P;
+            int s = 0;
+            uint4 q = pj >= 0 ? s_ln[warp][pj][0] : zq;
+            while (next < nv + P) {
+                uint32_t w[4][V];
+                ms_load_rows<V>(lines + ((size_t)q.x << 5) + lv, lines + ((size_t)q.y << 5) + lv,
+                                lines + ((size_t)q.z << 5) + lv, lines + ((size_t)q.w << 5) + lv, w);
+                uint32_t x[V], any = 0u;
+#pragma unroll
+                for (int k = 0; k < V; k++) {
+                    x[k] = w[0][k] & w[1][k] & w[2][k] & w[3][k];
+                    any |= x[k];
+                }
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
+                const unsigned gbits = (bal >> gbase) & ((1u << G) - 1u);
+                uint32_t wsel = x[V - 1], widx = V - 1;
+#pragma unroll
+                for (int k = V - 2; k >= 0; k--) {
+                    wsel = x[k] ? x[k] : wsel;
+                    widx = x[k] ? (uint32_t)k : widx;
+                }
+                const uint32_t cand = ((uint32_t)s * 32u + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
+                if (any != 0u && (gbits & below) == 0u) s_res[warp][pj] = cand;
+                const bool act = pj >= 0;
+                const bool done = act && (gbits != 0u || s + 1 >= nsteps);
+                const unsigned dm = __ballot_sync(0xFFFFFFFFu, done && gl == 0);
+                const int np = next + __popc(dm & groups_below);
+                const bool take = np < nv;
+                // the next block's line numbers: a new packet's block 0, or this
+                // packet's next parked block (one shared 16-byte load either way)
+                const int ns = done ? 0 : s + (act ? 1 : 0);
+                const int qi = done ? (np & 31) : (pj & 31);
+                const uint4 qn = s_ln[warp][qi][ns < K ? ns : 0];
+                q = (done && !take) || !act ? zq : qn;
+                if (act && !done && ns >= K) {  // past the parked blocks: indices from global memory
+                    const uint4 rw = s_row[warp][pj];
+                    const uint32_t b = (uint32_t)ns;
+                    q.x = __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
+                    q.y = __ldg(u.loff + u.nblk + b) + __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
+                    q.z = __ldg(u.loff + 2 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
+                    q.w = __ldg(u.loff + 3 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
+                }
+                s = ns;
                 pj = done ? (take ? np : -1) : pj;
                 next += __popc(dm);
             }
@@ -1529,11 +1694,25 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     // (auto: 4-lane groups with 256-bit loads up to 8K rules -- measured +7% at
     // 4K rules, +10% at 1K; at 10K rules all variants are within 1%, the
     // general kernel is kept there)
-    const int lean = g_ms_lean == 3 ? (h->n <= 8192 ? 2 : 0) : g_ms_lean;
+    const int lean = g_ms_lean == 3 ? (h->n <= 2048 ? 2 : 1) : g_ms_lean;
+    // compressed rows, whole table, no summaries: the lean compressed kernel
+    // (tuning ms_lean_cmp: 0 off, 1 8-lane groups, 2 4-lane groups / 256-bit loads)
+    void (*kern_lc)(ScanParams, MsView, MsCmp, uint32_t) = nullptr;
+    if (g_ms_lean_cmp && kern_c && !sum && !win)
+        kern_lc = g_ms_lean_cmp == 2 ? ms_lean_cmp_kernel<MODE, 4> : ms_lean_cmp_kernel<MODE, 8>;
     if (lean && kern && !win && grp == 8 && g_ms_words == 4)
-        kern_l = (g_ms_prefetch && p.pkts)
-                     ? (lean == 2 ? ms_lean_kernel<MODE, 4, true> : ms_lean_kernel<MODE, 8, true>)
-                     : (lean == 2 ? ms_lean_kernel<MODE, 4, false> : ms_lean_kernel<MODE, 8, false>);
+        switch (lean) {
+            // 1: 8-lane groups, 1024-rule steps (cp.async lookup pipeline with ms_prefetch)
+            case 1: kern_l = (g_ms_prefetch && p.pkts) ? ms_lean_kernel<MODE, 8, 4, true, PFW_MS_MINB>
+                                                       : ms_lean_kernel<MODE, 8, 4, false, PFW_MS_MINB>; break;
+            // 2: 4-lane groups, 256-bit loads, 1024-rule steps, 8 packets per warp
+            case 2: kern_l = ms_lean_kernel<MODE, 4, 8, false, 4>; break;
+            // 4: 4-lane groups, 512-rule steps (half the bytes per step), 8 packets per warp
+            case 4: kern_l = ms_lean_kernel<MODE, 4, 4, false, PFW_MS_MINB>; break;
+            // 5: as 1 at 6 resident blocks per SM (42 registers)
+            case 5: kern_l = ms_lean_kernel<MODE, 8, 4, false, 6>; break;
+            default: break;
+        }
     int occ = g_ctas_per_sm;
     if (occ <= 0) {
         if (kern_l) CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern_l, MS_BLOCK, 0));
@@ -1554,7 +1733,14 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
         }
         pc.blocks_read = g_counter_dev;
     }
-    if (kern_l) {
+    if (kern_lc) {
+        if (g_ctas_per_sm <= 0) {
+            int o2 = 1;
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, kern_lc, MS_BLOCK, 0));
+            grid = std::min<int64_t>((int64_t)h->sms * std::max(o2, 1), need);
+        }
+        kern_lc<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, uc, (uint32_t)m->nlines);
+    } else if (kern_l) {
         // word offset of the zero padding after the src rows (idle groups read it)
         const uint32_t zoff = (uint32_t)((m->d_bits[0] - m->d_bits_all) + m->rows[0] * m->wp);
         kern_l<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, zoff);

@@ -1432,14 +1432,18 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");
         g_ms_group = (int)value;
+    } else if (!strcmp(key, "ms_lean_cmp")) {
+        if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_lean_cmp: 0 off, 1 8-lane, 2 4-lane groups");
+        g_ms_lean_cmp = (int)value;
     } else if (!strcmp(key, "ms_prefetch")) {
         g_ms_prefetch = value != 0;
     } else if (!strcmp(key, "ms_odd_rows")) {
         g_ms_odd_rows = value != 0;
     } else if (!strcmp(key, "ms_lean")) {
-        if (value < 0 || value > 3)
+        if (value < 0 || value > 5)
             return set_err(PFW_ERR_INVALID, "ms_lean: 0 general kernel, 1 lean (8-lane groups), 2 lean (4-lane "
-                                            "groups, 256-bit loads), 3 auto");
+                                            "groups, 256-bit loads), 3 auto, 4 lean (4-lane groups, 512-rule "
+                                            "steps), 5 lean (8-lane groups, 6 blocks per SM)");
         g_ms_lean = (int)value;
     } else {
         return set_err(PFW_ERR_INVALID, "unknown tuning key '%s'", key);

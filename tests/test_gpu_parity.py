@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_prefetch", 0)):
+                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_prefetch", 0), ("ms_lean_cmp", 0)):
         _native.set_tuning(k, v)
 
 
@@ -631,7 +631,7 @@ def test_match_set_step_shapes(group, words):
     test_fused_min_combine_virtual_ranks(0)
 
 
-@pytest.mark.parametrize("lean,pf", [(0, 1), (1, 1), (1, 0), (2, 1), (2, 0)])
+@pytest.mark.parametrize("lean,pf", [(0, 1), (1, 1), (1, 0), (2, 0), (4, 0), (5, 0)])
 def test_lean_whole_table_scan(lean, pf):
     """Whole-table scans over plain rows: the general kernel (0), the lean one
     (1) and the lean one with L1 no-allocate row loads (2) are bit-exact
@@ -662,6 +662,31 @@ def test_lean_whole_table_scan(lean, pf):
     cc = comps.cpu().numpy().astype(np.int64)
     np.testing.assert_array_equal(cc, np.where(first >= 0, first + 1, 10_000))
     assert stats.cpu().tolist() == [int(cc.sum()), int(cc.max())]
+
+
+@pytest.mark.parametrize("lc", [0, 1, 2])
+def test_lean_compressed_rows(lc):
+    """Whole-table scans over compressed rows: the general kernel (0) and the
+    lean compressed kernel with 8- or 4-lane groups (1, 2) are bit-exact, incl.
+    scans that run past the parked blocks (late matches, default deny)."""
+    _native.set_tuning("algo", 2)
+    _native.set_tuning("ms_compress", 1)
+    _native.set_tuning("ms_summary", 0)
+    _native.set_tuning("ms_lean_cmp", lc)
+    for name, rn, tn in SCANS:
+        test_scan_matches_reference_golden(name, rn, tn)
+    test_ragged_sizes_and_empty()
+    test_adversarial_recipe_sample()        # most packets scan far past the parked blocks
+    test_function_parallel_100k_rules()     # nodes = 1 is a whole-table scan
+    test_engine_models_match_reference_golden("data")
+    rules = golden_rules("r100000_s1")
+    c = compiled(rules)
+    n = 1 << 20
+    p = pfw.generate_traffic_device(pfw.TrafficProfile(count=n, seed=2), device=0)
+    first = first_to_host(c.scan_range_device(p, 0, 100_000))
+    idx = np.arange(0, n, 211)
+    sub = {f: v[idx] for f, v in p.columns().items()}
+    np.testing.assert_array_equal(first[idx], oracle.scan_range(rules, sub, 0, 100_000))
 
 
 def test_match_set_budget_falls_back_to_rule_scan():
