@@ -962,6 +962,7 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
             int pj = grp < nv ? grp : -1;
             int next = P;  // next packet to hand out; every group idle <=> next == nv + P
             int s = 0;
+            const uint32_t s_off_base = (uint32_t)__cvta_generic_to_shared(&s_off[warp][0]);
             uint4 o = s_off[warp][pj >= 0 ? pj : 32];
             o.x += lv;
             o.y += lv;
@@ -996,12 +997,23 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
                 // one advances one step, an idle one stays on the zero line
                 const int np = next + __popc(dm & groups_below);
                 const bool take = np < nv;
-                const uint4 q = s_off[warp][take ? np : 32];
-                const uint32_t adv = act ? STEP : 0u;
-                o.x = done ? q.x + lv : o.x + adv;
-                o.y = done ? q.y + lv : o.y + adv;
-                o.z = done ? q.z + lv : o.z + adv;
-                o.w = done ? q.w + lv : o.w + adv;
+                // a finished group loads its next packet's offsets straight into
+                // o (predicated shared load), then every lane adds lv (new
+                // packet) or one step (active) or nothing (idle)
+                {
+                    const uint32_t sa = s_off_base + (uint32_t)(take ? np : 32) * 16u;
+                    asm volatile(
+                        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
+                        "@q ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
+                        : "+r"(o.x), "+r"(o.y), "+r"(o.z), "+r"(o.w)
+                        : "r"((uint32_t)done), "r"(sa)
+                        : "memory");
+                }
+                const uint32_t add = done ? lv : (act ? STEP : 0u);
+                o.x += add;
+                o.y += add;
+                o.z += add;
+                o.w += add;
                 s = done ? 0 : s + (act ? 1 : 0);
                 pj = done ? (take ? np : -1) : pj;
                 next += __popc(dm);
