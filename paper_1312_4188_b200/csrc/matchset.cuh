@@ -54,7 +54,7 @@ constexpr int64_t MS_CMP_MIN_RULES = 24576;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
-int g_ms_lean_cmp = 0;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane
+int g_ms_lean_cmp = 1;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane
 int g_ms_prefetch = 0;         // lean kernel over 16-byte records: cp.async pipeline of packets + lookup entries (measured 3-4% slower: off)
 int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
@@ -370,7 +370,8 @@ __global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_
     // the count (bit 7: more candidates follow the parked ones)
     __shared__ uint16_t s_cb[(SUM && CMP) ? MS_BLOCK / 32 : 1][(SUM && CMP) ? BATCH : 1][PFW_MS_PARK];
     __shared__ uint8_t s_nc[(SUM && CMP) ? MS_BLOCK / 32 : 1][(SUM && CMP) ? BATCH : 1];  // CMP: line numbers, 8 blocks x 4 dims (u32)
-    __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match of the batch's packets
+    __shared__ uint32_t s_res[MS_BLOCK / 32][BATCH];  // per warp: first match (word base until resolved)
+    __shared__ uint32_t s_xw[MS_BLOCK / 32][BATCH][V];  // per packet: the finding lane's AND words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
@@ -652,20 +653,18 @@ __global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_
                     if (two && !gbits2 && gbits == 0u) s = s2;  // (the last block this step read)
                 }
                 const bool found = gbits != 0u;  // (idle groups have no bits)
-                if (bal) {  // warp-uniform: some group found its packet's first match
-                    // this lane's lowest set bit: first non-zero word, its lowest bit
-                    uint32_t wsel = x[V - 1], widx = V - 1;
+                if (found) {
+                    // the group's lowest lane with a set bit parks its words and
+                    // their position; the bit is resolved after the loop, one
+                    // packet per lane
+                    uint32_t anyx = 0u;
 #pragma unroll
-                    for (int v = V - 2; v >= 0; v--) {
-                        if (x[v]) {
-                            wsel = x[v];
-                            widx = v;
-                        }
+                    for (int v = 0; v < V; v++) anyx |= x[v];
+                    if (anyx != 0u && (gbits & ((1u << gl) - 1u)) == 0u) {
+                        s_res[warp][pj] = cbeg + (uint32_t)s * STEP + lv;
+#pragma unroll
+                        for (int v = 0; v < V; v++) s_xw[warp][pj][v] = x[v];
                     }
-                    const uint32_t cand =
-                        __shfl_sync(0xFFFFFFFFu, (cbeg + (uint32_t)s * STEP + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1),
-                                    gbase + (__ffs(gbits) - 1) * (gbits != 0u));
-                    if (found && gl == 0) s_res[warp][pj] = cand;
                 }
                 bool done = act && (found || s + 1 >= nsteps);
                 int ns = s + 1;  // next step (SUM: the next candidate block)
@@ -746,7 +745,18 @@ __global__ void __launch_bounds__(MS_BLOCK, (SUM && CMP) ? PFW_MS_MINB_SC : PFW_
         for (int k = 0; k < LPB; k++) {
             const int64_t i = b0 + k * 32 + lane;
             if (i < n) {
-                const uint32_t res = s_res[warp][k * 32 + lane];
+                uint32_t res = s_res[warp][k * 32 + lane];
+                if (res != PFW_NO_MATCH) {  // the parked words' first non-zero word, its lowest bit
+                    const uint32_t *xw = s_xw[warp][k * 32 + lane];
+                    uint32_t wsel = xw[V - 1], widx = V - 1;
+#pragma unroll
+                    for (int v = V - 2; v >= 0; v--) {
+                        const uint32_t xv = xw[v];
+                        wsel = xv ? xv : wsel;
+                        widx = xv ? (uint32_t)v : widx;
+                    }
+                    res = (res + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
+                }
                 PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
                 emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
             }
@@ -822,6 +832,28 @@ __device__ __forceinline__ void ms_load_rows(const uint32_t *a, const uint32_t *
 //  * G = 4: each lane loads 32 bytes per row (256-bit loads), so one load
 //    instruction per row serves 8 packets per warp (8 steps per iteration).
 // Results are identical (same lowest set bit of the same AND).
+// The first set bit of a finding lane's parked AND words (V words starting at
+// word index wbase of the row): (wbase + first non-zero word) * 32 + its lowest bit
+template <int V>
+__device__ __forceinline__ uint32_t ms_parked_first_bit(const uint4 *px, uint32_t wbase) {
+    uint32_t x[V];
+#pragma unroll
+    for (int k = 0; k < V; k += 4) {
+        const uint4 q4 = px[k / 4];
+        x[k] = q4.x;
+        x[k + 1] = q4.y;
+        x[k + 2] = q4.z;
+        x[k + 3] = q4.w;
+    }
+    uint32_t wsel = x[V - 1], widx = V - 1;
+#pragma unroll
+    for (int k = V - 2; k >= 0; k--) {
+        wsel = x[k] ? x[k] : wsel;
+        widx = x[k] ? (uint32_t)k : widx;
+    }
+    return (wbase + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
+}
+
 // cp.async (LDGSTS) helpers: global -> shared without registers
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
@@ -1078,6 +1110,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
     __shared__ uint4 s_ln[MS_BLOCK / 32][32][K];  // per packet: line numbers of blocks 0..K-1 (x..w = dimension)
     __shared__ uint4 s_row[MS_BLOCK / 32][32];    // per packet: its four rows (blocks >= K)
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];
+    __shared__ uint4 s_x[MS_BLOCK / 32][32][V / 4];  // per packet: the finding lane's AND words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const uint32_t lv = (uint32_t)gl * V;
@@ -1142,14 +1175,11 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
                 }
                 const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
                 const unsigned gbits = (bal >> gbase) & ((1u << G) - 1u);
-                uint32_t wsel = x[V - 1], widx = V - 1;
+                if (any != 0u && (gbits & below) == 0u) {  // park the words; the bit is resolved after the loop
+                    s_res[warp][pj] = (uint32_t)s * 32u + lv;
 #pragma unroll
-                for (int k = V - 2; k >= 0; k--) {
-                    wsel = x[k] ? x[k] : wsel;
-                    widx = x[k] ? (uint32_t)k : widx;
+                    for (int k = 0; k < V; k += 4) s_x[warp][pj][k / 4] = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
                 }
-                const uint32_t cand = ((uint32_t)s * 32u + lv + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
-                if (any != 0u && (gbits & below) == 0u) s_res[warp][pj] = cand;
                 const bool act = pj >= 0;
                 const bool done = act && (gbits != 0u || s + 1 >= nsteps);
                 const unsigned dm = __ballot_sync(0xFFFFFFFFu, done && gl == 0);
@@ -1176,7 +1206,8 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
         }
         __syncwarp();
         if (i < n) {
-            const uint32_t res = s_res[warp][lane];
+            uint32_t res = s_res[warp][lane];
+            if (res != PFW_NO_MATCH) res = ms_parked_first_bit<V>(&s_x[warp][lane][0], res);
             PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
             emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
         }
