@@ -55,7 +55,6 @@ constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet kee
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
 int g_ms_lean_cmp = 1;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane
-int g_ms_prefetch = 0;         // lean kernel over 16-byte records: cp.async pipeline of packets + lookup entries (measured 3-4% slower: off)
 int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
 
@@ -854,6 +853,18 @@ __device__ __forceinline__ uint32_t ms_parked_first_bit(const uint4 *px, uint32_
     return (wbase + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
 }
 
+// Lean scan of whole-table windows over plain rows (the data-parallel /
+// grid / sequential configs): the search of ms_scan_kernel<MODE, G, V,
+// false> -- groups of G lanes, one 128-byte line of each of the packet's four
+// rows per step (1024 rules), groups refilled from the warp's batch of 32 --
+// with the per-step work cut to what the search needs:
+//  * idle groups read a zero line (the padding after the src rows) instead
+//    of being predicated off, so no per-iteration zeroing / predicate setup;
+//  * only the group's lowest lane with a set bit resolves the index, from
+//    its own registers (no shuffle); the next state is selected branch-free;
+//  * G = 4: each lane loads 32 bytes per row (256-bit loads), so one load
+//    instruction per row serves 8 packets per warp (8 steps per iteration).
+// Results are identical (same lowest set bit of the same AND).
 // cp.async (LDGSTS) helpers: global -> shared without registers
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
@@ -876,21 +887,16 @@ struct MsLk {
     uint32_t port[2];  // sport / dport -> interval
 };
 
-template <int MODE, int G, int V, bool PF, int MINB>
+template <int MODE, int G, int V, int LPB, int MINB>
 __global__ void __launch_bounds__(MS_BLOCK, MINB)
     ms_lean_kernel(ScanParams p, MsView t, uint32_t zoff) {
-    constexpr int P = 32 / G;
+    constexpr int P = 32 / G;                   // packets in flight per warp
+    constexpr int B = 32 * LPB;                 // packets per warp batch
     constexpr uint32_t STEP = (uint32_t)G * V;  // words per step (G*V = 32: one line per row)
     static_assert(V % 4 == 0 && 128 % STEP == 0, "4 or 8 words per lane; steps divide the 128-word row unit");
-    __shared__ uint4 s_off[MS_BLOCK / 32][33];  // [32]: the zero line (idle groups)
-    __shared__ uint32_t s_res[MS_BLOCK / 32][32];
-    __shared__ uint4 s_x[MS_BLOCK / 32][32][V / 4];  // per packet: the finding lane's AND words
-    // PF (16-byte records): a two-batch software pipeline of async copies --
-    // while batch j's step loop runs, the packets of batch j+2 and the lookup
-    // table entries of batch j+1 land in shared memory, so a batch's lookup
-    // phase waits only for the (rare) boundary search
-    __shared__ uint4 s_pk[PF ? MS_BLOCK / 32 : 1][PF ? 2 : 1][32];
-    __shared__ MsLk s_lk[PF ? MS_BLOCK / 32 : 1][PF ? 2 : 1][32];
+    __shared__ uint4 s_off[MS_BLOCK / 32][B + 1];  // per packet: its four rows' word offsets; [B]: the zero line
+    __shared__ uint32_t s_res[MS_BLOCK / 32][B];   // per packet: word base of its first match (resolved after)
+    __shared__ uint4 s_x[MS_BLOCK / 32][B][V / 4];  // per packet: the finding lane's AND words
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const uint32_t lv = (uint32_t)gl * V;
@@ -903,99 +909,53 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
     const int nsteps = p.lo >= p.hi ? 0 : (int)((uint32_t)((p.hi - 1) >> 5) / STEP) + 1;
     const uint32_t wp = (uint32_t)t.wp;
     const uint32_t *bits = t.bits0;
-    if (lane == 0) s_off[warp][32] = make_uint4(zoff, zoff, zoff, zoff);
+    if (lane == 0) s_off[warp][B] = make_uint4(zoff, zoff, zoff, zoff);
+    const uint32_t s_off_base = (uint32_t)__cvta_generic_to_shared(&s_off[warp][0]);
     unsigned long long st_sum = 0;
     unsigned st_max = 0;
 
-    // PF: gather batch jb's lookup entries (its packets already in s_pk[.][buf])
-    auto issue_lookups = [&](int64_t bb, int buf) {
-        if (bb + lane < n) {
-            const uint4 v = s_pk[PF ? warp : 0][PF ? buf : 0][lane];
-            MsLk *d = &s_lk[PF ? warp : 0][PF ? buf : 0][lane];
-            cp_async8(&d->ipc[0], t.ipc[0] + (v.x >> 16));
-            cp_async8(&d->ipc[1], t.ipc[1] + (v.y >> 16));
-            cp_async4(&d->port[0], t.port[0] + (v.z >> 16));
-            cp_async4(&d->port[1], t.port[1] + (v.z & 0xFFFFu));
-        }
-    };
-    auto issue_packets = [&](int64_t bb, int buf) {
-        if (bb + lane < n) cp_async16(&s_pk[PF ? warp : 0][PF ? buf : 0][lane], p.pkts + bb + lane);
-    };
-    if (PF) {  // prologue: packets of the first two batches, lookups of the first
-        issue_packets(gw * 32, 0);
-        issue_packets(gw * 32 + nw * 32, 1);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncwarp();
-        issue_lookups(gw * 32, 0);
-        cp_async_commit();
-    }
-    int buf = 0;
-    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32, buf ^= 1) {
-        const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
-        const int64_t i = b0 + lane;
-        if (PF) {
-            cp_async_wait_all();
-            __syncwarp();
-        }
-        if (i < n) {
-            uint4 v;
-            uint4 r;
-            if (PF) {
-                v = s_pk[PF ? warp : 0][PF ? buf : 0][lane];
-                const MsLk lk = s_lk[PF ? warp : 0][PF ? buf : 0][lane];
-                uint32_t rr[2];
+    for (int64_t b0 = gw * B; b0 < n; b0 += nw * B) {
+        const int nv = (int)((n - b0) < B ? (n - b0) : B);
+        // lookups, one packet per lane per round (all LPB packet loads in flight first)
+        uint4 v[LPB];
 #pragma unroll
-                for (int d = 0; d < 2; d++) {  // ms_ip_row with the /16 entry already here
-                    const uint32_t ip = d ? v.y : v.x;
-                    uint32_t lo = lk.ipc[d].x, hi = lk.ipc[d].y;
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) >> 1;
-                        if (__ldg(t.ipb[d] + mid) <= ip) lo = mid + 1;
-                        else hi = mid;
-                    }
-                    rr[d] = lo - 1;
-                }
-                r = make_uint4(rr[0], rr[1], (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + lk.port[0],
-                               lk.port[1]);
-            } else {
+        for (int k = 0; k < LPB; k++) {
+            const int64_t i = b0 + k * 32 + lane;
+            v[k] = make_uint4(0u, 0u, 0u, 0u);
+            if (i < n) {
                 if (p.pkts) {
-                    v = __ldcs(p.pkts + i);  // streamed once: evict-first in L2 (the tables stay)
+                    v[k] = __ldcs(p.pkts + i);  // streamed once: evict-first in L2 (the tables stay)
                 } else {
-                    v.x = __ldcs(p.cols.src + i);
-                    v.y = __ldcs(p.cols.dst + i);
-                    v.z = ((uint32_t)__ldcs(p.cols.sport + i) << 16) | (uint32_t)__ldcs(p.cols.dport + i);
-                    v.w = __ldcs(p.cols.proto + i);
+                    v[k].x = __ldcs(p.cols.src + i);
+                    v[k].y = __ldcs(p.cols.dst + i);
+                    v[k].z = ((uint32_t)__ldcs(p.cols.sport + i) << 16) | (uint32_t)__ldcs(p.cols.dport + i);
+                    v[k].w = __ldcs(p.cols.proto + i);
                 }
-                r = make_uint4(
-                    ms_ip_row(t.ipb[0], t.ipc[0], v.x), ms_ip_row(t.ipb[1], t.ipc[1], v.y),
-                    (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
-                    __ldg(t.port[1] + (v.z & 0xFFFFu)));
             }
-            PFW_CHECK(r.x < t.nrows[0] && r.y < t.nrows[1] && r.z < t.nrows[2] && r.w < t.nrows[3]);
-            s_off[warp][lane] = make_uint4(r.x * wp + t.off[0], r.y * wp + t.off[1], r.z * wp + t.off[2],
-                                           r.w * wp + t.off[3]);
         }
-        s_res[warp][lane] = PFW_NO_MATCH;
-        if (PF) {
-            // next batch's lookups (its packets landed with the wait above),
-            // then the batch after next's packets into the buffer just read
-            __syncwarp();
-            issue_lookups(b0 + nw * 32, buf ^ 1);
-            issue_packets(b0 + 2 * nw * 32, buf);
-            cp_async_commit();
+#pragma unroll
+        for (int k = 0; k < LPB; k++) {
+            const int64_t i = b0 + k * 32 + lane;
+            if (i < n) {
+                const uint4 r = make_uint4(
+                    ms_ip_row(t.ipb[0], t.ipc[0], v[k].x), ms_ip_row(t.ipb[1], t.ipc[1], v[k].y),
+                    (uint32_t)__ldg(t.cls + (v[k].w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v[k].z >> 16)),
+                    __ldg(t.port[1] + (v[k].z & 0xFFFFu)));
+                PFW_CHECK(r.x < t.nrows[0] && r.y < t.nrows[1] && r.z < t.nrows[2] && r.w < t.nrows[3]);
+                s_off[warp][k * 32 + lane] = make_uint4(r.x * wp + t.off[0], r.y * wp + t.off[1],
+                                                        r.z * wp + t.off[2], r.w * wp + t.off[3]);
+            }
+            s_res[warp][k * 32 + lane] = PFW_NO_MATCH;
         }
         __syncwarp();
         if (nsteps > 0) {
             // group state: packet pj of the batch (-1: idle, reading the zero
             // line), step s, the four rows' word offsets at this lane's words
             // (s_off holds each packet's row offsets; a lane adds its own lv)
-            // (s_off[warp][32] is the zero line's offset: idle groups point there)
             int pj = grp < nv ? grp : -1;
             int next = P;  // next packet to hand out; every group idle <=> next == nv + P
             int s = 0;
-            const uint32_t s_off_base = (uint32_t)__cvta_generic_to_shared(&s_off[warp][0]);
-            uint4 o = s_off[warp][pj >= 0 ? pj : 32];
+            uint4 o = s_off[warp][pj >= 0 ? pj : B];
             o.x += lv;
             o.y += lv;
             o.z += lv;
@@ -1033,7 +993,7 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
                 // o (predicated shared load), then every lane adds lv (new
                 // packet) or one step (active) or nothing (idle)
                 {
-                    const uint32_t sa = s_off_base + (uint32_t)(take ? np : 32) * 16u;
+                    const uint32_t sa = s_off_base + (uint32_t)(take ? np : B) * 16u;
                     asm volatile(
                         "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
                         "@q ld.shared.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
@@ -1052,28 +1012,15 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
             }
         }
         __syncwarp();
-        if (i < n) {
-            uint32_t res = s_res[warp][lane];
-            if (res != PFW_NO_MATCH) {  // the parked words' first non-zero word, its lowest bit
-                uint32_t x[V];
 #pragma unroll
-                for (int k = 0; k < V; k += 4) {
-                    const uint4 q4 = s_x[warp][lane][k / 4];
-                    x[k] = q4.x;
-                    x[k + 1] = q4.y;
-                    x[k + 2] = q4.z;
-                    x[k + 3] = q4.w;
-                }
-                uint32_t wsel = x[V - 1], widx = V - 1;
-#pragma unroll
-                for (int k = V - 2; k >= 0; k--) {
-                    wsel = x[k] ? x[k] : wsel;
-                    widx = x[k] ? (uint32_t)k : widx;
-                }
-                res = (res + widx) * 32u + (uint32_t)(__ffs(wsel) - 1);
+        for (int k = 0; k < LPB; k++) {
+            const int64_t i = b0 + k * 32 + lane;
+            if (i < n) {
+                uint32_t res = s_res[warp][k * 32 + lane];
+                if (res != PFW_NO_MATCH) res = ms_parked_first_bit<V>(&s_x[warp][k * 32 + lane][0], res);
+                PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
+                emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
             }
-            PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
-            emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
         }
         __syncwarp();
     }
@@ -1737,7 +1684,7 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     // (auto: 4-lane groups with 256-bit loads up to 8K rules -- measured +7% at
     // 4K rules, +10% at 1K; at 10K rules all variants are within 1%, the
     // general kernel is kept there)
-    const int lean = g_ms_lean == 3 ? (h->n <= 2048 ? 2 : 1) : g_ms_lean;
+    const int lean = g_ms_lean == 3 ? (h->n <= 2048 ? 2 : 6) : g_ms_lean;
     // compressed rows, whole table, no summaries: the lean compressed kernel
     // (tuning ms_lean_cmp: 0 off, 1 8-lane groups, 2 4-lane groups / 256-bit loads)
     void (*kern_lc)(ScanParams, MsView, MsCmp, uint32_t) = nullptr;
@@ -1745,15 +1692,16 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
         kern_lc = g_ms_lean_cmp == 2 ? ms_lean_cmp_kernel<MODE, 4> : ms_lean_cmp_kernel<MODE, 8>;
     if (lean && kern && !win && grp == 8 && g_ms_words == 4)
         switch (lean) {
-            // 1: 8-lane groups, 1024-rule steps (cp.async lookup pipeline with ms_prefetch)
-            case 1: kern_l = (g_ms_prefetch && p.pkts) ? ms_lean_kernel<MODE, 8, 4, true, PFW_MS_MINB>
-                                                       : ms_lean_kernel<MODE, 8, 4, false, PFW_MS_MINB>; break;
+            // 1: 8-lane groups, 1024-rule steps, 32-packet batches
+            case 1: kern_l = ms_lean_kernel<MODE, 8, 4, 1, PFW_MS_MINB>; break;
             // 2: 4-lane groups, 256-bit loads, 1024-rule steps, 8 packets per warp
-            case 2: kern_l = ms_lean_kernel<MODE, 4, 8, false, 4>; break;
+            case 2: kern_l = ms_lean_kernel<MODE, 4, 8, 1, 4>; break;
             // 4: 4-lane groups, 512-rule steps (half the bytes per step), 8 packets per warp
-            case 4: kern_l = ms_lean_kernel<MODE, 4, 4, false, PFW_MS_MINB>; break;
+            case 4: kern_l = ms_lean_kernel<MODE, 4, 4, 1, PFW_MS_MINB>; break;
             // 5: as 1 at 6 resident blocks per SM (42 registers)
-            case 5: kern_l = ms_lean_kernel<MODE, 8, 4, false, 6>; break;
+            case 5: kern_l = ms_lean_kernel<MODE, 8, 4, 1, 6>; break;
+            // 6: as 1 with 64-packet batches (half the batch boundaries)
+            case 6: kern_l = ms_lean_kernel<MODE, 8, 4, 2, PFW_MS_MINB>; break;
             default: break;
         }
     int occ = g_ctas_per_sm;

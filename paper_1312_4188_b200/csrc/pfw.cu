@@ -1435,15 +1435,13 @@ int pfw_set_tuning(const char *key, int64_t value) {
     } else if (!strcmp(key, "ms_lean_cmp")) {
         if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_lean_cmp: 0 off, 1 8-lane, 2 4-lane groups");
         g_ms_lean_cmp = (int)value;
-    } else if (!strcmp(key, "ms_prefetch")) {
-        g_ms_prefetch = value != 0;
     } else if (!strcmp(key, "ms_odd_rows")) {
         g_ms_odd_rows = value != 0;
     } else if (!strcmp(key, "ms_lean")) {
-        if (value < 0 || value > 5)
+        if (value < 0 || value > 6)
             return set_err(PFW_ERR_INVALID, "ms_lean: 0 general kernel, 1 lean (8-lane groups), 2 lean (4-lane "
                                             "groups, 256-bit loads), 3 auto, 4 lean (4-lane groups, 512-rule "
-                                            "steps), 5 lean (8-lane groups, 6 blocks per SM)");
+                                            "steps), 5 lean (8-lane groups, 6 blocks per SM), 6 lean (64-packet batches)");
         g_ms_lean = (int)value;
     } else {
         return set_err(PFW_ERR_INVALID, "unknown tuning key '%s'", key);

@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_prefetch", 0), ("ms_lean_cmp", 0)):
+                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_lean_cmp", 1)):
         _native.set_tuning(k, v)
 
 
@@ -631,16 +631,16 @@ def test_match_set_step_shapes(group, words):
     test_fused_min_combine_virtual_ranks(0)
 
 
-@pytest.mark.parametrize("lean,pf", [(0, 1), (1, 1), (1, 0), (2, 0), (4, 0), (5, 0)])
-def test_lean_whole_table_scan(lean, pf):
-    """Whole-table scans over plain rows: the general kernel (0), the lean one
-    (1) and the lean one with L1 no-allocate row loads (2) are bit-exact
+@pytest.mark.parametrize("lean", [0, 1, 2, 4, 5, 6])
+def test_lean_whole_table_scan(lean):
+    """Whole-table scans over plain rows: the general kernel (0) and every
+    lean variant (1: 8-lane groups; 2: 4-lane groups with 256-bit loads; 4:
+    512-rule steps; 5: 6 blocks per SM; 6: 64-packet batches) are bit-exact
     against the reference goldens, ragged batches and the full-size data
     config's strided oracle sample."""
     _native.set_tuning("algo", 2)
     _native.set_tuning("ms_compress", 0)
     _native.set_tuning("ms_lean", lean)
-    _native.set_tuning("ms_prefetch", pf)
     for name, rn, tn in (("oracle_r1000_t100000", "r1000_s1", "t100000_s2"), ("r2048_t1000", "r2048_s21_w15", "t1000_s22"),
                          ("r300_t10000", "r300_s40_w30", "t10000_s41"), ("r64_t600", "r64_s30_w40", "t600_s25"),
                          ("r1000_t3000icmp", "r1000_s1", "t3000_s11_icmp")):
