@@ -531,10 +531,12 @@ def run_ours(args, w, world, rank, local) -> int:
             if fused is not None:
                 fused.run(batch, stats=stats, stream=stream.cuda_stream)
             elif w.model == "function":
-                _native.check(_native.lib().pfw_accumulator_init(m, out_first.data_ptr(), out_comps.data_ptr(),
-                                                                 stream.cuda_stream), "init")
-                compiled.scan_partition_accumulate(batch, 0, compiled.num_rules, out_first, out_comps, stats,
-                                                   stream=stream.cuda_stream)
+                # this rank's shard is ONE partition of the model (engines.py:316-321):
+                # its scan writes the shard-local first match (global index) and the
+                # per-task comparisons directly (no accumulator pass), then the
+                # NCCL MIN / SUM combine across ranks (engines.py:202-212, 359-369)
+                compiled.scan_range_device(batch, 0, compiled.num_rules, first=out_first, comps=out_comps,
+                                           stats=stats, stream=stream.cuda_stream)
                 parallel.function_parallel_combine(out_first, out_comps, None)
             else:
                 compiled.scan_range_device(batch, r_lo, r_hi, first=out_first, comps=out_comps,

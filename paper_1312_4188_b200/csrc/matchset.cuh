@@ -1681,9 +1681,9 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
         return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
     // whole-table scans over plain rows in the default shape: the lean kernel
     void (*kern_l)(ScanParams, MsView, uint32_t) = nullptr;
-    // (auto: 4-lane groups with 256-bit loads up to 8K rules -- measured +7% at
-    // 4K rules, +10% at 1K; at 10K rules all variants are within 1%, the
-    // general kernel is kept there)
+    // (auto, measured on B200: 4-lane groups with 256-bit loads up to 2K rules
+    // (oracle config 5.7 vs 5.3 Gpps), above that 8-lane groups with 64-packet
+    // batches (data 13.65 Gpps vs 12.55 on the general kernel, grid 16.15)
     const int lean = g_ms_lean == 3 ? (h->n <= 2048 ? 2 : 6) : g_ms_lean;
     // compressed rows, whole table, no summaries: the lean compressed kernel
     // (tuning ms_lean_cmp: 0 off, 1 8-lane groups, 2 4-lane groups / 256-bit loads)
