@@ -701,12 +701,12 @@ def run_ours(args, w, world, rank, local) -> int:
     # timed the same way, against the INT32 roofline
     rule_rec = None
     if algo == "matchset" and not args.no_rule_scan and fused is None:
-        # on the first 1/8 of this rank's packets (>= 1Mi): the rule scan is
+        # on the first 1/8 of this rank's packets (>= 4Mi): the rule scan is
         # ~10x slower per packet, so the whole stream would make it the
-        # dominant kernel of the bench command's launch list (its multi-pass
-        # compaction loses a little at smaller batches: 0.676 of the INT32
-        # peak at 64Mi packets, 0.646 at 8Mi)
-        m = min(n, max(1 << 20, n // 8))
+        # dominant kernel of the default bench command's launch list (its
+        # multi-pass compaction loses a little at smaller batches: 0.676 of
+        # the INT32 peak at 64Mi packets, 0.646 at 8Mi)
+        m = min(n, max(1 << 22, n // 8))
         sub = pkts.slice(0, m)
         rstep_ = make_step(sub, first[:m], comps[:m], verdict[:m])
         _native.set_tuning("algo", 1)
