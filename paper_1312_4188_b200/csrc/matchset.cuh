@@ -1047,7 +1047,7 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
 // two or three) read the index from global memory.  Idle groups read the zero
 // line after the last distinct line.
 #ifndef MS_LEAN_PARK
-#define MS_LEAN_PARK 4
+#define MS_LEAN_PARK 6
 #endif
 template <int MODE, int G>
 __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
