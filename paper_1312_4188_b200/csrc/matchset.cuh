@@ -54,6 +54,7 @@ constexpr int64_t MS_CMP_MIN_RULES = 24576;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
+int g_ms_lean_sum = 2;         // whole-table summary scans over compressed rows: lean candidate walk (0 general kernel, 1 at 5 / 2 at 4 blocks per SM)
 int g_ms_lean_cmp = 1;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane
 int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
@@ -1173,6 +1174,208 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
     }
 }
 
+// Lean scan of whole-table windows with BLOCK SUMMARIES over compressed rows
+// (the adversarial config: most blocks hold no rule that can match a packet
+// on every field).  Lookup phase (one packet per lane): the packet's
+// candidate blocks -- set bits of the AND of its four summary rows -- and the
+// four line numbers of the first MS_SUM_PARK of them, parked in shared memory
+// (one 16-byte entry per candidate, the zero line past the last one).  The
+// step loop then walks each packet's list like the lean kernels walk steps:
+// one candidate block per group per iteration, the first-match bit resolved
+// after the loop.  A packet with more candidates than parked ones whose
+// parked blocks all fail continues after the loop, one packet per lane, with
+// the summary search over the remaining blocks (rare: the parked list covers
+// the adversarial recipe's tail).
+#ifndef MS_SUM_PARK
+#define MS_SUM_PARK 6
+#endif
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(MS_BLOCK, MINB)
+    ms_lean_sum_kernel(ScanParams p, MsView t, MsCmp u, uint32_t zline) {
+    constexpr int G = 8, V = 4, P = 4, K = MS_SUM_PARK;
+    // per packet: the candidates' line numbers (the matching candidate's
+    // entry is reused for the finding lane's AND words), blocks, count
+    __shared__ uint4 s_cl[MS_BLOCK / 32][32][K];
+    __shared__ uint16_t s_cb[MS_BLOCK / 32][32][K];
+    __shared__ uint8_t s_nc[MS_BLOCK / 32][32];  // candidates parked | (more << 7)
+    __shared__ uint32_t s_res[MS_BLOCK / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane / G, gl = lane % G, gbase = grp * G;
+    const uint32_t lv = (uint32_t)gl * V;
+    const unsigned below = (1u << gl) - 1u;
+    const unsigned groups_below = (1u << gbase) - 1u;
+    const int64_t gw = ((int64_t)blockIdx.x * MS_BLOCK + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * MS_BLOCK) >> 5;
+    const int64_t n = p.n;
+    const uint32_t span = (uint32_t)(p.win_hi > p.win_lo ? p.win_hi - p.win_lo : 0);
+    const bool empty = p.lo >= p.hi;
+    const uint32_t kb1 = empty ? 0u : (uint32_t)((p.hi - 1) >> 10);  // last block of the window
+    const uint32_t *lines = u.lines;
+    const uint4 zq = make_uint4(zline, zline, zline, zline);
+    unsigned long long st_sum = 0, st_blocks = 0;
+    unsigned st_max = 0;
+
+    for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
+        const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
+        const int64_t i = b0 + lane;
+        int nc = 0, more = 0;
+        if (i < n && !empty) {
+            uint4 v;
+            if (p.pkts) {
+                v = __ldcs(p.pkts + i);
+            } else {
+                v.x = __ldcs(p.cols.src + i);
+                v.y = __ldcs(p.cols.dst + i);
+                v.z = ((uint32_t)__ldcs(p.cols.sport + i) << 16) | (uint32_t)__ldcs(p.cols.dport + i);
+                v.w = __ldcs(p.cols.proto + i);
+            }
+            const uint32_t rr[4] = {ms_ip_row(t.ipb[0], t.ipc[0], v.x), ms_ip_row(t.ipb[1], t.ipc[1], v.y),
+                                    (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
+                                    __ldg(t.port[1] + (v.z & 0xFFFFu))};
+            PFW_CHECK(rr[0] < t.nrows[0] && rr[1] < t.nrows[1] && rr[2] < t.nrows[2] && rr[3] < t.nrows[3]);
+            for (uint32_t w = 0; w <= kb1 / 32u && !more; w++) {
+                uint32_t a = __ldg(u.sum[0] + (size_t)rr[0] * u.sw + w) & __ldg(u.sum[1] + (size_t)rr[1] * u.sw + w) &
+                             __ldg(u.sum[2] + (size_t)rr[2] * u.sw + w) & __ldg(u.sum[3] + (size_t)rr[3] * u.sw + w);
+                const int rel1 = (int)kb1 - 32 * (int)w;
+                a &= rel1 >= 31 ? 0xFFFFFFFFu : ((2u << rel1) - 1u);
+                while (a) {
+                    if (nc == K) {
+                        more = 1;
+                        break;
+                    }
+                    const uint32_t b = 32u * w + (uint32_t)(__ffs(a) - 1);
+                    a &= a - 1u;
+                    uint32_t q[4];
+#pragma unroll
+                    for (int d = 0; d < 4; d++) {
+                        const uint16_t ix = b < 8u ? __ldg(u.head + u.head_off[d] + (size_t)rr[d] * 8 + b)
+                                                   : __ldg(u.ptr + u.ptr_off[d] + (size_t)rr[d] * u.pstride + b);
+                        q[d] = __ldg(u.loff + d * u.nblk + b) + ix;
+                    }
+                    s_cl[warp][lane][nc] = make_uint4(q[0], q[1], q[2], q[3]);
+                    s_cb[warp][lane][nc] = (uint16_t)b;
+                    nc++;
+                }
+            }
+        }
+        if (nc == 0) s_cl[warp][lane][0] = zq;  // an empty list: its first entry is the zero line
+        s_nc[warp][lane] = (uint8_t)(nc | (more << 7));
+        s_res[warp][lane] = PFW_NO_MATCH;
+        __syncwarp();
+        {
+            // group state: packet pj (-1 idle), candidate ck of its list, the
+            // candidate's four line numbers q (+ this lane's words)
+            int pj = grp < nv ? grp : -1;
+            int next = P;
+            int ck = 0;
+            uint4 q = pj >= 0 ? s_cl[warp][pj][0] : zq;
+            int pnc = pj >= 0 ? (int)(s_nc[warp][pj] & 0x7F) : 0;
+            while (next < nv + P) {
+                uint32_t w[4][V];
+                ms_load_rows<V>(lines + ((size_t)q.x << 5) + lv, lines + ((size_t)q.y << 5) + lv,
+                                lines + ((size_t)q.z << 5) + lv, lines + ((size_t)q.w << 5) + lv, w);
+                uint32_t x[V], any = 0u;
+#pragma unroll
+                for (int k = 0; k < V; k++) {
+                    x[k] = w[0][k] & w[1][k] & w[2][k] & w[3][k];
+                    any |= x[k];
+                }
+                const unsigned bal = __ballot_sync(0xFFFFFFFFu, any != 0u);
+                const unsigned gbits = (bal >> gbase) & ((1u << G) - 1u);
+                const bool act = pj >= 0;
+                if (any != 0u && (gbits & below) == 0u) {  // park the words: the bit is resolved after the loop
+                    // block, list slot, lane words (< 2^31: never PFW_NO_MATCH)
+                    s_res[warp][pj] = ((uint32_t)s_cb[warp][pj][ck] << 8) | (uint32_t)ck | (lv << 24);
+                    s_cl[warp][pj][ck] = make_uint4(x[0], x[1], x[2], x[3]);
+                }
+                if (act && gl == 0 && p.blocks_read) st_blocks++;
+                // done: matched, or the parked list is exhausted (the fallback
+                // after the loop takes packets with more candidates)
+                const bool done = act && (gbits != 0u || ck + 1 >= pnc);
+                const unsigned dm = __ballot_sync(0xFFFFFFFFu, done && gl == 0);
+                const int np = next + __popc(dm & groups_below);
+                const bool take = np < nv;
+                // the next candidate: a new packet's first, or this packet's next
+                // (an empty list's first entry is the zero line: it ends at once)
+                const int ci = done ? (take ? np : 0) : (pj & 31);
+                const int cj = done ? 0 : ck + 1;
+                const uint4 qn = s_cl[warp][ci][cj < K ? cj : 0];
+                const bool idle_next = done ? !take : !act;
+                q = idle_next ? zq : qn;
+                pnc = done ? (take ? (int)(s_nc[warp][np] & 0x7F) : 0) : pnc;
+                ck = cj;
+                pj = done ? (take ? np : -1) : pj;
+                next += __popc(dm);
+            }
+        }
+        __syncwarp();
+        if (i < n) {
+            uint32_t res = s_res[warp][lane];
+            if (res != PFW_NO_MATCH) {  // (block << 8 | list slot | lv << 24): the parked words' first bit
+                const uint32_t blk = (res >> 8) & 0xFFFFu, slot = res & 0xFFu, wl = res >> 24;
+                res = ms_parked_first_bit<V>(&s_cl[warp][lane][slot], blk * 32u + wl);
+            } else if (s_nc[warp][lane] & 0x80) {
+                // more candidates than parked, none of the parked ones matched:
+                // continue the summary search after the last parked block, this
+                // lane alone, a whole line (32 words) per row and block
+                uint4 v;
+                if (p.pkts) {
+                    v = __ldg(p.pkts + i);
+                } else {
+                    v.x = __ldg(p.cols.src + i);
+                    v.y = __ldg(p.cols.dst + i);
+                    v.z = ((uint32_t)__ldg(p.cols.sport + i) << 16) | (uint32_t)__ldg(p.cols.dport + i);
+                    v.w = __ldg(p.cols.proto + i);
+                }
+                const uint32_t rr[4] = {ms_ip_row(t.ipb[0], t.ipc[0], v.x), ms_ip_row(t.ipb[1], t.ipc[1], v.y),
+                                        (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
+                                        __ldg(t.port[1] + (v.z & 0xFFFFu))};
+                uint32_t b = (uint32_t)s_cb[warp][lane][K - 1] + 1u;
+                for (; b <= kb1 && res == PFW_NO_MATCH; b++) {
+                    const uint32_t wsum = b / 32u, bit = 1u << (b % 32u);
+                    if (!(__ldg(u.sum[0] + (size_t)rr[0] * u.sw + wsum) & __ldg(u.sum[1] + (size_t)rr[1] * u.sw + wsum) &
+                          __ldg(u.sum[2] + (size_t)rr[2] * u.sw + wsum) & __ldg(u.sum[3] + (size_t)rr[3] * u.sw + wsum) & bit))
+                        continue;
+                    if (p.blocks_read) st_blocks++;
+                    const uint32_t *lp[4];
+#pragma unroll
+                    for (int d = 0; d < 4; d++) {
+                        const uint16_t ix = b < 8u ? __ldg(u.head + u.head_off[d] + (size_t)rr[d] * 8 + b)
+                                                   : __ldg(u.ptr + u.ptr_off[d] + (size_t)rr[d] * u.pstride + b);
+                        lp[d] = lines + ((size_t)(__ldg(u.loff + d * u.nblk + b) + ix) << 5);
+                    }
+                    for (uint32_t wd = 0; wd < 32u; wd++) {
+                        const uint32_t xa = __ldg(lp[0] + wd) & __ldg(lp[1] + wd) & __ldg(lp[2] + wd) & __ldg(lp[3] + wd);
+                        if (xa) {
+                            res = (b * 32u + wd) * 32u + (uint32_t)(__ffs(xa) - 1);
+                            break;
+                        }
+                    }
+                }
+            }
+            PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
+            emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
+        }
+        __syncwarp();
+    }
+    if (p.stats) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            st_sum += __shfl_xor_sync(0xFFFFFFFFu, st_sum, o);
+            st_max = max(st_max, __shfl_xor_sync(0xFFFFFFFFu, st_max, o));
+        }
+        if (lane == 0) {
+            if (st_sum) atomicAdd(&p.stats[0], st_sum);
+            if (st_max) atomicMax(&p.stats[1], (unsigned long long)st_max);
+        }
+    }
+    if (p.blocks_read) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) st_blocks += __shfl_xor_sync(0xFFFFFFFFu, st_blocks, o);
+        if (lane == 0 && st_blocks) atomicAdd(p.blocks_read, st_blocks);
+    }
+}
+
 void ms_free(MatchSet *m) {
     if (!m) return;
     if (m->d_bits_all) cudaFree(m->d_bits_all);
@@ -1690,6 +1893,9 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     void (*kern_lc)(ScanParams, MsView, MsCmp, uint32_t) = nullptr;
     if (g_ms_lean_cmp && kern_c && !sum && !win)
         kern_lc = g_ms_lean_cmp == 2 ? ms_lean_cmp_kernel<MODE, 4> : ms_lean_cmp_kernel<MODE, 8>;
+    // block summaries over compressed rows, whole table: the lean candidate walk
+    if (g_ms_lean_sum && kern_c && sum && !win)
+        kern_lc = g_ms_lean_sum == 2 ? ms_lean_sum_kernel<MODE, 4> : ms_lean_sum_kernel<MODE, PFW_MS_MINB>;
     if (lean && kern && !win && grp == 8 && g_ms_words == 4)
         switch (lean) {
             // 1: 8-lane groups, 1024-rule steps, 32-packet batches
@@ -1730,7 +1936,7 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
             CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, kern_lc, MS_BLOCK, 0));
             grid = std::min<int64_t>((int64_t)h->sms * std::max(o2, 1), need);
         }
-        kern_lc<<<(unsigned)grid, MS_BLOCK, 0, st>>>(p, t, uc, (uint32_t)m->nlines);
+        kern_lc<<<(unsigned)grid, MS_BLOCK, 0, st>>>(sum ? pc : p, t, uc, (uint32_t)m->nlines);
     } else if (kern_l) {
         // word offset of the zero padding after the src rows (idle groups read it)
         const uint32_t zoff = (uint32_t)((m->d_bits[0] - m->d_bits_all) + m->rows[0] * m->wp);

@@ -1432,6 +1432,9 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value != 0 && value != 8 && value != 16 && value != 32)
             return set_err(PFW_ERR_INVALID, "ms_group: 0 (auto), 8, 16 or 32");
         g_ms_group = (int)value;
+    } else if (!strcmp(key, "ms_lean_sum")) {
+        if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_lean_sum: 0 off, 1 on, 2 on at 4 blocks per SM");
+        g_ms_lean_sum = (int)value;
     } else if (!strcmp(key, "ms_lean_cmp")) {
         if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_lean_cmp: 0 off, 1 8-lane, 2 4-lane groups");
         g_ms_lean_cmp = (int)value;
