@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_lean_cmp", 1)):
+                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_lean_cmp", 1), ("ms_lean_sum", 2)):
         _native.set_tuning(k, v)
 
 
@@ -960,3 +960,16 @@ def test_classify_host_ramped_chunk_schedule(n):
     np.testing.assert_array_equal(v, np.where(dev_first >= 0, rules["action_accept"][np.maximum(dev_first, 0)], False))
     comps = oracle.sequential_comparisons(dev_first, 4096)
     assert st.tolist() == [int(comps.sum()), int(comps.max())]
+
+
+@pytest.mark.parametrize("lean_sum", [0, 1, 2])
+def test_summary_scan_kernels(lean_sum):
+    """Whole-table summary scans over compressed rows on the general kernel (0)
+    and the lean candidate walk (1: 5 blocks per SM, 2: 4): the adversarial
+    recipe, scans whose candidates outnumber the parked ones (the lane-serial
+    continuation after the loop), forced summaries on goldens -- identical."""
+    _native.set_tuning("ms_lean_sum", lean_sum)
+    test_adversarial_recipe_sample()
+    test_summary_candidates_past_the_parked_ones()
+    test_compressed_rows_forced()
+    test_match_set_block_summaries(1)
