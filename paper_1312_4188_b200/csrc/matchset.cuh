@@ -1058,7 +1058,8 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
     __shared__ uint4 s_ln[MS_BLOCK / 32][32][K];  // per packet: line numbers of blocks 0..K-1 (x..w = dimension)
     __shared__ uint4 s_row[MS_BLOCK / 32][32];    // per packet: its four rows (blocks >= K)
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];
-    __shared__ uint4 s_x[MS_BLOCK / 32][32][V / 4];  // per packet: the finding lane's AND words
+    // (a finished packet's line-number slots are reused for the finding lane's AND words)
+    static_assert(V / 4 <= K, "the parked words fit the packet's line-number slots");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const uint32_t lv = (uint32_t)gl * V;
@@ -1092,17 +1093,20 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
                                     __ldg(t.port[1] + (v.z & 0xFFFFu))};
             PFW_CHECK(rr[0] < t.nrows[0] && rr[1] < t.nrows[1] && rr[2] < t.nrows[2] && rr[3] < t.nrows[3]);
             s_row[warp][lane] = make_uint4(rr[0], rr[1], rr[2], rr[3]);
-            uint32_t ln[4][K];
+            uint4 hq[4];  // each dimension's head entry: the first 8 blocks' u16 line indices
 #pragma unroll
-            for (int d = 0; d < 4; d++) {
-                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(u.head + u.head_off[d] + (size_t)rr[d] * 8));
-                const uint32_t qq[4] = {q.x, q.y, q.z, q.w};
+            for (int d = 0; d < 4; d++)
+                hq[d] = __ldg(reinterpret_cast<const uint4 *>(u.head + u.head_off[d] + (size_t)rr[d] * 8));
 #pragma unroll
-                for (int j = 0; j < K; j++)
-                    ln[d][j] = __ldg(u.loff + d * u.nblk + j) + ((qq[j >> 1] >> (16 * (j & 1))) & 0xFFFFu);
+            for (int j = 0; j < K; j++) {
+                uint32_t l[4];
+#pragma unroll
+                for (int d = 0; d < 4; d++) {
+                    const uint32_t h2 = (j >> 1) == 0 ? hq[d].x : (j >> 1) == 1 ? hq[d].y : (j >> 1) == 2 ? hq[d].z : hq[d].w;
+                    l[d] = __ldg(u.loff + d * u.nblk + j) + ((h2 >> (16 * (j & 1))) & 0xFFFFu);
+                }
+                s_ln[warp][lane][j] = make_uint4(l[0], l[1], l[2], l[3]);
             }
-#pragma unroll
-            for (int j = 0; j < K; j++) s_ln[warp][lane][j] = make_uint4(ln[0][j], ln[1][j], ln[2][j], ln[3][j]);
         }
         s_res[warp][lane] = PFW_NO_MATCH;
         __syncwarp();
@@ -1126,7 +1130,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
                 if (any != 0u && (gbits & below) == 0u) {  // park the words; the bit is resolved after the loop
                     s_res[warp][pj] = (uint32_t)s * 32u + lv;
 #pragma unroll
-                    for (int k = 0; k < V; k += 4) s_x[warp][pj][k / 4] = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
+                    for (int k = 0; k < V; k += 4) s_ln[warp][pj][k / 4] = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
                 }
                 const bool act = pj >= 0;
                 const bool done = act && (gbits != 0u || s + 1 >= nsteps);
@@ -1155,7 +1159,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
         __syncwarp();
         if (i < n) {
             uint32_t res = s_res[warp][lane];
-            if (res != PFW_NO_MATCH) res = ms_parked_first_bit<V>(&s_x[warp][lane][0], res);
+            if (res != PFW_NO_MATCH) res = ms_parked_first_bit<V>(&s_ln[warp][lane][0], res);
             PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
             emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
         }
