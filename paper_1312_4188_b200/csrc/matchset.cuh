@@ -235,8 +235,8 @@ struct MsView {
     const uint32_t *bits0;    // the four dimensions' rows, one allocation
     uint32_t off[4];          // word offset of each dimension's rows from bits0
     const uint32_t *ipb[2];   // src / dst boundaries
-    const uint2 *ipc[2];      // per /16 block: [first, end) boundary index
-    const uint32_t *port[2];  // sport / dport -> interval
+    const uint32_t *ipc[2];   // per /16 block: first boundary index | count << 24 (65537 entries)
+    const uint16_t *port[2];  // sport / dport -> interval
     const uint8_t *cls;       // protocol -> class
     int64_t wp;
     uint32_t sp_rows;
@@ -269,10 +269,14 @@ struct MsArg {
     using type = std::conditional_t<CMP, MsCmp, std::conditional_t<SUM, MsSum, MsNoSum>>;
 };
 
-// interval of an IP: index of the last boundary <= ip (boundary 0 is 0)
-__device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint2 *c, uint32_t ip) {
-    const uint2 k = __ldg(c + (ip >> 16));
-    uint32_t lo = k.x, hi = k.y;
+// interval of an IP: index of the last boundary <= ip (boundary 0 is 0).
+// c[ip >> 16] packs the /16 block's first boundary index (24 bits) and its
+// boundary count (8 bits; 255: up to the next block's first); 4-byte entries
+// and 2-byte port entries keep the lookup tables small enough to stay in L1
+__device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint32_t *c, uint32_t ip) {
+    const uint32_t k = __ldg(c + (ip >> 16));
+    uint32_t lo = k & 0xFFFFFFu;
+    uint32_t hi = (k >> 24) == 255u ? (__ldg(c + (ip >> 16) + 1) & 0xFFFFFFu) : lo + (k >> 24);
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (__ldg(b + mid) <= ip) lo = mid + 1;
@@ -1644,7 +1648,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     m->rows[MSD_DPORT] = (int64_t)bdp.size();
     size_t bytes = 0;
     for (int d = 0; d < 4; d++) bytes += (size_t)m->rows[d] * (size_t)m->wp * 4;
-    bytes += (bs.size() + bd.size()) * 4 + 2 * 65536 * (8 + 4) + 256;
+    bytes += (bs.size() + bd.size()) * 4 + 2 * 65537 * 4 + 2 * 65536 * 2 + 256;
     m->bytes = bytes;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
@@ -1657,12 +1661,13 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     // rows do not fit -- ~20x smaller; slower than plain rows only while
     // those stay L2-friendly (<= ~24K rules)
     const bool use_cmp = g_ms_compress == 1 || (g_ms_compress == 2 && (!fits || n > MS_CMP_MIN_RULES));
-    if (!fits && !use_cmp) {
+    // (boundary indices are packed in 24 bits: beyond ~8M rules the ruleset scans rule by rule)
+    if ((!fits && !use_cmp) || bs.size() >= (1u << 24) || bd.size() >= (1u << 24)) {
         delete m;
         return PFW_OK;  // too large for the budget: rule-by-rule scan
     }
     // lookup tables
-    std::vector<uint2> ipc[2];
+    std::vector<uint32_t> ipc[2];
     const std::vector<uint32_t> *ipb[2] = {&bs, &bd};
     for (int d = 0; d < 2; d++) {
         const std::vector<uint32_t> &b = *ipb[d];
@@ -1673,17 +1678,20 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
             c[blk] = (uint32_t)k;
         }
         c[65536] = (uint32_t)b.size();
-        ipc[d].resize(65536);
-        for (uint32_t blk = 0; blk < 65536; blk++) ipc[d][blk] = make_uint2(c[blk], c[blk + 1]);
+        ipc[d].resize(65537);
+        for (uint32_t blk = 0; blk <= 65536; blk++) {
+            const uint32_t cnt = blk < 65536 ? c[blk + 1] - c[blk] : 0u;
+            ipc[d][blk] = c[blk] | ((cnt < 255u ? cnt : 255u) << 24);
+        }
     }
-    std::vector<uint32_t> ptab[2];
+    std::vector<uint16_t> ptab[2];
     const std::vector<uint32_t> *pb[2] = {&bsp, &bdp};
     for (int d = 0; d < 2; d++) {
         ptab[d].resize(65536);
         size_t k = 0;
         for (uint32_t v = 0; v < 65536; v++) {
             while (k + 1 < pb[d]->size() && (*pb[d])[k + 1] <= v) k++;
-            ptab[d][v] = (uint32_t)k;
+            ptab[d][v] = (uint16_t)k;  // (port intervals <= 65536)
         }
     }
     // device copies of the rule columns (build only)

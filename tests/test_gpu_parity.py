@@ -973,3 +973,23 @@ def test_summary_scan_kernels(lean_sum):
     test_summary_candidates_past_the_parked_ones()
     test_compressed_rows_forced()
     test_match_set_block_summaries(1)
+
+
+def test_many_ip_boundaries_in_one_slash16():
+    """More than 255 IP interval boundaries inside one /16 block: the packed
+    lookup entry's count saturates and the search runs up to the next block's
+    first boundary -- identical to the oracle (src and dst, /32 .. /24 rules)."""
+    rng = np.random.default_rng(11)
+    R = 1500
+    rules = oracle.gen_ruleset(R, 77, wp=0.2)
+    plen = rng.integers(24, 33, R)
+    mask = np.where(plen == 32, 0xFFFFFFFF, (0xFFFFFFFF << (32 - plen)) & 0xFFFFFFFF).astype(np.uint32)
+    base = (np.uint32(0x0A0B0000) | rng.integers(0, 1 << 16, R).astype(np.uint32)) & mask
+    rules["src_base"], rules["src_mask"] = base, mask
+    rules["dst_base"], rules["dst_mask"] = base[::-1].copy(), mask[::-1].copy()
+    pk = oracle.gen_traffic_uniform(50_000, 5)
+    pk["src_ip"][:40_000] = 0x0A0B0000 | rng.integers(0, 1 << 16, 40_000).astype(np.uint32)
+    pk["dst_ip"][10_000:] = 0x0A0B0000 | rng.integers(0, 1 << 16, 40_000).astype(np.uint32)
+    c, p = compiled(rules), dev_pkts(pk)
+    assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
+    np.testing.assert_array_equal(c.scan_range(p, 0, R), oracle.scan_range(rules, pk, 0, R))
