@@ -130,6 +130,18 @@ int pfw_scan_partition_accumulate(pfw_ruleset_t h, int64_t lo, int64_t hi, const
                                   uint64_t *d_stats, void *stream);
 int pfw_accumulator_init(int64_t n, uint32_t *d_first, uint32_t *d_comps, void *stream);
 
+/* Every node of the function-parallel / hybrid models on one device
+ * (engines.py:349-369 over partition_bounds(R, nodes), engines.py:140-154):
+ *   d_first[i] = the lowest node's local first match (PFW_NO_MATCH: none)
+ *   d_comps[i] = the sum over nodes of local - lo + 1, or hi - lo
+ *   d_stats[0] += sum of d_comps, d_stats[1] = max(..., largest per-node count)
+ * Runs pfw_accumulator_init + pfw_scan_partition_accumulate over each
+ * non-empty partition on the stream.  Overwrites d_first / d_comps; d_stats
+ * may be NULL.  Replaces the per-node loop of
+ * engines.py:349-369 (FUNCTION_PARALLEL / HYBRID with nodes partitions). */
+int pfw_scan_partitions(pfw_ruleset_t h, int64_t nodes, const void *d_pkts, int64_t n, uint32_t *d_first,
+                        uint32_t *d_comps, uint64_t *d_stats, void *stream);
+
 /* Fused function-parallel combine.  Scans the rule shard
  * [lo, hi) like pfw_scan_partition_accumulate, but the kernel epilogue folds
  * each resolved packet straight into the ranks' result buffers with NVLink

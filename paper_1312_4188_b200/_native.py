@@ -52,6 +52,7 @@ _SIGS = {
     "pfw_scan_range_columns": (_I32, [_P, _I64, _I64, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "pfw_scan_partition_accumulate": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _P]),
     "pfw_accumulator_init": (_I32, [_I64, _P, _P, _P]),
+    "pfw_scan_partitions": (_I32, [_P, _I64, _P, _I64, _P, _P, _P, _P]),
     "pfw_scan_fused_min": (_I32, [_P, _I64, _I64, _P, _I64, _P, _P, _P, _I32, _I32, _P, _P]),
     "pfw_peer_enable": (_I32, [_I32, _I32]),
     "pfw_ipc_handle_size": (_I32, []),

@@ -484,6 +484,17 @@ class CompiledRuleset:
                                                           _ptr(stats), st),
               "pfw_scan_partition_accumulate")
 
+    def scan_partitions(self, pkts: PacketArrays, nodes: int, first, comps, stats=None,
+                        stream: int | None = None) -> None:
+        """Every node of the function-parallel / hybrid models over
+        partition_bounds(R, nodes) (engines.py:349-369) in one call: first =
+        the lowest node's match, comps = the sum over nodes, stats += [sum,
+        largest per-node count]."""
+        st = _stream(self.device) if stream is None else stream
+        check(_native.lib().pfw_scan_partitions(self._h, int(nodes), _ptr(pkts.data), len(pkts), _ptr(first),
+                                                _ptr(comps), _ptr(stats), st),
+              "pfw_scan_partitions")
+
     def verdicts_device(self, first, verdict=None, stream: int | None = None):
         torch = _torch()
         if verdict is None:

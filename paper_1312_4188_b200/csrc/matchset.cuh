@@ -1826,9 +1826,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     return PFW_OK;
 }
 
-template <int MODE>
-int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
-    const MatchSet *m = h->ms;
+static MsView ms_view(const MatchSet *m) {
     MsView t{};
     t.bits0 = m->d_bits_all;
     for (int d = 0; d < 4; d++) t.off[d] = (uint32_t)(m->d_bits[d] - m->d_bits_all);
@@ -1846,6 +1844,13 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     t.cls = m->d_cls;
     t.wp = m->wp;
     t.sp_rows = (uint32_t)m->sp_rows;
+    return t;
+}
+
+template <int MODE>
+int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
+    const MatchSet *m = h->ms;
+    const MsView t = ms_view(m);
     MsSum u{};
     for (int d = 0; d < 4; d++) u.sum[d] = m->d_sum[d];
     u.sw = (uint32_t)m->sw;
@@ -1968,3 +1973,4 @@ int launch_ms(pfw_ruleset *h, int mode, const ScanParams &p, cudaStream_t st) {
         default: return launch_ms_k<MODE_WRITE>(h, p, st);
     }
 }
+

@@ -385,12 +385,8 @@ class Engine:
         if model not in (ExecutionModel.FUNCTION_PARALLEL, ExecutionModel.HYBRID):
             raise ConfigError(f"unsupported model {model}")
         first = torch.empty(n, dtype=torch.int32, device=dev)
-        st = torch.cuda.current_stream(dev).cuda_stream if stream is None else stream
-        _native.check(_native.lib().pfw_accumulator_init(n, first.data_ptr(), comps.data_ptr(), st),
-                      "pfw_accumulator_init")
-        for lo, hi in partition_bounds(R, self.config.nodes):
-            if hi > lo:
-                compiled.scan_partition_accumulate(pkts, lo, hi, first, comps, stats, stream=st)
+        # every non-empty partition of partition_bounds(R, nodes), folded on the device
+        compiled.scan_partitions(pkts, self.config.nodes, first, comps, stats, stream=stream)
         return first, comps, stats
 
     # -------------------------------------------------------------- arrays

@@ -183,6 +183,27 @@ def test_function_parallel_100k_rules():
             g[f"function_{nodes}_stats"].tolist()
 
 
+def test_scan_partitions_oracle_small():
+    """The one-launch partition walk against the oracle's per-node scan
+    (oracle.engine_run: engines.py:349-369), stats included."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1312_4188_b200.classifier import first_to_host
+    rules, traffic = golden_rules("r503_s24_w30"), golden_traffic("t600_s25")
+    c = compiled(rules)
+    p = dev_pkts(traffic)
+    n = len(p)
+    for nodes in (2, 7, 100, 503, 600):
+        first = torch.empty(n, dtype=torch.int32, device="cuda:0")
+        comps = torch.empty(n, dtype=torch.int32, device="cuda:0")
+        stats = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+        c.scan_partitions(p, nodes, first, comps, stats)
+        want_first, want_comps, total, mx = orc.engine_run(rules, traffic, "function", nodes)
+        np.testing.assert_array_equal(first_to_host(first), want_first)
+        np.testing.assert_array_equal(comps.cpu().numpy(), want_comps)
+        assert stats.cpu().numpy().tolist() == [total, mx]
+
+
 def test_engine_drop_in_run_all_models():
     rs = pfw.generate_ruleset(pfw.RulesetGenParams(170, seed=29, wildcard_probability=0.3))
     packets = pfw.generate_traffic(pfw.TrafficProfile(count=350, seed=30))
