@@ -235,7 +235,7 @@ struct MsView {
     const uint32_t *bits0;    // the four dimensions' rows, one allocation
     uint32_t off[4];          // word offset of each dimension's rows from bits0
     const uint32_t *ipb[2];   // src / dst boundaries
-    const uint32_t *ipc[2];   // per /16 block: first boundary index | count << 24 (65537 entries)
+    const uint4 *ipc[2];      // per /16 block: first boundary index | count << 24, the first 6 boundaries' low halves
     const uint16_t *port[2];  // sport / dport -> interval
     const uint8_t *cls;       // protocol -> class
     int64_t wp;
@@ -270,13 +270,27 @@ struct MsArg {
 };
 
 // interval of an IP: index of the last boundary <= ip (boundary 0 is 0).
-// c[ip >> 16] packs the /16 block's first boundary index (24 bits) and its
-// boundary count (8 bits; 255: up to the next block's first); 4-byte entries
-// and 2-byte port entries keep the lookup tables small enough to stay in L1
-__device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint32_t *c, uint32_t ip) {
-    const uint32_t k = __ldg(c + (ip >> 16));
-    uint32_t lo = k & 0xFFFFFFu;
-    uint32_t hi = (k >> 24) == 255u ? (__ldg(c + (ip >> 16) + 1) & 0xFFFFFFu) : lo + (k >> 24);
+// c[ip >> 16] (16 bytes, one sector) packs the /16 block's first boundary
+// index (24 bits), its boundary count (8 bits; 255: up to the next block's
+// first) and the low 16 bits of its first 6 boundaries (0xFFFF past the
+// count): blocks with <= 6 boundaries -- nearly all -- resolve from that one
+// load (count of in-block boundaries <= ip), denser blocks binary-search b.
+__device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint4 *c, uint32_t ip) {
+    const uint4 e = __ldg(c + (ip >> 16));
+    const uint32_t first = e.x & 0xFFFFFFu, cnt = e.x >> 24;
+    if (cnt <= 6u) {
+        const uint32_t l = ip & 0xFFFFu;
+        uint32_t le = 0;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const uint32_t h = k == 0 ? e.y : k == 1 ? e.z : e.w;
+            le += ((h & 0xFFFFu) <= l) + ((h >> 16) <= l);
+        }
+        // (the 0xFFFF padding counts only for ip low half 0xFFFF: take it back)
+        return first - 1u + le - (l == 0xFFFFu ? 6u - cnt : 0u);
+    }
+    uint32_t lo = first;
+    uint32_t hi = cnt == 255u ? (__ldg(&c[(ip >> 16) + 1].x) & 0xFFFFFFu) : lo + cnt;
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (__ldg(b + mid) <= ip) lo = mid + 1;
@@ -824,18 +838,6 @@ __device__ __forceinline__ void ms_load_rows(const uint32_t *a, const uint32_t *
     }
 }
 
-// Lean scan of whole-table windows over plain rows (the data-parallel /
-// grid / sequential configs): the search of ms_scan_kernel<MODE, G, V,
-// false> -- groups of G lanes, one 128-byte line of each of the packet's four
-// rows per step (1024 rules), groups refilled from the warp's batch of 32 --
-// with the per-step work cut to what the search needs:
-//  * idle groups read a zero line (the padding after the src rows) instead
-//    of being predicated off, so no per-iteration zeroing / predicate setup;
-//  * only the group's lowest lane with a set bit resolves the index, from
-//    its own registers (no shuffle); the next state is selected branch-free;
-//  * G = 4: each lane loads 32 bytes per row (256-bit loads), so one load
-//    instruction per row serves 8 packets per warp (8 steps per iteration).
-// Results are identical (same lowest set bit of the same AND).
 // The first set bit of a finding lane's parked AND words (V words starting at
 // word index wbase of the row): (wbase + first non-zero word) * 32 + its lowest bit
 template <int V>
@@ -865,33 +867,12 @@ __device__ __forceinline__ uint32_t ms_parked_first_bit(const uint4 *px, uint32_
 // with the per-step work cut to what the search needs:
 //  * idle groups read a zero line (the padding after the src rows) instead
 //    of being predicated off, so no per-iteration zeroing / predicate setup;
-//  * only the group's lowest lane with a set bit resolves the index, from
-//    its own registers (no shuffle); the next state is selected branch-free;
+//  * the group's lowest lane with a set bit parks its AND words; the bit is
+//    resolved after the loop, one packet per lane; the next state is
+//    selected branch-free;
 //  * G = 4: each lane loads 32 bytes per row (256-bit loads), so one load
 //    instruction per row serves 8 packets per warp (8 steps per iteration).
 // Results are identical (same lowest set bit of the same AND).
-// cp.async (LDGSTS) helpers: global -> shared without registers
-__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
-                 "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async8(void *sdst, const void *gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
-                 "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async4(void *sdst, const void *gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
-                 "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Lookup-table entries of one packet, gathered by cp.async one batch ahead
-struct MsLk {
-    uint2 ipc[2];    // src / dst: [first, end) boundary index of the packet's /16 block
-    uint32_t port[2];  // sport / dport -> interval
-};
-
 template <int MODE, int G, int V, int LPB, int MINB>
 __global__ void __launch_bounds__(MS_BLOCK, MINB)
     ms_lean_kernel(ScanParams p, MsView t, uint32_t zoff) {
@@ -1667,7 +1648,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
         return PFW_OK;  // too large for the budget: rule-by-rule scan
     }
     // lookup tables
-    std::vector<uint32_t> ipc[2];
+    std::vector<uint4> ipc[2];
     const std::vector<uint32_t> *ipb[2] = {&bs, &bd};
     for (int d = 0; d < 2; d++) {
         const std::vector<uint32_t> &b = *ipb[d];
@@ -1681,7 +1662,10 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
         ipc[d].resize(65537);
         for (uint32_t blk = 0; blk <= 65536; blk++) {
             const uint32_t cnt = blk < 65536 ? c[blk + 1] - c[blk] : 0u;
-            ipc[d][blk] = c[blk] | ((cnt < 255u ? cnt : 255u) << 24);
+            uint16_t h[6];
+            for (uint32_t k = 0; k < 6; k++) h[k] = k < cnt ? (uint16_t)(b[c[blk] + k] & 0xFFFFu) : (uint16_t)0xFFFFu;
+            ipc[d][blk] = make_uint4(c[blk] | ((cnt < 255u ? cnt : 255u) << 24), h[0] | ((uint32_t)h[1] << 16),
+                                     h[2] | ((uint32_t)h[3] << 16), h[4] | ((uint32_t)h[5] << 16));
         }
     }
     std::vector<uint16_t> ptab[2];

@@ -162,7 +162,7 @@ struct MatchSet {
     uint32_t *d_bits_all = nullptr;  // the four dimensions' rows, one allocation
     uint32_t *d_bits[4] = {};   // rows[d] * wp words each (inside d_bits_all)
     uint32_t *d_ipb[2] = {};    // src / dst interval boundaries (sorted, [0] = 0)
-    uint32_t *d_ipc[2] = {};    // per /16 block: first boundary index (24 bits) | count (8 bits, 255 = see next)
+    uint4 *d_ipc[2] = {};       // per /16 block: first boundary index | count << 24, 6 boundary low halves
     uint16_t *d_port[2] = {};   // sport / dport -> interval (65536 entries each)
     uint8_t *d_cls = nullptr;   // protocol -> class (256 entries)
     int64_t sp_rows = 0;        // sport intervals = rows per protocol class
