@@ -1222,6 +1222,10 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
                                     (uint32_t)__ldg(t.cls + (v.w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v.z >> 16)),
                                     __ldg(t.port[1] + (v.z & 0xFFFFu))};
             PFW_CHECK(rr[0] < t.nrows[0] && rr[1] < t.nrows[1] && rr[2] < t.nrows[2] && rr[3] < t.nrows[3]);
+            // the candidates' line indices come 8 blocks (16 bytes) per load and
+            // dimension: a packet's candidates cluster, so one chunk serves several
+            uint4 ch[4];
+            uint32_t cc = 0xFFFFFFFFu;  // chunk (block / 8) held in ch
             for (uint32_t w = 0; w <= kb1 / 32u && !more; w++) {
                 uint32_t a = __ldg(u.sum[0] + (size_t)rr[0] * u.sw + w) & __ldg(u.sum[1] + (size_t)rr[1] * u.sw + w) &
                              __ldg(u.sum[2] + (size_t)rr[2] * u.sw + w) & __ldg(u.sum[3] + (size_t)rr[3] * u.sw + w);
@@ -1234,12 +1238,20 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
                     }
                     const uint32_t b = 32u * w + (uint32_t)(__ffs(a) - 1);
                     a &= a - 1u;
+                    if ((b >> 3) != cc) {
+                        cc = b >> 3;
+#pragma unroll
+                        for (int d = 0; d < 4; d++)
+                            ch[d] = __ldg(reinterpret_cast<const uint4 *>(
+                                b < 8u ? u.head + u.head_off[d] + (size_t)rr[d] * 8
+                                       : u.ptr + u.ptr_off[d] + (size_t)rr[d] * u.pstride + 8u * cc));
+                    }
                     uint32_t q[4];
+                    const uint32_t wi = (b >> 1) & 3u, sh = 16u * (b & 1u);
 #pragma unroll
                     for (int d = 0; d < 4; d++) {
-                        const uint16_t ix = b < 8u ? __ldg(u.head + u.head_off[d] + (size_t)rr[d] * 8 + b)
-                                                   : __ldg(u.ptr + u.ptr_off[d] + (size_t)rr[d] * u.pstride + b);
-                        q[d] = __ldg(u.loff + d * u.nblk + b) + ix;
+                        const uint32_t h2 = wi == 0 ? ch[d].x : wi == 1 ? ch[d].y : wi == 2 ? ch[d].z : ch[d].w;
+                        q[d] = __ldg(u.loff + d * u.nblk + b) + ((h2 >> sh) & 0xFFFFu);
                     }
                     s_cl[warp][lane][nc] = make_uint4(q[0], q[1], q[2], q[3]);
                     s_cb[warp][lane][nc] = (uint16_t)b;
