@@ -1029,14 +1029,18 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
 // packet's absolute line numbers (loff[d][b] + index) for its first MS_LEAN_PARK
 // blocks in shared memory, from the dense head array (one 16-byte load per
 // dimension); a step takes its block's four line numbers with one shared
-// 16-byte load; blocks past the parked ones (rare: most scans end in the first
-// two or three) read the index from global memory.  Idle groups read the zero
-// line after the last distinct line.
+// 16-byte load; a packet that walks past its parked window (rare: most scans
+// end in the first two or three blocks) has its group park the next
+// MS_LEAN_PARK blocks' line numbers, one block per lane.  Idle groups read the
+// zero line after the last distinct line.
 #ifndef MS_LEAN_PARK
 #define MS_LEAN_PARK 6
 #endif
+#ifndef MS_CMP_MINB
+#define MS_CMP_MINB PFW_MS_MINB
+#endif
 template <int MODE, int G>
-__global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
+__global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
     ms_lean_cmp_kernel(ScanParams p, MsView t, MsCmp u, uint32_t zline) {
     constexpr int V = 32 / G, P = 32 / G, K = MS_LEAN_PARK;
     static_assert(K >= 1 && K <= 8, "1..8 parked blocks (the head array holds 8)");
@@ -1098,7 +1102,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
         if (nsteps > 0) {
             int pj = grp < nv ? grp : -1;
             int next = P;
-            int s = 0;
+            int s = 0, slot = 0;  // block, and its slot in the packet's parked window
             uint4 q = pj >= 0 ? s_ln[warp][pj][0] : zq;
             while (next < nv + P) {
                 uint32_t w[4][V];
@@ -1125,18 +1129,28 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : PFW_MS_MINB)
                 // the next block's line numbers: a new packet's block 0, or this
                 // packet's next parked block (one shared 16-byte load either way)
                 const int ns = done ? 0 : s + (act ? 1 : 0);
-                const int qi = done ? (np & 31) : (pj & 31);
-                const uint4 qn = s_ln[warp][qi][ns < K ? ns : 0];
-                q = (done && !take) || !act ? zq : qn;
-                if (act && !done && ns >= K) {  // past the parked blocks: indices from global memory
-                    const uint4 rw = s_row[warp][pj];
-                    const uint32_t b = (uint32_t)ns;
-                    q.x = __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
-                    q.y = __ldg(u.loff + u.nblk + b) + __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
-                    q.z = __ldg(u.loff + 2 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
-                    q.w = __ldg(u.loff + 3 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
+                const int nslot = done ? 0 : (act ? (slot + 1 == K ? 0 : slot + 1) : slot);
+                // past the parked window (rare): the group parks the next K
+                // blocks' line numbers, one block per lane (one round trip per
+                // K blocks instead of one per block)
+                const bool repark = act && !done && nslot == 0;
+                if (__any_sync(0xFFFFFFFFu, repark)) {
+                    for (int j = gl; repark && j < K && ns + j < nsteps; j += G) {
+                        const uint4 rw = s_row[warp][pj];
+                        const uint32_t b = (uint32_t)(ns + j);
+                        s_ln[warp][pj][j] = make_uint4(
+                            __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b),
+                            __ldg(u.loff + u.nblk + b) + __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b),
+                            __ldg(u.loff + 2 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b),
+                            __ldg(u.loff + 3 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b));
+                    }
+                    __syncwarp();
                 }
+                const int qi = done ? (np & 31) : (pj & 31);
+                const uint4 qn = s_ln[warp][qi][nslot];
+                q = (done && !take) || !act ? zq : qn;
                 s = ns;
+                slot = nslot;
                 pj = done ? (take ? np : -1) : pj;
                 next += __popc(dm);
             }
