@@ -526,8 +526,11 @@ def run_ours(args, w, world, rank, local) -> int:
     def make_step(batch, out_first, out_comps, out_verdict):
         m = len(batch)
 
-        def step():
-            stats.zero_()
+        def step(zero=True):
+            # (the timed loop zeroes the stats once before its first step and
+            # lets the steps accumulate them: no per-step fill launch)
+            if zero:
+                stats.zero_()
             if fused is not None:
                 fused.run(batch, stats=stats, stream=stream.cuda_stream)
             elif w.model == "function":
@@ -556,9 +559,14 @@ def run_ours(args, w, world, rank, local) -> int:
 
     def timed(run_step, steps, clocks=None):
         """steps timed launches (CUDA events on the launching stream, L2
-        flushed before each) -> total ms of this rank."""
-        times = []
+        flushed before each) -> total ms of this rank.  The steps are queued
+        back to back (flush, event, step, event) with one synchronize after the
+        last: the host enqueues ahead of the device (each flush alone is ~40 us
+        of device time), so an event pair times the step's device execution,
+        not the host's launch latency."""
+        evs = []
         barrier()
+        torch.cuda.synchronize(dev)
         for _ in range(steps):
             if flush_l2:
                 flush.fill_(1)
@@ -566,10 +574,10 @@ def run_ours(args, w, world, rank, local) -> int:
             e0.record(stream)
             run_step()
             e1.record(stream)
-            e1.synchronize()
-            times.append(e0.elapsed_time(e1))
+            evs.append((e0, e1))
+        torch.cuda.synchronize(dev)
         barrier()
-        return sum(times)
+        return sum(a.elapsed_time(b) for a, b in evs)
 
     def max_over_ranks(x: float) -> float:
         t = torch.tensor([x], dtype=torch.float64, device=dev)
@@ -585,7 +593,7 @@ def run_ours(args, w, world, rank, local) -> int:
         flush.fill_(1)
         step()
     barrier()
-    run_step = step
+    run_step = lambda: step(False)  # noqa: E731
     graph_launches = 0  # kernels per replay (replays bypass the library's launch counter)
     if args.graph and fused is None and world == 1:
         # the library launches on the caller's stream, so stream capture
@@ -598,7 +606,7 @@ def run_ours(args, w, world, rank, local) -> int:
             stream = cap
             before = _native.launch_count()
             with torch.cuda.graph(g, stream=cap):
-                step()
+                step(False)
             graph_launches = _native.launch_count() - before
             stream = stream_saved
         torch.cuda.synchronize()
@@ -606,6 +614,8 @@ def run_ours(args, w, world, rank, local) -> int:
         run_step()
         torch.cuda.synchronize()
     # algorithmic work of one step: sum of this rank's (per-task) comparisons
+    stats.zero_()
+    run_step()
     local_comps = int(stats[0].item())
     # the match-set scan with block summaries skips blocks: count the blocks it
     # reads in one extra (untimed) step for its roofline
@@ -619,8 +629,14 @@ def run_ours(args, w, world, rank, local) -> int:
         blocks_read = _native.read_counter("blocks_read")
 
     launches0 = _native.launch_count()
+    stats.zero_()
     with ClockSampler(local) as clocks:
         total_ms = timed(run_step, args.steps)
+    # every timed step ran the whole scan: the accumulated comparisons say so
+    timed_comps = int(stats[0].item())
+    if fused is None and timed_comps != local_comps * args.steps:
+        raise RuntimeError(f"timed steps accumulated {timed_comps} comparisons, expected "
+                           f"{args.steps} x {local_comps}")
     launches = _native.launch_count() - launches0 + graph_launches * args.steps
     job_ms = max_over_ranks(total_ms)
     pk_per_step = w.packets if w.model == "function" else int(sum_over_ranks(float(n)))
@@ -717,7 +733,7 @@ def run_ours(args, w, world, rank, local) -> int:
             rsteps = max(3, min(args.steps, 5))
             launches_r0 = _native.launch_count()
             with ClockSampler(local) as rclocks:
-                r_ms = timed(rstep_, rsteps)
+                r_ms = timed(lambda: rstep_(False), rsteps)
             r_launches = _native.launch_count() - launches_r0
             r_job = max_over_ranks(r_ms)
             r_pk = int(sum_over_ranks(float(m))) if w.model != "function" else m
@@ -749,7 +765,7 @@ def run_ours(args, w, world, rank, local) -> int:
         wstep = make_step(wp_, wf, wc, wv)
         wstep()
         with ClockSampler(local) as wclocks:
-            w_ms = timed(wstep, args.steps)
+            w_ms = timed(lambda: wstep(False), args.steps)
         w_job = max_over_ranks(w_ms)
         w_total = int(sum_over_ranks(float(nw)))
         weak_rec = {"value": round(w_total * args.steps / (w_job / 1e3) / 1e6, 3), "unit": "Mpps",
