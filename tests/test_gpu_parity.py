@@ -1014,3 +1014,43 @@ def test_many_ip_boundaries_in_one_slash16():
     c, p = compiled(rules), dev_pkts(pk)
     assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
     np.testing.assert_array_equal(c.scan_range(p, 0, R), oracle.scan_range(rules, pk, 0, R))
+
+
+def test_ip_lookup_entries_sparse_blocks_edges():
+    """The 16-byte /16 lookup entries: blocks holding 1..8 and 12 boundaries
+    (the first six carried in the entry, more searched), boundaries at low
+    half 0x0000 and 0xFFFF (host rules ending a block), adjacent hosts; every
+    boundary address and its neighbours probed, src and dst -- identical to
+    the oracle."""
+    rng = np.random.default_rng(5)
+    hosts = []
+    for blk, k in ((0x0A01, 1), (0x0A02, 2), (0x0A03, 3), (0x0A04, 5), (0x0A05, 6), (0x0A06, 7),
+                   (0x0A07, 8), (0x0A08, 12), (0xFFFF, 6), (0x0000, 6)):
+        lows = set(rng.choice(np.arange(1, 0xFFFE), k - 1, replace=False).tolist()) | {0xFFFF}
+        if blk in (0x0A05, 0x0000):
+            lows |= {0x0000}
+        hosts += [(blk << 16) | lo for lo in sorted(lows)[:k]]
+    hosts = np.array(hosts, dtype=np.uint32)
+    R = 2 * len(hosts) + 40
+    rules = oracle.gen_ruleset(R, 91, wp=0.3)
+    # /32 hosts (boundaries at a and a + 1) on src for the first half, dst for the second
+    # half, /31 pairs among them; then random rules
+    for j, a in enumerate(hosts):
+        for f, k in (("src", j), ("dst", len(hosts) + j)):
+            plen = 31 if j % 5 == 0 else 32
+            mask = np.uint32((0xFFFFFFFF << (32 - plen)) & 0xFFFFFFFF)
+            rules[f + "_base"][k] = a & mask
+            rules[f + "_mask"][k] = mask
+            other = "dst" if f == "src" else "src"
+            rules[other + "_base"][k] = 0
+            rules[other + "_mask"][k] = 0
+    probe = np.unique(np.concatenate([hosts, hosts + np.uint32(1), hosts - np.uint32(1),
+                                      (hosts & np.uint32(0xFFFF0000)), hosts | np.uint32(0xFFFF)]))
+    n = 40_000
+    pk = oracle.gen_traffic_uniform(n, 92)
+    pk["src_ip"][: n // 2] = rng.choice(probe, n // 2)
+    pk["dst_ip"][n // 4:] = rng.choice(probe, n - n // 4)
+    c, p = compiled(rules), dev_pkts(pk)
+    assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
+    np.testing.assert_array_equal(c.scan_range(p, 0, R), oracle.scan_range(rules, pk, 0, R))
+    np.testing.assert_array_equal(c.scan_range(p, 0, len(hosts)), oracle.scan_range(rules, pk, 0, len(hosts)))
