@@ -262,6 +262,14 @@ int pfw_format_results(const int64_t *ids, const uint32_t *first, const uint8_t 
  * and the rule-scan options "ks", "tile", "first_pass", "bucket",
  * "bucket_min", "proto_split", "short_circuit", "force_imad", "ctas_per_sm". */
 int64_t pfw_launch_count(void);
+/* L2 read-bandwidth probe (bench.py's roofline peak, measured live): on the
+ * current device, blocks_per_sm x SMs blocks of 256 threads, each group of 8
+ * lanes reading one random 128-byte line of d_buf (>= 1 MiB, L2-resident
+ * size) per load, lines_in_flight (2, 4, 8 or 16) per lane per iteration, iters
+ * iterations; bytes read = SMs x blocks_per_sm x 32 x lines_in_flight x iters
+ * x 128.  The caller times it (events on the stream). */
+int pfw_probe_l2_lines(const void *d_buf, int64_t bytes, int lines_in_flight, int blocks_per_sm, int iters,
+                       void *stream);
 /* Instrumentation counters, read and reset: "blocks_read" = 1024-rule blocks
  * the match-set scan with block summaries read (counted while tuning
  * "count_blocks" is 1; used by bench.py for that variant's roofline). */

@@ -73,6 +73,7 @@ _SIGS = {
     "pfw_parse_traffic": (_I32, [_P, _I64, _I64, _P, _P, ctypes.POINTER(_I64)]),
     "pfw_format_results": (_I32, [_P, _P, _P, _I64, _P, _I64, ctypes.POINTER(_I64)]),
     "pfw_launch_count": (_I64, []),
+    "pfw_probe_l2_lines": (_I32, [_P, _I64, _I32, _I32, _I32, _P]),
     "pfw_read_counter": (_I32, [ctypes.c_char_p, ctypes.POINTER(_I64)]),
     "pfw_set_tuning": (_I32, [ctypes.c_char_p, _I64]),
 }

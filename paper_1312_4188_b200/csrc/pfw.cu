@@ -1341,6 +1341,31 @@ int grid_for(int64_t n) {
     return (int)(g < 1 ? 1 : g);
 }
 
+
+// L2 read-bandwidth probe for the match-set scan's access pattern (bench.py's
+// roofline peak, measured on the same device in the same run): groups of 8
+// lanes each read one random 128-byte line (16 bytes per lane) of an
+// L2-resident buffer, K independent lines per lane in flight per iteration.
+template <int K>
+__global__ void __launch_bounds__(256) probe_l2_lines_kernel(const uint4 *__restrict__ p, uint32_t nlines,
+                                                             int iters, uint32_t *sink) {
+    const int lane = threadIdx.x & 31, grp = lane / 8, gl = lane % 8;
+    uint32_t x = 0x9E3779B9u * (blockIdx.x * 32u + (threadIdx.x >> 5) * 4u + (uint32_t)grp + 1u);
+    uint32_t acc = 0;
+    for (int it = 0; it < iters; it++) {
+        uint4 v[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            x = x * 1664525u + 1013904223u;  // group-uniform LCG
+            const uint32_t line = (uint32_t)(((uint64_t)(x >> 8) * nlines) >> 24);
+            v[k] = __ldg(p + (size_t)line * 8 + gl);
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) acc ^= v[k].x ^ v[k].y ^ v[k].z ^ v[k].w;
+    }
+    if (acc == 0x12345678u) *sink = acc;  // keeps the loads
+}
+
 }  // namespace
 
 // =================================================================== C-ABI
@@ -1360,6 +1385,30 @@ int pfw_device_count(void) {
         return 0;
     }
     return n;
+}
+
+int pfw_probe_l2_lines(const void *d_buf, int64_t bytes, int lines_in_flight, int blocks_per_sm, int iters,
+                       void *stream) {
+    if (!d_buf || bytes < (1 << 20) || iters < 1 || blocks_per_sm < 1 || blocks_per_sm > 8)
+        return set_err(PFW_ERR_INVALID, "bad probe arguments");
+    int dev = 0, sms = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    static uint32_t *sink = nullptr;
+    if (!sink) CUDA_TRY(cudaMalloc(&sink, sizeof(uint32_t)));
+    const uint32_t nlines = (uint32_t)std::min<int64_t>(bytes / 128, 0x7FFFFFFF);
+    const auto *p = reinterpret_cast<const uint4 *>(d_buf);
+    const cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = (unsigned)(sms * blocks_per_sm);
+    switch (lines_in_flight) {
+        case 2: probe_l2_lines_kernel<2><<<grid, 256, 0, st>>>(p, nlines, iters, sink); break;
+        case 4: probe_l2_lines_kernel<4><<<grid, 256, 0, st>>>(p, nlines, iters, sink); break;
+        case 8: probe_l2_lines_kernel<8><<<grid, 256, 0, st>>>(p, nlines, iters, sink); break;
+        case 16: probe_l2_lines_kernel<16><<<grid, 256, 0, st>>>(p, nlines, iters, sink); break;
+        default: return set_err(PFW_ERR_INVALID, "lines_in_flight: 2, 4, 8 or 16");
+    }
+    CUDA_TRY(cudaGetLastError());
+    return PFW_OK;
 }
 
 int64_t pfw_launch_count(void) { return g_launches.load(); }

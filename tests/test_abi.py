@@ -13,7 +13,7 @@ from paper_1312_4188_b200 import _native
 
 def header_symbols() -> set[str]:
     text = open(os.path.join(ROOT, "include", "pfw.h")).read()
-    return set(re.findall(r"\b(pfw_[a-z_]+)\s*\(", text))
+    return set(re.findall(r"\b(pfw_[a-z0-9_]+)\s*\(", text))
 
 
 def test_library_exports_every_header_symbol():
