@@ -1054,3 +1054,21 @@ def test_ip_lookup_entries_sparse_blocks_edges():
     assert _native.lib().pfw_ruleset_matchset_bytes(c.handle) > 0
     np.testing.assert_array_equal(c.scan_range(p, 0, R), oracle.scan_range(rules, pk, 0, R))
     np.testing.assert_array_equal(c.scan_range(p, 0, len(hosts)), oracle.scan_range(rules, pk, 0, len(hosts)))
+
+
+@pytest.mark.parametrize("lc", [1, 2])
+@pytest.mark.parametrize("R", [6 * 1024 + 1, 12 * 1024, 13 * 1024 - 7, 20_000])
+def test_lean_compressed_repark_windows(lc, R):
+    """Sparse rulesets over compressed rows: most packets walk past their 6
+    parked blocks (the group re-parks the next 6, the last window cut short
+    by the table end) or scan everything (default deny) -- bit-exact."""
+    _native.set_tuning("algo", 2)
+    _native.set_tuning("ms_compress", 1)
+    _native.set_tuning("ms_summary", 0)
+    _native.set_tuning("ms_lean_cmp", lc)
+    rules = oracle.gen_ruleset(R, 300 + R % 97, wp=0.02)
+    pk = oracle.gen_traffic_uniform(30_000, 301)
+    c, p = compiled(rules), dev_pkts(pk)
+    want = oracle.scan_range(rules, pk, 0, R)
+    assert (want < 0).mean() > 0.05  # default deny walks every block
+    np.testing.assert_array_equal(c.scan_range(p, 0, R), want)
