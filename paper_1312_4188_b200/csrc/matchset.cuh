@@ -55,7 +55,7 @@ constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet kee
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
 int g_ms_lean_sum = 2;         // whole-table summary scans over compressed rows: lean candidate walk (0 general kernel, 1 at 5 / 2 at 4 blocks per SM)
-int g_ms_lean_cmp = 1;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane
+int g_ms_lean_cmp = 3;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane, 3 lean 8-lane with u16 parked indices (<= MS_CP_BLOCKS blocks, else 1)
 int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
 
@@ -1039,16 +1039,40 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
 #ifndef MS_CMP_MINB
 #define MS_CMP_MINB PFW_MS_MINB
 #endif
-template <int MODE, int G>
+#ifndef MS_CP_BLOCKS
+#define MS_CP_BLOCKS 256
+#endif
+template <int MODE, int G, bool CP = false>
 __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
     ms_lean_cmp_kernel(ScanParams p, MsView t, MsCmp u, uint32_t zline) {
     constexpr int V = 32 / G, P = 32 / G, K = MS_LEAN_PARK;
     static_assert(K >= 1 && K <= 8, "1..8 parked blocks (the head array holds 8)");
-    __shared__ uint4 s_ln[MS_BLOCK / 32][32][K];  // per packet: line numbers of blocks 0..K-1 (x..w = dimension)
-    __shared__ uint4 s_row[MS_BLOCK / 32][32];    // per packet: its four rows (blocks >= K)
+    // CP: a parked block is its four u16 line indices (8 bytes) and the
+    // (dimension, block) line offsets sit in one shared table (<= MS_CP_BLOCKS
+    // blocks); otherwise a parked block is its four absolute line numbers
+    using Slot = std::conditional_t<CP, uint2, uint4>;
+    __shared__ __align__(16) Slot s_ln[MS_BLOCK / 32][32][K];  // per packet: blocks of its parked window
+    __shared__ uint4 s_lo[CP ? MS_CP_BLOCKS : 1];             // CP: loff of block b, x..w = dimension
+    __shared__ uint4 s_row[MS_BLOCK / 32][32];    // per packet: its four rows (re-parking)
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];
     // (a finished packet's line-number slots are reused for the finding lane's AND words)
-    static_assert(V / 4 <= K, "the parked words fit the packet's line-number slots");
+    static_assert((CP ? V / 2 : V / 4) <= K, "the parked words fit the packet's line-number slots");
+    static_assert(!CP || K % 2 == 0, "16-byte aligned parked words");
+    if constexpr (CP) {
+        for (int b = threadIdx.x; b < (int)u.nblk && b < MS_CP_BLOCKS; b += MS_BLOCK)
+            s_lo[b] = make_uint4(__ldg(u.loff + b), __ldg(u.loff + u.nblk + b), __ldg(u.loff + 2 * u.nblk + b),
+                                 __ldg(u.loff + 3 * u.nblk + b));
+        __syncthreads();
+    }
+    // a slot's four line numbers for block b
+    auto line4 = [&](const Slot &e, uint32_t b) -> uint4 {
+        if constexpr (CP) {
+            const uint4 lo = s_lo[b];
+            return make_uint4(lo.x + (e.x & 0xFFFFu), lo.y + (e.x >> 16), lo.z + (e.y & 0xFFFFu), lo.w + (e.y >> 16));
+        } else {
+            return e;
+        }
+    };
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int grp = lane / G, gl = lane % G, gbase = grp * G;
     const uint32_t lv = (uint32_t)gl * V;
@@ -1092,9 +1116,10 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
 #pragma unroll
                 for (int d = 0; d < 4; d++) {
                     const uint32_t h2 = (j >> 1) == 0 ? hq[d].x : (j >> 1) == 1 ? hq[d].y : (j >> 1) == 2 ? hq[d].z : hq[d].w;
-                    l[d] = __ldg(u.loff + d * u.nblk + j) + ((h2 >> (16 * (j & 1))) & 0xFFFFu);
+                    l[d] = ((h2 >> (16 * (j & 1))) & 0xFFFFu) + (CP ? 0u : __ldg(u.loff + d * u.nblk + j));
                 }
-                s_ln[warp][lane][j] = make_uint4(l[0], l[1], l[2], l[3]);
+                if constexpr (CP) s_ln[warp][lane][j] = make_uint2(l[0] | (l[1] << 16), l[2] | (l[3] << 16));
+                else s_ln[warp][lane][j] = make_uint4(l[0], l[1], l[2], l[3]);
             }
         }
         s_res[warp][lane] = PFW_NO_MATCH;
@@ -1103,7 +1128,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
             int pj = grp < nv ? grp : -1;
             int next = P;
             int s = 0, slot = 0;  // block, and its slot in the packet's parked window
-            uint4 q = pj >= 0 ? s_ln[warp][pj][0] : zq;
+            uint4 q = pj >= 0 ? line4(s_ln[warp][pj][0], 0u) : zq;
             while (next < nv + P) {
                 uint32_t w[4][V];
                 ms_load_rows<V>(lines + ((size_t)q.x << 5) + lv, lines + ((size_t)q.y << 5) + lv,
@@ -1118,8 +1143,9 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
                 const unsigned gbits = (bal >> gbase) & ((1u << G) - 1u);
                 if (any != 0u && (gbits & below) == 0u) {  // park the words; the bit is resolved after the loop
                     s_res[warp][pj] = (uint32_t)s * 32u + lv;
+                    uint4 *px = reinterpret_cast<uint4 *>(&s_ln[warp][pj][0]);
 #pragma unroll
-                    for (int k = 0; k < V; k += 4) s_ln[warp][pj][k / 4] = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
+                    for (int k = 0; k < V; k += 4) px[k / 4] = make_uint4(x[k], x[k + 1], x[k + 2], x[k + 3]);
                 }
                 const bool act = pj >= 0;
                 const bool done = act && (gbits != 0u || s + 1 >= nsteps);
@@ -1138,16 +1164,21 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
                     for (int j = gl; repark && j < K && ns + j < nsteps; j += G) {
                         const uint4 rw = s_row[warp][pj];
                         const uint32_t b = (uint32_t)(ns + j);
-                        s_ln[warp][pj][j] = make_uint4(
-                            __ldg(u.loff + b) + __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b),
-                            __ldg(u.loff + u.nblk + b) + __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b),
-                            __ldg(u.loff + 2 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b),
-                            __ldg(u.loff + 3 * u.nblk + b) + __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b));
+                        const uint32_t i0 = __ldg(u.ptr + u.ptr_off[0] + (size_t)rw.x * u.pstride + b);
+                        const uint32_t i1 = __ldg(u.ptr + u.ptr_off[1] + (size_t)rw.y * u.pstride + b);
+                        const uint32_t i2 = __ldg(u.ptr + u.ptr_off[2] + (size_t)rw.z * u.pstride + b);
+                        const uint32_t i3 = __ldg(u.ptr + u.ptr_off[3] + (size_t)rw.w * u.pstride + b);
+                        if constexpr (CP)
+                            s_ln[warp][pj][j] = make_uint2(i0 | (i1 << 16), i2 | (i3 << 16));
+                        else
+                            s_ln[warp][pj][j] = make_uint4(__ldg(u.loff + b) + i0, __ldg(u.loff + u.nblk + b) + i1,
+                                                           __ldg(u.loff + 2 * u.nblk + b) + i2,
+                                                           __ldg(u.loff + 3 * u.nblk + b) + i3);
                     }
                     __syncwarp();
                 }
                 const int qi = done ? (np & 31) : (pj & 31);
-                const uint4 qn = s_ln[warp][qi][nslot];
+                const uint4 qn = line4(s_ln[warp][qi][nslot], (uint32_t)ns);
                 q = (done && !take) || !act ? zq : qn;
                 s = ns;
                 slot = nslot;
@@ -1158,7 +1189,7 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
         __syncwarp();
         if (i < n) {
             uint32_t res = s_res[warp][lane];
-            if (res != PFW_NO_MATCH) res = ms_parked_first_bit<V>(&s_ln[warp][lane][0], res);
+            if (res != PFW_NO_MATCH) res = ms_parked_first_bit<V>(reinterpret_cast<const uint4 *>(&s_ln[warp][lane][0]), res);
             PFW_CHECK(res == PFW_NO_MATCH || (res >= p.lo && res < p.hi));
             emit_result<MODE, true>(p, (uint32_t)i, res, span, st_sum, st_max);
         }
@@ -1919,7 +1950,9 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
     // (tuning ms_lean_cmp: 0 off, 1 8-lane groups, 2 4-lane groups / 256-bit loads)
     void (*kern_lc)(ScanParams, MsView, MsCmp, uint32_t) = nullptr;
     if (g_ms_lean_cmp && kern_c && !sum && !win)
-        kern_lc = g_ms_lean_cmp == 2 ? ms_lean_cmp_kernel<MODE, 4> : ms_lean_cmp_kernel<MODE, 8>;
+        kern_lc = g_ms_lean_cmp == 2 ? ms_lean_cmp_kernel<MODE, 4>
+                  : (g_ms_lean_cmp == 3 && m->nblk <= MS_CP_BLOCKS) ? ms_lean_cmp_kernel<MODE, 8, true>
+                                                                     : ms_lean_cmp_kernel<MODE, 8>;
     // block summaries over compressed rows, whole table: the lean candidate walk
     if (g_ms_lean_sum && kern_c && sum && !win)
         kern_lc = g_ms_lean_sum == 2 ? ms_lean_sum_kernel<MODE, 4> : ms_lean_sum_kernel<MODE, PFW_MS_MINB>;

@@ -1485,7 +1485,8 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_lean_sum: 0 off, 1 on, 2 on at 4 blocks per SM");
         g_ms_lean_sum = (int)value;
     } else if (!strcmp(key, "ms_lean_cmp")) {
-        if (value < 0 || value > 2) return set_err(PFW_ERR_INVALID, "ms_lean_cmp: 0 off, 1 8-lane, 2 4-lane groups");
+        if (value < 0 || value > 3)
+            return set_err(PFW_ERR_INVALID, "ms_lean_cmp: 0 off, 1 8-lane, 2 4-lane groups, 3 8-lane with u16 parked indices");
         g_ms_lean_cmp = (int)value;
     } else if (!strcmp(key, "ms_odd_rows")) {
         g_ms_odd_rows = value != 0;

@@ -39,7 +39,7 @@ def _reset_tuning():
     for k, v in (("ks", 8), ("tile", 2048), ("ctas_per_sm", 0), ("force_imad", 1), ("first_pass", 1024),
                  ("proto_split", 0), ("short_circuit", 0), ("bucket", 1), ("bucket_min", 1 << 20),
                  ("algo", 0), ("ms_group", 0), ("ms_words", 4), ("matchset", 1), ("matchset_budget_mb", 0),
-                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_lean_cmp", 1), ("ms_lean_sum", 2)):
+                 ("ms_summary", 2), ("count_blocks", 0), ("ms_compress", 2), ("ms_lean", 3), ("ms_lean_cmp", 3), ("ms_lean_sum", 2)):
         _native.set_tuning(k, v)
 
 
@@ -685,7 +685,7 @@ def test_lean_whole_table_scan(lean):
     assert stats.cpu().tolist() == [int(cc.sum()), int(cc.max())]
 
 
-@pytest.mark.parametrize("lc", [0, 1, 2])
+@pytest.mark.parametrize("lc", [0, 1, 2, 3])
 def test_lean_compressed_rows(lc):
     """Whole-table scans over compressed rows: the general kernel (0) and the
     lean compressed kernel with 8- or 4-lane groups (1, 2) are bit-exact, incl.
@@ -1056,7 +1056,7 @@ def test_ip_lookup_entries_sparse_blocks_edges():
     np.testing.assert_array_equal(c.scan_range(p, 0, len(hosts)), oracle.scan_range(rules, pk, 0, len(hosts)))
 
 
-@pytest.mark.parametrize("lc", [1, 2])
+@pytest.mark.parametrize("lc", [1, 2, 3])
 @pytest.mark.parametrize("R", [6 * 1024 + 1, 12 * 1024, 13 * 1024 - 7, 20_000])
 def test_lean_compressed_repark_windows(lc, R):
     """Sparse rulesets over compressed rows: most packets walk past their 6
