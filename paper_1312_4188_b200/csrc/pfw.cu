@@ -1394,8 +1394,10 @@ int pfw_probe_l2_lines(const void *d_buf, int64_t bytes, int lines_in_flight, in
     int dev = 0, sms = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    static uint32_t *sink = nullptr;
-    if (!sink) CUDA_TRY(cudaMalloc(&sink, sizeof(uint32_t)));
+    static uint32_t *sinks[64] = {};  // per device (the kernel's never-taken store target)
+    if (dev < 0 || dev >= 64) return set_err(PFW_ERR_INVALID, "device %d out of range", dev);
+    if (!sinks[dev]) CUDA_TRY(cudaMalloc(&sinks[dev], sizeof(uint32_t)));
+    uint32_t *sink = sinks[dev];
     const uint32_t nlines = (uint32_t)std::min<int64_t>(bytes / 128, 0x7FFFFFFF);
     const auto *p = reinterpret_cast<const uint4 *>(d_buf);
     const cudaStream_t st = (cudaStream_t)stream;
