@@ -1223,6 +1223,9 @@ __global__ void __launch_bounds__(MS_BLOCK, G == 4 ? 4 : MS_CMP_MINB)
 #ifndef MS_SUM_PARK
 #define MS_SUM_PARK 6
 #endif
+#ifndef MS_SUM_LO_BLOCKS
+#define MS_SUM_LO_BLOCKS 64  // (1 KB of shared memory: rulesets up to 64K rules)
+#endif
 template <int MODE, int MINB>
 __global__ void __launch_bounds__(MS_BLOCK, MINB)
     ms_lean_sum_kernel(ScanParams p, MsView t, MsCmp u, uint32_t zline) {
@@ -1231,6 +1234,7 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
     // entry is reused for the finding lane's AND words), blocks, count
     __shared__ uint4 s_cl[MS_BLOCK / 32][32][K];
     __shared__ uint16_t s_cb[MS_BLOCK / 32][32][K];
+    __shared__ uint4 s_lo[MS_SUM_LO_BLOCKS];  // loff of block b (x..w = dimension), when nblk <= MS_SUM_LO_BLOCKS
     __shared__ uint8_t s_nc[MS_BLOCK / 32][32];  // candidates parked | (more << 7)
     __shared__ uint32_t s_res[MS_BLOCK / 32][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1248,6 +1252,13 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
     const uint4 zq = make_uint4(zline, zline, zline, zline);
     unsigned long long st_sum = 0, st_blocks = 0;
     unsigned st_max = 0;
+    const bool lo_sh = u.nblk <= MS_SUM_LO_BLOCKS;  // the parking loop reads loff from shared memory
+    if (lo_sh) {
+        for (int b = threadIdx.x; b < (int)u.nblk; b += MS_BLOCK)
+            s_lo[b] = make_uint4(__ldg(u.loff + b), __ldg(u.loff + u.nblk + b), __ldg(u.loff + 2 * u.nblk + b),
+                                 __ldg(u.loff + 3 * u.nblk + b));
+        __syncthreads();
+    }
 
     for (int64_t b0 = gw * 32; b0 < n; b0 += nw * 32) {
         const int nv = (int)((n - b0) < 32 ? (n - b0) : 32);
@@ -1293,10 +1304,14 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
                     }
                     uint32_t q[4];
                     const uint32_t wi = (b >> 1) & 3u, sh = 16u * (b & 1u);
+                    uint4 lo4;
+                    if (lo_sh) lo4 = s_lo[b];
+                    else lo4 = make_uint4(__ldg(u.loff + b), __ldg(u.loff + u.nblk + b), __ldg(u.loff + 2 * u.nblk + b),
+                                          __ldg(u.loff + 3 * u.nblk + b));
 #pragma unroll
                     for (int d = 0; d < 4; d++) {
                         const uint32_t h2 = wi == 0 ? ch[d].x : wi == 1 ? ch[d].y : wi == 2 ? ch[d].z : ch[d].w;
-                        q[d] = __ldg(u.loff + d * u.nblk + b) + ((h2 >> sh) & 0xFFFFu);
+                        q[d] = (d == 0 ? lo4.x : d == 1 ? lo4.y : d == 2 ? lo4.z : lo4.w) + ((h2 >> sh) & 0xFFFFu);
                     }
                     s_cl[warp][lane][nc] = make_uint4(q[0], q[1], q[2], q[3]);
                     s_cb[warp][lane][nc] = (uint16_t)b;
