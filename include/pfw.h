@@ -213,6 +213,17 @@ int pfw_classify_host_ex(pfw_ruleset_t h, const void *h_pkts, const uint8_t *h_p
                          const uint16_t *h_dst_port, int64_t n, uint32_t *h_first, uint8_t *h_verdict,
                          uint64_t *h_stats, int64_t chunk, uint32_t flags);
 
+/* The same pipeline for the function-parallel / hybrid models (engines.py:
+ * 316-369 over partition_bounds(R, nodes)): each chunk runs every node's
+ * partition scan folded on the device (pfw_scan_partitions), so h_first =
+ * the lowest node's match, h_comps = the per-packet sum over nodes of the
+ * per-task comparisons, h_stats = [sum, largest per-node count]; verdicts
+ * from h_first.  Whole rulesets only (not a rule shard).  h_comps required. */
+int pfw_classify_host_partitions(pfw_ruleset_t h, int64_t nodes, const void *h_pkts, const uint8_t *h_proto,
+                                 const uint32_t *h_src_ip, const uint16_t *h_src_port, const uint32_t *h_dst_ip,
+                                 const uint16_t *h_dst_port, int64_t n, uint32_t *h_first, uint32_t *h_comps,
+                                 uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk, uint32_t flags);
+
 /* Bit-exact UNIFORM traffic generation on the device.  Replaces
  * generate_traffic(TrafficProfile(...)) with match_mode UNIFORM
  * (traffic.py:117-130, 148-160; rng.py:31-62): the pinned xorshift64* stream

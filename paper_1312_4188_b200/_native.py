@@ -64,6 +64,7 @@ _SIGS = {
     "pfw_classify_host": (_I32, [_P, _P, _I64, _P, _P, _P, _I64]),
     "pfw_classify_host_columns": (_I32, [_P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I64]),
     "pfw_classify_host_ex": (_I32, [_P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _U32]),
+    "pfw_classify_host_partitions": (_I32, [_P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _U32]),
     "pfw_generate_traffic": (_I32, [_I32, _U64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,
                                     _I32, _I32, _P, _P]),
     "pfw_generate_traffic_at": (_I32, [_I32, _U64, _I64, _I64, _I32, _U32, _I32, _U32, _I32, _I32, _I32,

@@ -319,6 +319,21 @@ def _rule_columns(ruleset: Ruleset) -> dict:
     }
 
 
+def _host_packet_ptrs(packets):
+    """Host packet batch -> (arrays kept alive, n, record pointer, 5 column
+    pointers): a dict of the reference's PacketArrays columns or (n, 4)
+    uint32 16-byte records."""
+    if isinstance(packets, dict):
+        arrs = [np.ascontiguousarray(packets[f], dtype=d) for f, d in zip(PACKET_COLUMNS, _PACKET_DTYPES)]
+        n = len(arrs[0])
+        for f, a in zip(PACKET_COLUMNS, arrs):
+            if len(a) != n:
+                raise ValueError(f"packet column {f} has {len(a)} entries, expected {n}")
+        return arrs, n, None, [a.ctypes.data for a in arrs]
+    rec = np.ascontiguousarray(packets, dtype=np.uint32).reshape(-1, 4)
+    return [rec], rec.shape[0], rec.ctypes.data, [None] * 5
+
+
 class CompiledRuleset:
     """Ruleset uploaded to one GPU (drop-in for classifier.py:98-185)."""
 
@@ -444,18 +459,7 @@ class CompiledRuleset:
         calls), so results land by DMA with no staging copy; ``out`` = (first
         int32, verdict uint8 or bool) host arrays to write instead."""
         torch = _torch()
-        if isinstance(packets, dict):
-            arrs = [np.ascontiguousarray(packets[f], dtype=d) for f, d in zip(PACKET_COLUMNS, _PACKET_DTYPES)]
-            n = len(arrs[0])
-            for f, a in zip(PACKET_COLUMNS, arrs):
-                if len(a) != n:
-                    raise ValueError(f"packet column {f} has {len(a)} entries, expected {n}")
-            rec_ptr, col_ptrs = None, [a.ctypes.data for a in arrs]
-        else:
-            rec = np.ascontiguousarray(packets, dtype=np.uint32).reshape(-1, 4)
-            arrs = [rec]
-            n = rec.shape[0]
-            rec_ptr, col_ptrs = rec.ctypes.data, [None] * 5
+        arrs, n, rec_ptr, col_ptrs = _host_packet_ptrs(packets)
         if out is None:
             first = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
             verdict = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy().view(np.bool_)
@@ -469,6 +473,26 @@ class CompiledRuleset:
                                                  verdict.ctypes.data, stats.ctypes.data, chunk,
                                                  _native.HOST_FIRST_MINUS1), "pfw_classify_host_ex")
         return first, verdict, stats.astype(np.int64)
+
+    def classify_host_partitions(self, packets, nodes: int, chunk: int = 1 << 23):
+        """classify_host for the function-parallel / hybrid models over
+        partition_bounds(R, nodes) (engines.py:316-369): the same chunked
+        H2D / scan / D2H pipeline, each chunk scanned by every node partition
+        and folded on the device.  Returns (first int32 [-1 = default deny],
+        comparisons int32 [sum over nodes], verdict bool, stats int64 [sum,
+        largest per-node count])."""
+        torch = _torch()
+        arrs, n, rec_ptr, col_ptrs = _host_packet_ptrs(packets)
+        first = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+        comps = torch.empty(n, dtype=torch.int32, pin_memory=True).numpy()
+        verdict = torch.empty(n, dtype=torch.uint8, pin_memory=True).numpy().view(np.bool_)
+        stats = np.zeros(2, dtype=np.uint64)
+        check(_native.lib().pfw_classify_host_partitions(self._h, int(nodes), rec_ptr, *col_ptrs, n,
+                                                         first.ctypes.data, comps.ctypes.data, verdict.ctypes.data,
+                                                         stats.ctypes.data, chunk, _native.HOST_FIRST_MINUS1),
+              "pfw_classify_host_partitions")
+        del arrs
+        return first, comps, verdict, stats.astype(np.int64)
 
     def classify_host_columns(self, cols: dict, chunk: int = 1 << 23):
         """classify_host over the five columns, first as int64 (scan_range's dtype)."""

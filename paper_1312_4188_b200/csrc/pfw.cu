@@ -948,6 +948,18 @@ __global__ void acc_init_kernel(int64_t n, uint32_t *first, uint32_t *comps) {
     }
 }
 
+// e2e chunk of the function-parallel / hybrid models: verdicts from the
+// combined first match, and the host's no-match value
+__global__ void e2e_finish_kernel(const uint8_t *accept, uint32_t *first, uint8_t *verdict, int64_t n,
+                                  uint32_t nomatch_out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = first[i];
+        if (verdict) verdict[i] = f != PFW_NO_MATCH ? accept[f] : (uint8_t)0;
+        if (f == PFW_NO_MATCH) first[i] = nomatch_out;
+    }
+}
+
 __global__ void verdict_kernel(const uint8_t *accept, const uint32_t *first, int64_t n,
                                uint8_t *verdict) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1921,7 +1933,7 @@ static bool host_is_pinned(const void *p) {
 
 static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketCols *hc, int64_t n,
                               uint32_t *h_first, uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk,
-                              uint32_t flags = 0) {
+                              uint32_t flags = 0, int64_t nodes = 0, uint32_t *h_comps = nullptr) {
     // Three-stage pipeline over E2E_SLOTS buffer slots:
     //   copy-in stream   H2D chunk k into slot k%S     (waits: scan k-S done)
     //   compute streams  scan chunk k on stream k%2    (waits: H2D k done); two
@@ -1940,6 +1952,9 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     if (h_stats) h_stats[0] = h_stats[1] = 0;
     if (n == 0) return PFW_OK;
     if ((!h_pkts && !hc) || !h_first) return set_err(PFW_ERR_INVALID, "null host buffer");
+    if (nodes < 0) return set_err(PFW_ERR_INVALID, "nodes must be >= 0");
+    if (nodes > 0 && h->index_base != 0)
+        return set_err(PFW_ERR_INVALID, "the partitioned e2e path needs a whole ruleset, not a rule shard");
     if (chunk <= 0) chunk = 1 << 23;
     // at least ~8 chunks per call (>= 256K packets each), so that smaller
     // batches pipeline too: a single chunk runs copy-in, scan and copy-out
@@ -1968,8 +1983,12 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     for (int i = 0; i < nin; i++) any_in |= stage_in[i] = !host_is_pinned(in_ptr[i]);
     const bool stage_first = !host_is_pinned(h_first);
     const bool stage_verd = h_verdict && !host_is_pinned(h_verdict);
+    const bool stage_comps = h_comps && !host_is_pinned(h_comps);
+    const bool stage_out = stage_first || stage_verd || stage_comps;
     // slot: packets (16B records, or 13B of columns) + first 4B + verdict 1B
-    const size_t slot = (((size_t)chunk * 21 + 255) / 256) * 256;
+    // (+ comparisons 4B for the partitioned models)
+    const size_t off_f = (size_t)chunk * 16, off_v = (size_t)chunk * 20, off_c = (((size_t)chunk * 21 + 15) / 16) * 16;
+    const size_t slot = ((off_c + (nodes > 0 ? (size_t)chunk * 4 : 0) + 255) / 256) * 256;
     const size_t need = S * slot + 256;
     if (h->ws_bytes < need) {
         if (h->d_ws) cudaFree(h->d_ws);
@@ -1978,7 +1997,7 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         CUDA_TRY(cudaMalloc(&h->d_ws, need));
         h->ws_bytes = need;
     }
-    if ((any_in || stage_first || stage_verd) && h->stage_bytes < S * slot) {
+    if ((any_in || stage_out) && h->stage_bytes < S * slot) {
         if (h->h_stage) cudaFreeHost(h->h_stage);
         h->h_stage = nullptr;
         h->stage_bytes = 0;
@@ -2042,10 +2061,11 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
             if (e != cudaSuccess) return e;
             const int64_t c0 = starts[(size_t)drained], m = sizes[(size_t)drained];
             char *base = hs + sl * slot;
-            HostPool::Copy cps[2];
+            HostPool::Copy cps[3];
             int ncp = 0;
-            if (stage_first) cps[ncp++] = HostPool::Copy{h_first + c0, base + (size_t)chunk * 16, (size_t)m * 4};
-            if (stage_verd) cps[ncp++] = HostPool::Copy{h_verdict + c0, base + (size_t)chunk * 20, (size_t)m};
+            if (stage_first) cps[ncp++] = HostPool::Copy{h_first + c0, base + off_f, (size_t)m * 4};
+            if (stage_verd) cps[ncp++] = HostPool::Copy{h_verdict + c0, base + off_v, (size_t)m};
+            if (stage_comps) cps[ncp++] = HostPool::Copy{h_comps + c0, base + off_c, (size_t)m * 4};
             pool.copy_many(cps, ncp);
         }
         return cudaSuccess;
@@ -2069,8 +2089,9 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         char *base = ws + sl * slot;
         char *sbase = hs + sl * slot;
         uint4 *dp = reinterpret_cast<uint4 *>(base);
-        uint32_t *df = reinterpret_cast<uint32_t *>(base + (size_t)chunk * 16);
-        uint8_t *dv = reinterpret_cast<uint8_t *>(base + (size_t)chunk * 20);
+        uint32_t *df = reinterpret_cast<uint32_t *>(base + off_f);
+        uint8_t *dv = reinterpret_cast<uint8_t *>(base + off_v);
+        uint32_t *dcm = reinterpret_cast<uint32_t *>(base + off_c);
         PacketCols dc{reinterpret_cast<const uint8_t *>(base + in_off[4]), reinterpret_cast<const uint32_t *>(base),
                       reinterpret_cast<const uint16_t *>(base + in_off[2]),
                       reinterpret_cast<const uint32_t *>(base + in_off[1]),
@@ -2110,24 +2131,49 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         E2E_TRY(cudaEventRecord(ev_in[sl], s_in));
         E2E_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
         if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
-        rc = launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
-                         h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr,
-                         (flags & PFW_HOST_FIRST_MINUS1) ? 0xFFFFFFFFu : PFW_NO_MATCH);
+        const uint32_t nomatch_out = (flags & PFW_HOST_FIRST_MINUS1) ? 0xFFFFFFFFu : PFW_NO_MATCH;
+        if (nodes == 0) {
+            rc = launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
+                             h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr,
+                             nomatch_out);
+        } else {
+            // every node partition of partition_bounds(R, nodes) folded into the
+            // chunk's first / comparisons (engines.py:349-369), then verdicts
+            const int64_t R = h->n, parts = std::min<int64_t>(nodes, std::max<int64_t>(R, 1));
+            acc_init_kernel<<<grid_for(m), 256, 0, s_comp>>>(m, df, dcm);
+            g_launches++;
+            const int64_t q = R / parts, r = R % parts;
+            for (int64_t j = 0, lo = 0; j < parts && R > 0 && rc == PFW_OK; j++) {
+                const int64_t hi = lo + q + (j < r ? 1 : 0);
+                rc = launch_scan(h, MODE_ACC, lo, hi, hc ? nullptr : dp, m, df, dcm, nullptr,
+                                 h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr);
+                lo = hi;
+            }
+            if (rc == PFW_OK) {
+                e2e_finish_kernel<<<grid_for(m), 256, 0, s_comp>>>(h->d_accept, df, h_verdict ? dv : nullptr, m,
+                                                                    nomatch_out);
+                g_launches++;
+                E2E_TRY(cudaGetLastError());
+            }
+        }
         if (rc != PFW_OK) break;
         E2E_TRY(cudaEventRecord(ev_scan[sl], s_comp));
         E2E_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
         // a staged output slot is reused by chunk k: chunk k - S's results
         // must have been copied out of it first
-        if (stage_first || stage_verd) E2E_TRY(drain(k - S + 1 > 0 ? k - S + 1 : 0));
-        E2E_TRY(cudaMemcpyAsync(stage_first ? reinterpret_cast<uint32_t *>(sbase + (size_t)chunk * 16) : h_first + c0,
+        if (stage_out) E2E_TRY(drain(k - S + 1 > 0 ? k - S + 1 : 0));
+        E2E_TRY(cudaMemcpyAsync(stage_first ? reinterpret_cast<uint32_t *>(sbase + off_f) : h_first + c0,
                                 df, m * 4, cudaMemcpyDeviceToHost, s_out));
         if (h_verdict)
-            E2E_TRY(cudaMemcpyAsync(stage_verd ? reinterpret_cast<uint8_t *>(sbase + (size_t)chunk * 20) : h_verdict + c0,
+            E2E_TRY(cudaMemcpyAsync(stage_verd ? reinterpret_cast<uint8_t *>(sbase + off_v) : h_verdict + c0,
                                     dv, m, cudaMemcpyDeviceToHost, s_out));
+        if (h_comps && nodes > 0)
+            E2E_TRY(cudaMemcpyAsync(stage_comps ? reinterpret_cast<uint32_t *>(sbase + off_c) : h_comps + c0,
+                                    dcm, m * 4, cudaMemcpyDeviceToHost, s_out));
         E2E_TRY(cudaEventRecord(ev_out[sl], s_out));
         // copy out what has landed meanwhile (keeps the host busy while the
         // GPU works; never waits for the chunk just issued)
-        if ((stage_first || stage_verd) && k >= 1) E2E_TRY(drain(k - 1 > drained ? k - 1 : drained));
+        if (stage_out && k >= 1) E2E_TRY(drain(k - 1 > drained ? k - 1 : drained));
     }
 #undef E2E_TRY
     for (auto &st : h->streams) {
@@ -2136,7 +2182,7 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
             rc = set_err(PFW_ERR_CUDA, "cudaStreamSynchronize failed: %s", cudaGetErrorString(e));
     }
     if (rc != PFW_OK) return rc;
-    if (stage_first || stage_verd) {
+    if (stage_out) {
         const cudaError_t e = drain(nchunks);
         if (e != cudaSuccess) return set_err(PFW_ERR_CUDA, "staged copy-out failed: %s", cudaGetErrorString(e));
     }
@@ -2144,7 +2190,7 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     if (trace)
         fprintf(stderr, "pfw e2e: n=%lld chunks=%lld stage_in=%d stage_out=%d call %.2f ms, slot waits %.2f ms, "
                         "staging copies %.2f ms (%d pool threads)\n", (long long)n, (long long)nchunks, (int)any_in,
-                (int)(stage_first || stage_verd), (host_seconds() - t_call) * 1e3, t_wait * 1e3, t_copy * 1e3,
+                (int)stage_out, (host_seconds() - t_call) * 1e3, t_wait * 1e3, t_copy * 1e3,
                 pool.threads());
     return PFW_OK;
 }
@@ -2175,6 +2221,20 @@ int pfw_classify_host_ex(pfw_ruleset_t h, const void *h_pkts, const uint8_t *h_p
         return set_err(PFW_ERR_INVALID, "null packet column");
     const PacketCols hc{h_proto, h_src_ip, h_src_port, h_dst_ip, h_dst_port};
     return classify_host_impl(h, nullptr, &hc, n, h_first, h_verdict, h_stats, chunk, flags);
+}
+
+int pfw_classify_host_partitions(pfw_ruleset_t h, int64_t nodes, const void *h_pkts, const uint8_t *h_proto,
+                                 const uint32_t *h_src_ip, const uint16_t *h_src_port, const uint32_t *h_dst_ip,
+                                 const uint16_t *h_dst_port, int64_t n, uint32_t *h_first, uint32_t *h_comps,
+                                 uint8_t *h_verdict, uint64_t *h_stats, int64_t chunk, uint32_t flags) {
+    if (flags & ~(uint32_t)PFW_HOST_FIRST_MINUS1) return set_err(PFW_ERR_INVALID, "unknown flags 0x%x", flags);
+    if (nodes < 1) return set_err(PFW_ERR_INVALID, "nodes must be >= 1, got %lld", (long long)nodes);
+    if (n > 0 && !h_comps) return set_err(PFW_ERR_INVALID, "null comparisons buffer");
+    if (h_pkts) return classify_host_impl(h, h_pkts, nullptr, n, h_first, h_verdict, h_stats, chunk, flags, nodes, h_comps);
+    if (n > 0 && (!h_proto || !h_src_ip || !h_src_port || !h_dst_ip || !h_dst_port))
+        return set_err(PFW_ERR_INVALID, "null packet column");
+    const PacketCols hc{h_proto, h_src_ip, h_src_port, h_dst_ip, h_dst_port};
+    return classify_host_impl(h, nullptr, &hc, n, h_first, h_verdict, h_stats, chunk, flags, nodes, h_comps);
 }
 
 int pfw_generate_traffic(int device, uint64_t seed, int64_t n, int proto, uint32_t src_base,

@@ -415,6 +415,14 @@ class Engine:
                 first, verdict, st = self._data_host(compiled, packets, n)
             return EngineResult(first, None, verdict, ClassifyStats(int(st[0]), n, time.perf_counter_ns() - start,
                                                                     int(st[1])), num_rules=R)
+        if host and self.gpus == 1:
+            # function-parallel / hybrid: the same H2D / scan / D2H pipeline,
+            # every node partition per chunk folded on the device
+            with _nvtx(f"Engine.run_arrays: e2e {model.value} (host batch)"):
+                comp = self._copy(compiled, self._dev(0))
+                first_h, comps_h, verdict, st = comp.classify_host_partitions(packets, self.config.nodes)
+            return EngineResult(first_h, comps_h, verdict, ClassifyStats(int(st[0]), n, time.perf_counter_ns() - start,
+                                                                        int(st[1])), num_rules=R)
         if host:
             with _nvtx("Engine.run_arrays: upload"):
                 pk = packets if isinstance(packets, dict) else PacketArrays.unpack_host(packets)

@@ -24,7 +24,7 @@ if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
 
 import paper_1312_4188_b200 as pfw  # noqa: E402
 from paper_1312_4188_b200 import _native  # noqa: E402
-from paper_1312_4188_b200.classifier import MatchResults  # noqa: E402
+from paper_1312_4188_b200.classifier import MatchResults, first_to_host  # noqa: E402
 from oracle import oracle  # noqa: E402
 from oracle.oracle import PKT_FIELDS  # noqa: E402
 
@@ -55,6 +55,57 @@ def test_run_arrays_host_batch_equals_golden(layout):
         np.testing.assert_array_equal(res.verdict_accept, g["verdict"])
         assert res.stats.total_comparisons == int(g["total_comparisons"]) == int(res.comparisons.sum())
         assert res.stats.max_worker_comparisons == int(g["max_worker_comparisons"])
+
+
+@pytest.mark.parametrize("model", ["function", "hybrid"])
+@pytest.mark.parametrize("layout", ["pageable", "pinned", "records"])
+def test_run_arrays_host_batch_partitioned_models(model, layout):
+    """Function-parallel / hybrid with a host batch: the chunked H2D / scan /
+    D2H pipeline with every node partition folded on the device per chunk
+    (pfw_classify_host_partitions) -- first, per-packet comparisons, verdicts
+    and stats equal the reference's goldens for every node count."""
+    g = golden("engine_r503_t600.npz")
+    rules, traffic = golden_rules("r503_s24_w30"), golden_traffic("t600_s25")
+    c = pfw.CompiledRuleset.from_columns(rules, device=0)
+    pk = traffic
+    if layout == "pinned":
+        pk = _pinned(pk)
+    elif layout == "records":
+        pk = pfw.PacketArrays.pack_host(*[pk[f] for f in PKT_FIELDS])
+    for nodes in (1, 2, 3, 8, 64, 512):
+        res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=nodes)).run_arrays(c, pk)
+        key = f"{model}_{nodes}"
+        np.testing.assert_array_equal(res.first, g[f"{key}_first"])
+        np.testing.assert_array_equal(res.comparisons, g[f"{key}_comps"])
+        want_v = np.where(g[f"{key}_first"] >= 0, rules["action_accept"][np.maximum(g[f"{key}_first"], 0)], False)
+        np.testing.assert_array_equal(res.verdict_accept, want_v)
+        s = res.stats
+        assert [s.total_comparisons, s.max_worker_comparisons, s.packets_processed] == g[f"{key}_stats"].tolist()
+
+
+def test_partitioned_host_pipeline_many_chunks_vs_device():
+    """Several chunks (ramped schedule), pageable in and out, compressed rows
+    and a 7-node split: identical to the device-resident partition scans."""
+    rules = oracle.gen_ruleset(30_000, 3, wp=0.2)
+    c = pfw.CompiledRuleset.from_columns(rules, device=0)
+    n = 3_000_001
+    pk = oracle.gen_traffic_uniform(n, 78)
+    first, comps, verdict, st = c.classify_host_partitions(pk, 7, chunk=1 << 18)
+    p = pfw.PacketArrays.from_columns(*[pk[f] for f in PKT_FIELDS], device=0)
+    df = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    dc = torch.empty(n, dtype=torch.int32, device="cuda:0")
+    ds = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+    c.scan_partitions(p, 7, df, dc, ds)
+    want_f = first_to_host(df)
+    np.testing.assert_array_equal(first, want_f)
+    np.testing.assert_array_equal(comps, dc.cpu().numpy())
+    np.testing.assert_array_equal(verdict, np.where(want_f >= 0, rules["action_accept"][np.maximum(want_f, 0)], False))
+    assert st.tolist() == ds.cpu().numpy().tolist()
+    idx = np.arange(0, n, 9973)
+    sub = {f: v[idx] for f, v in pk.items()}
+    f2, c2, _, _ = oracle.engine_run(rules, sub, "function", 7)
+    np.testing.assert_array_equal(first[idx], f2)
+    np.testing.assert_array_equal(comps[idx], c2)
 
 
 def test_host_batch_staging_large_pageable():
