@@ -76,8 +76,9 @@ def load_l2_peak():
 def probe_l2_live(dev) -> dict | None:
     """The roofline peak measured on this device in this run: random 128-byte
     lines read by 8-lane groups from a 48 MiB L2-resident buffer (the
-    match-set scan's access pattern; pfw_probe_l2_lines), 4/8/16 lines in
-    flight per lane x 4/5/6/8 blocks per SM, best shape."""
+    match-set scan's access pattern; pfw_probe_l2_lines), 8/16 lines in
+    flight per lane x 5/6/8 blocks per SM (the round-1 sweep's best region;
+    ~2 ms launches: shorter ones read low), best shape."""
     import torch
     from paper_1312_4188_b200 import _native
     try:
@@ -87,9 +88,9 @@ def probe_l2_live(dev) -> dict | None:
         st = torch.cuda.current_stream(dev)
         lib = _native.lib()
         best, shape = 0.0, None
-        for occ in (4, 5, 6, 8):
-            for k in (4, 8, 16):
-                iters = 2048 if k < 16 else 1024
+        for occ in (5, 6, 8):
+            for k in (8, 16):
+                iters = max(128, 66000 // (occ * k))  # ~40 GB of line reads per timed launch (~2 ms)
                 _native.check(lib.pfw_probe_l2_lines(buf.data_ptr(), buf.numel(), k, occ, 16, st.cuda_stream),
                               "pfw_probe_l2_lines")
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -692,7 +693,7 @@ def run_ours(args, w, world, rank, local) -> int:
     if live:
         l2_peak = live["gbs"]
         l2_src = (f"measured in this run on this device (pfw_probe_l2_lines: random 128-byte lines, 8-lane "
-                  f"groups, 48 MiB L2-resident buffer, best of 12 shapes: {live['shape']}); "
+                  f"groups, 48 MiB L2-resident buffer, best of 6 shapes: {live['shape']}); "
                   f"round-1 probe file: {l2_file} GB/s")
     int_peak = sms * INT32_LANES_PER_SM_CLK * clk * 1e6 / 1e12  # T int-ops/s
     int_peak_src = (f"derived: {sms} SMs x {INT32_LANES_PER_SM_CLK} int32 lanes/clk x sm_max_mhz {clk:.0f} "
