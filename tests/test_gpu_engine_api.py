@@ -173,3 +173,30 @@ def test_gpus_beyond_visible_devices_is_config_error():
     have = _native.device_count()
     with pytest.raises(pfw.ConfigError, match="CUDA devices are visible"):
         pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.DATA_PARALLEL, gpus=have + 1))
+
+
+def test_partitioned_host_pipeline_pageable_outputs_c_abi():
+    """pfw_classify_host_partitions called directly with ordinary numpy
+    output arrays (first, comparisons, verdicts staged out through the pinned
+    ring) and 16-byte records in: equal to the pinned-output call."""
+    rules = oracle.gen_ruleset(5000, 11, wp=0.2)
+    c = pfw.CompiledRuleset.from_columns(rules, device=0)
+    n = 2_500_003
+    pk = oracle.gen_traffic_uniform(n, 12)
+    rec = pfw.PacketArrays.pack_host(*[pk[f] for f in PKT_FIELDS])
+    want_f, want_c, want_v, want_st = c.classify_host_partitions(pk, 5, chunk=1 << 18)
+    f = np.empty(n, np.int32)
+    cm = np.empty(n, np.int32)
+    v = np.empty(n, np.uint8)
+    st = np.zeros(2, np.uint64)
+    _native.check(_native.lib().pfw_classify_host_partitions(
+        c.handle, 5, rec.ctypes.data, None, None, None, None, None, n, f.ctypes.data, cm.ctypes.data,
+        v.ctypes.data, st.ctypes.data, 1 << 18, _native.HOST_FIRST_MINUS1), "pfw_classify_host_partitions")
+    np.testing.assert_array_equal(f, want_f)
+    np.testing.assert_array_equal(cm, want_c)
+    np.testing.assert_array_equal(v.view(np.bool_), want_v)
+    assert st.astype(np.int64).tolist() == want_st.tolist()
+    with pytest.raises(ValueError):   # comparisons buffer required; nodes >= 1
+        _native.check(_native.lib().pfw_classify_host_partitions(
+            c.handle, 0, rec.ctypes.data, None, None, None, None, None, n, f.ctypes.data, cm.ctypes.data,
+            None, None, 0, 0), "pfw_classify_host_partitions")
