@@ -56,7 +56,6 @@ int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel,
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
 int g_ms_lean_sum = 2;         // whole-table summary scans over compressed rows: lean candidate walk (0 general kernel, 1 at 5 / 2 at 4 blocks per SM)
 int g_ms_lean_cmp = 3;         // whole-table scans over compressed rows: 0 general kernel, 1 lean 8-lane, 2 lean 4-lane, 3 lean 8-lane with u16 parked indices (<= MS_CP_BLOCKS blocks, else 1)
-int g_ms_odd_rows = 0;         // plain rows an odd number of lines long (L2 slice spread; experiment)
 unsigned long long *g_counter_dev = nullptr;  // device of the first counting launch
 
 struct MsBuildArgs {
@@ -1686,14 +1685,6 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     }
     MatchSet *m = new MatchSet();
     m->wp = (((n + 31) / 32 + 127) / 128) * 128;  // whole 4-word-per-lane steps
-    if (g_ms_odd_rows && !(g_ms_compress == 1)) {
-        // rows an odd number of 128-byte lines long: the rows' leading lines
-        // (where most scans end) then spread over every L2 slice-hash pattern
-        // instead of only multiples of 512 bytes; shapes whose step does not
-        // divide the row scan with the window masks
-        m->wp = (((n + 31) / 32 + 31) / 32) * 32;
-        if ((m->wp / 32) % 2 == 0) m->wp += 32;
-    }
     m->sp_rows = (int64_t)bsp.size();
     m->rows[MSD_SRC] = (int64_t)bs.size();
     m->rows[MSD_DST] = (int64_t)bd.size();

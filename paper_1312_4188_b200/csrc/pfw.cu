@@ -1502,8 +1502,6 @@ int pfw_set_tuning(const char *key, int64_t value) {
         if (value < 0 || value > 3)
             return set_err(PFW_ERR_INVALID, "ms_lean_cmp: 0 off, 1 8-lane, 2 4-lane groups, 3 8-lane with u16 parked indices");
         g_ms_lean_cmp = (int)value;
-    } else if (!strcmp(key, "ms_odd_rows")) {
-        g_ms_odd_rows = value != 0;
     } else if (!strcmp(key, "ms_lean")) {
         if (value < 0 || value > 6)
             return set_err(PFW_ERR_INVALID, "ms_lean: 0 general kernel, 1 lean (8-lane groups), 2 lean (4-lane "
