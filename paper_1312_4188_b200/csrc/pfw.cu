@@ -2021,7 +2021,7 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     std::vector<int64_t> sizes;
     {
         std::vector<int64_t> ramp;
-        for (int64_t r = chunk / 8; r < chunk; r *= 2)
+        for (int64_t r = chunk / 8; r > 0 && r < chunk; r *= 2)  // (chunk < 8: no ramp)
             if (r >= (1 << 16)) ramp.push_back(r);
         int64_t rs = 0;
         for (int64_t r : ramp) rs += r;

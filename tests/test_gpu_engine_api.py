@@ -200,3 +200,26 @@ def test_partitioned_host_pipeline_pageable_outputs_c_abi():
         _native.check(_native.lib().pfw_classify_host_partitions(
             c.handle, 0, rec.ctypes.data, None, None, None, None, None, n, f.ctypes.data, cm.ctypes.data,
             None, None, 0, 0), "pfw_classify_host_partitions")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 8, 9, 100, 65_535, 262_143, 262_145, 524_289])
+def test_host_pipeline_tiny_and_odd_batches(n):
+    """Host batches of every awkward size through the e2e pipeline (chunks
+    smaller than the ramp, one-packet batches, just past a chunk boundary),
+    both the whole-table and the partitioned models -- against the oracle."""
+    rules = oracle.gen_ruleset(3000, 21, wp=0.3)
+    c = pfw.CompiledRuleset.from_columns(rules, device=0)
+    pk = oracle.gen_traffic_uniform(n, 22 + n)
+    f, v, st = c.classify_host(pk)
+    want = oracle.scan_range(rules, pk, 0, 3000)
+    np.testing.assert_array_equal(f, want)
+    np.testing.assert_array_equal(v, np.where(want >= 0, rules["action_accept"][np.maximum(want, 0)], False))
+    comps = oracle.sequential_comparisons(want, 3000)
+    assert st.tolist() == [int(comps.sum()), int(comps.max())]
+    f2, c2, v2, st2 = c.classify_host_partitions(pk, 3)
+    wf, wc, total, mx = oracle.engine_run(rules, pk, "function", 3)
+    np.testing.assert_array_equal(f2, wf)
+    np.testing.assert_array_equal(c2, wc)
+    assert st2.tolist() == [total, mx]
+    res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.DATA_PARALLEL)).run_arrays(c, pk)
+    np.testing.assert_array_equal(res.first, want)
