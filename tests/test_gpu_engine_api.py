@@ -223,3 +223,19 @@ def test_host_pipeline_tiny_and_odd_batches(n):
     assert st2.tolist() == [total, mx]
     res = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.DATA_PARALLEL)).run_arrays(c, pk)
     np.testing.assert_array_equal(res.first, want)
+
+
+@pytest.mark.parametrize("model", ["data", "function", "hybrid"])
+def test_host_pipeline_empty_ruleset_and_batch(model):
+    """Empty ruleset (every packet default-denied after 0 comparisons) and
+    empty batches through the host pipelines, every model."""
+    empty = pfw.Ruleset()
+    pk = oracle.gen_traffic_uniform(1000, 5)
+    eng = pfw.Engine(pfw.EngineConfig(pfw.ExecutionModel.from_key(model), nodes=4))
+    res = eng.run_arrays(empty, pk)
+    assert (np.asarray(res.first) == -1).all() and not np.asarray(res.verdict_accept).any()
+    assert (np.asarray(res.comparisons) == 0).all()
+    assert (res.stats.total_comparisons, res.stats.max_worker_comparisons) == (0, 0)
+    rs = pfw.generate_ruleset(pfw.RulesetGenParams(100, seed=3))
+    res0 = eng.run_arrays(rs, {f: v[:0] for f, v in pk.items()})
+    assert len(res0) == 0
