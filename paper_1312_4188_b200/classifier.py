@@ -90,8 +90,11 @@ class ClassifyStats:
 def classify(ruleset: Ruleset, packet: Packet) -> MatchResult:
     """First match with early exit, default deny (classifier.py:54-59), on the GPU."""
     compiled = compile_ruleset(ruleset)
-    first = compiled.scan_range(PacketArrays.from_packets([packet], compiled.device), 0,
-                                compiled.num_rules)
+    # one packet through the host pipeline's packed tiny-batch path (one copy each way)
+    cols = {"proto": np.array([int(packet.proto)], np.uint8), "src_ip": np.array([packet.src_ip], np.uint32),
+            "src_port": np.array([packet.src_port], np.uint16), "dst_ip": np.array([packet.dst_ip], np.uint32),
+            "dst_port": np.array([packet.dst_port], np.uint16)}
+    first, _, _ = compiled.classify_host(cols)
     idx = int(first[0])
     if idx < 0:
         return MatchResult(Action.DROP, None, compiled.num_rules)

@@ -134,6 +134,7 @@ int g_first_pass = 1024; // rules in the first pass (0 = single pass); passes do
 constexpr int MAX_PASSES = 32;
 constexpr int MAX_PEERS = 64;
 constexpr int E2E_SLOTS = 3;
+constexpr int64_t E2E_SMALL = 4096;  // host batches up to this size take the packed one-copy path
 constexpr int MAX_CHAINS = 257;
 int g_proto_split = 0;   // opt-in: scan protocol-split rule chains
 int g_short_circuit = 0; // warp-level short-circuit of the port tests (SC variant; measured slower)
@@ -202,6 +203,7 @@ struct pfw_ruleset {
     size_t ws_bytes = 0;
     void *h_stage = nullptr;       // pinned staging ring for pageable e2e buffers (same slots as d_ws)
     size_t stage_bytes = 0;
+    void *h_small = nullptr;       // pinned buffer of the packed tiny-batch path (E2E_SMALL packets)
     cudaStream_t streams[4] = {};  // e2e copy-in, compute x2 (alternating chunks), copy-out
     cudaEvent_t events[3 * 3] = {};                          // e2e per-slot in / scan / out
     ScanWs ws;         // default (calls on the caller's stream)
@@ -1663,6 +1665,7 @@ int pfw_ruleset_destroy(pfw_ruleset_t h) {
     if (h->d_accept) cudaFree(h->d_accept);
     if (h->d_ws) cudaFree(h->d_ws);
     if (h->h_stage) cudaFreeHost(h->h_stage);
+    if (h->h_small) cudaFreeHost(h->h_small);
     free_ws(h->ws);
     if (h->d_peers) cudaFree(h->d_peers);
     for (auto &ch : h->chains) {
@@ -2010,6 +2013,97 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
     cudaEvent_t *ev_in = h->events, *ev_scan = h->events + S, *ev_out = h->events + 2 * S;
     char *ws = static_cast<char *>(h->d_ws);
     uint64_t *d_stats = reinterpret_cast<uint64_t *>(ws + S * slot);
+    const uint32_t nomatch_out = (flags & PFW_HOST_FIRST_MINUS1) ? 0xFFFFFFFFu : PFW_NO_MATCH;
+    // the scan of one chunk (m packets in the slot at `base`) on stream `sc`
+    auto scan_chunk = [&](char *base, int64_t m, cudaStream_t sc, ScanWs *wsp) -> int {
+        const uint4 *dp = reinterpret_cast<const uint4 *>(base);
+        uint32_t *df = reinterpret_cast<uint32_t *>(base + off_f);
+        uint8_t *dv = reinterpret_cast<uint8_t *>(base + off_v);
+        uint32_t *dcm = reinterpret_cast<uint32_t *>(base + off_c);
+        PacketCols dc{reinterpret_cast<const uint8_t *>(base + (size_t)chunk * 12), reinterpret_cast<const uint32_t *>(base),
+                      reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 8),
+                      reinterpret_cast<const uint32_t *>(base + (size_t)chunk * 4),
+                      reinterpret_cast<const uint16_t *>(base + (size_t)chunk * 10)};
+        if (nodes == 0)
+            return launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
+                               h_stats ? d_stats : nullptr, sc, wsp, nullptr, hc ? &dc : nullptr, nomatch_out);
+        // every node partition of partition_bounds(R, nodes) folded into the
+        // chunk's first / comparisons (engines.py:349-369), then verdicts
+        const int64_t R = h->n, parts = std::min<int64_t>(nodes, std::max<int64_t>(R, 1));
+        acc_init_kernel<<<grid_for(m), 256, 0, sc>>>(m, df, dcm);
+        g_launches++;
+        const int64_t q = R / parts, r = R % parts;
+        for (int64_t j = 0, lo = 0; j < parts && R > 0; j++) {
+            const int64_t hi = lo + q + (j < r ? 1 : 0);
+            const int rc2 = launch_scan(h, MODE_ACC, lo, hi, hc ? nullptr : dp, m, df, dcm, nullptr,
+                                        h_stats ? d_stats : nullptr, sc, wsp, nullptr, hc ? &dc : nullptr);
+            if (rc2 != PFW_OK) return rc2;
+            lo = hi;
+        }
+        e2e_finish_kernel<<<grid_for(m), 256, 0, sc>>>(h->d_accept, df, h_verdict ? dv : nullptr, m, nomatch_out);
+        g_launches++;
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? PFW_OK : set_err(PFW_ERR_CUDA, "e2e finish: %s", cudaGetErrorString(e));
+    };
+    // tiny batches (the serving case), any host memory: the inputs packed
+    // into one pinned buffer in the slot's layout, ONE copy in, the scan, ONE
+    // copy out of first / verdict / comparisons (+ the stats), one
+    // synchronize; the host copies are a few KB
+    if (n <= E2E_SMALL && n <= chunk) {
+        NvtxRange nv0("pfw_classify_host: packed tiny batch");
+        if (!h->h_small) CUDA_TRY(cudaHostAlloc(&h->h_small, (size_t)E2E_SMALL * 32 + 512, cudaHostAllocPortable));
+        char *hsm = static_cast<char *>(h->h_small);
+        const size_t in_bytes = hc ? (size_t)n * 13 : (size_t)n * 16;
+        for (int i = 0; i < nin; i++)
+            memcpy(hsm + (i == 0 || !hc ? 0 : (size_t)n * (i == 1 ? 4 : i == 2 ? 8 : i == 3 ? 10 : 12)), in_ptr[i],
+                   (size_t)n * in_w[i]);
+        cudaStream_t sc = h->streams[1];
+        char *base = ws;
+        if (h_stats) CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16, sc));
+        CUDA_TRY(cudaMemcpyAsync(base, hsm, in_bytes, cudaMemcpyHostToDevice, sc));
+        int rc0 = scan_chunk(base, n, sc, &h->ws_e2e[0]);
+        const size_t out_end = nodes > 0 ? off_c + (size_t)n * 4 : off_v + (size_t)n;
+        const size_t stats_at = ((out_end + 15) / 16) * 16;
+        if (rc0 == PFW_OK) {
+            cudaError_t e = cudaMemcpyAsync(hsm + off_f, base + off_f, out_end - off_f, cudaMemcpyDeviceToHost, sc);
+            if (e == cudaSuccess && h_stats) e = cudaMemcpyAsync(hsm + stats_at, d_stats, 16, cudaMemcpyDeviceToHost, sc);
+            if (e != cudaSuccess) rc0 = set_err(PFW_ERR_CUDA, "tiny-batch copy failed: %s", cudaGetErrorString(e));
+        }
+        const cudaError_t es = cudaStreamSynchronize(sc);
+        if (rc0 == PFW_OK && es != cudaSuccess)
+            rc0 = set_err(PFW_ERR_CUDA, "cudaStreamSynchronize failed: %s", cudaGetErrorString(es));
+        if (rc0 != PFW_OK) return rc0;
+        memcpy(h_first, hsm + off_f, (size_t)n * 4);
+        if (h_verdict) memcpy(h_verdict, hsm + off_v, (size_t)n);
+        if (h_comps && nodes > 0) memcpy(h_comps, hsm + off_c, (size_t)n * 4);
+        if (h_stats) memcpy(h_stats, hsm + stats_at, 16);
+        return PFW_OK;
+    }
+    // one chunk, pinned buffers (small batches): copy in, scan and copy out
+    // on one stream, one synchronize -- no events, no cross-stream waits
+    if (n <= chunk && !any_in && !stage_out) {
+        NvtxRange nv1("pfw_classify_host: single-stream small batch");
+        cudaStream_t sc = h->streams[1];
+        char *base = ws;
+        if (h_stats) CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16, sc));
+        for (int i = 0; i < nin; i++)
+            CUDA_TRY(cudaMemcpyAsync(base + (i == 0 || !hc ? 0 : (size_t)chunk * (i == 1 ? 4 : i == 2 ? 8 : i == 3 ? 10 : 12)),
+                                     in_ptr[i], (size_t)n * in_w[i], cudaMemcpyHostToDevice, sc));
+        int rc1 = scan_chunk(base, n, sc, &h->ws_e2e[0]);
+        if (rc1 == PFW_OK) {
+            cudaError_t e = cudaMemcpyAsync(h_first, base + off_f, (size_t)n * 4, cudaMemcpyDeviceToHost, sc);
+            if (e == cudaSuccess && h_verdict)
+                e = cudaMemcpyAsync(h_verdict, base + off_v, (size_t)n, cudaMemcpyDeviceToHost, sc);
+            if (e == cudaSuccess && h_comps && nodes > 0)
+                e = cudaMemcpyAsync(h_comps, base + off_c, (size_t)n * 4, cudaMemcpyDeviceToHost, sc);
+            if (e == cudaSuccess && h_stats) e = cudaMemcpyAsync(h_stats, d_stats, 16, cudaMemcpyDeviceToHost, sc);
+            if (e != cudaSuccess) rc1 = set_err(PFW_ERR_CUDA, "small-batch copy failed: %s", cudaGetErrorString(e));
+        }
+        const cudaError_t es = cudaStreamSynchronize(sc);  // (always: queued copies target the caller's buffers)
+        if (rc1 == PFW_OK && es != cudaSuccess)
+            rc1 = set_err(PFW_ERR_CUDA, "cudaStreamSynchronize failed: %s", cudaGetErrorString(es));
+        return rc1;
+    }
     if (h_stats) {
         CUDA_TRY(cudaMemsetAsync(d_stats, 0, 16, s_in));
         CUDA_TRY(cudaEventRecord(ev_in[0], s_in));  // ordered before every compute stream below
@@ -2086,14 +2180,9 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         cudaStream_t s_comp = h->streams[1 + (k & 1)];
         char *base = ws + sl * slot;
         char *sbase = hs + sl * slot;
-        uint4 *dp = reinterpret_cast<uint4 *>(base);
         uint32_t *df = reinterpret_cast<uint32_t *>(base + off_f);
         uint8_t *dv = reinterpret_cast<uint8_t *>(base + off_v);
         uint32_t *dcm = reinterpret_cast<uint32_t *>(base + off_c);
-        PacketCols dc{reinterpret_cast<const uint8_t *>(base + in_off[4]), reinterpret_cast<const uint32_t *>(base),
-                      reinterpret_cast<const uint16_t *>(base + in_off[2]),
-                      reinterpret_cast<const uint32_t *>(base + in_off[1]),
-                      reinterpret_cast<const uint16_t *>(base + in_off[3])};
         if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_in, ev_scan[sl], 0));   // packets slot free
         if (any_in) {
             // the staging slot's previous H2D (chunk k - S) must have read it
@@ -2129,31 +2218,7 @@ static int classify_host_impl(pfw_ruleset_t h, const void *h_pkts, const PacketC
         E2E_TRY(cudaEventRecord(ev_in[sl], s_in));
         E2E_TRY(cudaStreamWaitEvent(s_comp, ev_in[sl], 0));
         if (k >= S) E2E_TRY(cudaStreamWaitEvent(s_comp, ev_out[sl], 0));  // result slot drained
-        const uint32_t nomatch_out = (flags & PFW_HOST_FIRST_MINUS1) ? 0xFFFFFFFFu : PFW_NO_MATCH;
-        if (nodes == 0) {
-            rc = launch_scan(h, MODE_WRITE, 0, h->n, hc ? nullptr : dp, m, df, nullptr, h_verdict ? dv : nullptr,
-                             h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr,
-                             nomatch_out);
-        } else {
-            // every node partition of partition_bounds(R, nodes) folded into the
-            // chunk's first / comparisons (engines.py:349-369), then verdicts
-            const int64_t R = h->n, parts = std::min<int64_t>(nodes, std::max<int64_t>(R, 1));
-            acc_init_kernel<<<grid_for(m), 256, 0, s_comp>>>(m, df, dcm);
-            g_launches++;
-            const int64_t q = R / parts, r = R % parts;
-            for (int64_t j = 0, lo = 0; j < parts && R > 0 && rc == PFW_OK; j++) {
-                const int64_t hi = lo + q + (j < r ? 1 : 0);
-                rc = launch_scan(h, MODE_ACC, lo, hi, hc ? nullptr : dp, m, df, dcm, nullptr,
-                                 h_stats ? d_stats : nullptr, s_comp, &h->ws_e2e[k & 1], nullptr, hc ? &dc : nullptr);
-                lo = hi;
-            }
-            if (rc == PFW_OK) {
-                e2e_finish_kernel<<<grid_for(m), 256, 0, s_comp>>>(h->d_accept, df, h_verdict ? dv : nullptr, m,
-                                                                    nomatch_out);
-                g_launches++;
-                E2E_TRY(cudaGetLastError());
-            }
-        }
+        rc = scan_chunk(base, m, s_comp, &h->ws_e2e[k & 1]);
         if (rc != PFW_OK) break;
         E2E_TRY(cudaEventRecord(ev_scan[sl], s_comp));
         E2E_TRY(cudaStreamWaitEvent(s_out, ev_scan[sl], 0));
