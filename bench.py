@@ -821,7 +821,8 @@ def run_ours(args, w, world, rank, local) -> int:
     # memory (classifier.py:62-95, 13 B/packet); H2D, scans and D2H of the
     # first-match index + verdict inside the timed region
     e2e = None
-    if not args.no_e2e and w.model != "function":
+    fn_e2e = w.model == "function"  # (N = 1 only: ranks hold rule shards, not whole rulesets)
+    if not args.no_e2e and (w.model != "function" or (world == 1 and fused is None)):
         hc = pkts.columns()
         pinned = {}
         for f, a in hc.items():
@@ -829,7 +830,8 @@ def run_ours(args, w, world, rank, local) -> int:
                             pin_memory=True)
             t.numpy().view(a.dtype)[:] = a
             pinned[f] = t.numpy().view(a.dtype)
-        eng = Engine(EngineConfig(ExecutionModel.DATA_PARALLEL), device=local)
+        eng = Engine(EngineConfig(ExecutionModel.FUNCTION_PARALLEL, nodes=world) if fn_e2e
+                     else EngineConfig(ExecutionModel.DATA_PARALLEL), device=local)
         ref_first = first.cpu().numpy()
 
         def e2e_step(batch):
@@ -857,11 +859,14 @@ def run_ours(args, w, world, rank, local) -> int:
         link = host_link_peaks(dev)
         e2e_s = e_s / args.steps
         e2e = {"value": pk_per_step * args.steps / e_s / 1e6, "unit": "Mpps",
-               "h2d_bytes_per_step": n * 13, "d2h_bytes_per_step": n * 5,
-               "api": "Engine(EngineConfig(DATA_PARALLEL)).run_arrays(compiled, host_columns) -> EngineResult "
-                      "(the reference's five PacketArrays columns as numpy arrays in pinned host memory; "
-                      "pfw_classify_host_ex: chunked H2D / scan / D2H pipeline, copy-in + 2 compute + copy-out "
-                      "streams; results int32 first (-1 = default deny) + bool verdict in pinned memory)",
+               "h2d_bytes_per_step": n * 13, "d2h_bytes_per_step": n * (9 if fn_e2e else 5),
+               "api": (f"Engine(EngineConfig(FUNCTION_PARALLEL, nodes={world})).run_arrays(compiled, host_columns) "
+                       "-> EngineResult (pfw_classify_host_partitions: the same pipeline, per-packet comparisons "
+                       "copied out too)" if fn_e2e else
+                       "Engine(EngineConfig(DATA_PARALLEL)).run_arrays(compiled, host_columns) -> EngineResult "
+                       "(the reference's five PacketArrays columns as numpy arrays in pinned host memory; "
+                       "pfw_classify_host_ex: chunked H2D / scan / D2H pipeline, copy-in + 2 compute + copy-out "
+                       "streams; results int32 first (-1 = default deny) + bool verdict in pinned memory)"),
                "kernel_launches_per_step": e_launches,
                # the host link bounds this path: H2D of the 13-byte columns
                "h2d_gbs": round(n * 13 / e2e_s / 1e9, 2), "h2d_peak_gbs": link["h2d_gbs"],
