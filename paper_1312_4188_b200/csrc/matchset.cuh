@@ -19,11 +19,21 @@
 // Layout in HBM (struct MatchSet): the four dimensions' rows in one
 // allocation, rows x wp words each (wp = rules/32 rounded up to a whole step
 // of 128 words, 512 bytes); optional block summaries (one bit per 1024-rule
-// block per row); IP value -> interval through the sorted boundaries and a
-// 65536-entry table of boundary ranges per /16 block; port value -> interval
-// through a direct 65536-entry table; protocol -> class through a 256-entry
-// table.  The lookup tables (~1.5 MB) and the rows' leading lines (where most
-// first matches are) stay resident in L2 up to ~10K rules.
+// block per row); compressed rows above ~24K rules (each (dimension, 1024-rule
+// block) stores its distinct lines once, rows hold u16 line indices, a dense
+// head array the first 8 blocks'); IP value -> interval through a 65536-entry
+// table of 16-byte /16-block entries (boundary range + the first 6 boundaries'
+// low halves) and the sorted boundaries; port value -> interval through a
+// direct 65536-entry table; protocol -> class through a 256-entry table.  The
+// lookup tables (~2.5 MB) and the rows' leading lines (where most first
+// matches are) stay resident in L2 up to ~10K rules.
+//
+// Kernels: ms_lean_kernel (whole-table scans over plain rows: data / grid /
+// oracle configs), ms_lean_cmp_kernel (compressed rows: function config),
+// ms_lean_sum_kernel (block-summary candidate walk: adversarial config),
+// ms_scan_kernel (general: windows, accumulate / fused-combine epilogues, the
+// other shapes), plus the build kernels.  DESIGN.md section 3 has the shapes
+// and their measurements.
 
 constexpr int MS_BLOCK = 256;
 #ifndef PFW_MS_MINB
