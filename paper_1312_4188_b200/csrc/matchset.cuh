@@ -246,6 +246,7 @@ struct MsView {
     const uint32_t *ipb[2];   // src / dst boundaries
     const uint4 *ipc[2];      // per /16 block: first boundary index | count << 24, the first 6 boundaries' low halves
     const uint16_t *port[2];  // sport / dport -> interval
+    const uint32_t *pbk[2];   // sport / dport buckets of 32 ports: 2048 boundary-bit words, 2048 u16 bases
     const uint8_t *cls;       // protocol -> class
     int64_t wp;
     uint32_t sp_rows;
@@ -306,6 +307,15 @@ __device__ __forceinline__ uint32_t ms_ip_row(const uint32_t *b, const uint4 *c,
         else hi = mid;
     }
     return lo - 1;
+}
+
+// port -> interval from the 32-port bucket table (two independent L1-resident
+// loads; the lean plain-row kernel, whose carveout leaves L1 room for them --
+// the compressed-row / summary kernels' larger shared memory does not: -1%)
+__device__ __forceinline__ uint32_t ms_port_row(const uint32_t *bk, uint32_t port) {
+    const uint32_t b = port >> 5;
+    const uint32_t base = __ldg(reinterpret_cast<const uint16_t *>(bk + 2048) + b);
+    return base + (uint32_t)__popc(__ldg(bk + b) & (0xFFFFFFFFu >> (31u - (port & 31u))));
 }
 
 // The four rows' words of one step, loaded by one asm block so that all four
@@ -934,8 +944,8 @@ __global__ void __launch_bounds__(MS_BLOCK, MINB)
             if (i < n) {
                 const uint4 r = make_uint4(
                     ms_ip_row(t.ipb[0], t.ipc[0], v[k].x), ms_ip_row(t.ipb[1], t.ipc[1], v[k].y),
-                    (uint32_t)__ldg(t.cls + (v[k].w & 0xFFu)) * t.sp_rows + __ldg(t.port[0] + (v[k].z >> 16)),
-                    __ldg(t.port[1] + (v[k].z & 0xFFFFu)));
+                    (uint32_t)__ldg(t.cls + (v[k].w & 0xFFu)) * t.sp_rows + ms_port_row(t.pbk[0], v[k].z >> 16),
+                    ms_port_row(t.pbk[1], v[k].z & 0xFFFFu));
                 PFW_CHECK(r.x < t.nrows[0] && r.y < t.nrows[1] && r.z < t.nrows[2] && r.w < t.nrows[3]);
                 s_off[warp][k * 32 + lane] = make_uint4(r.x * wp + t.off[0], r.y * wp + t.off[1],
                                                         r.z * wp + t.off[2], r.w * wp + t.off[3]);
@@ -1461,6 +1471,8 @@ void ms_free(MatchSet *m) {
         if (c) cudaFree(c);
     for (auto *q : m->d_port)
         if (q) cudaFree(q);
+    for (auto *q : m->d_pbk)
+        if (q) cudaFree(q);
     if (m->d_cls) cudaFree(m->d_cls);
     delete m;
 }
@@ -1778,6 +1790,20 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     if (e == cudaSuccess) e = ms_upload(&m->d_ipc[1], ipc[1].data(), ipc[1].size());
     if (e == cudaSuccess) e = ms_upload(&m->d_port[0], ptab[0].data(), ptab[0].size());
     if (e == cudaSuccess) e = ms_upload(&m->d_port[1], ptab[1].data(), ptab[1].size());
+    // port buckets of 32 ports: interval(p) = base[p >> 5] + popc(bits[p >> 5]
+    // & ones up to bit p & 31) -- 12 KB per dimension (2048 u32 boundary-bit
+    // words, then 2048 u16 bases), small enough to stay in L1
+    for (int d = 0; d < 2 && e == cudaSuccess; d++) {
+        std::vector<uint32_t> bk(3072, 0u);
+        for (uint32_t b = 0; b < 2048; b++) {
+            uint32_t bits = 0;
+            for (uint32_t j = 1; j < 32; j++)
+                if (ptab[d][b * 32 + j] != ptab[d][b * 32 + j - 1]) bits |= 1u << j;
+            bk[b] = bits;
+            bk[2048 + b / 2] |= (uint32_t)ptab[d][b * 32] << (16 * (b & 1));
+        }
+        e = ms_upload(&m->d_pbk[d], bk.data(), bk.size());
+    }
     if (e == cudaSuccess) e = ms_upload(&m->d_cls, cls, 256);
     if (e == cudaSuccess) e = ms_upload(&d_sb, src_base, (size_t)n);
     if (e == cudaSuccess) e = ms_upload(&d_sm, src_mask, (size_t)n);
@@ -1898,6 +1924,8 @@ static MsView ms_view(const MatchSet *m) {
     t.ipc[1] = m->d_ipc[1];
     t.port[0] = m->d_port[0];
     t.port[1] = m->d_port[1];
+    t.pbk[0] = m->d_pbk[0];
+    t.pbk[1] = m->d_pbk[1];
     t.cls = m->d_cls;
     t.wp = m->wp;
     t.sp_rows = (uint32_t)m->sp_rows;

@@ -165,6 +165,7 @@ struct MatchSet {
     uint32_t *d_ipb[2] = {};    // src / dst interval boundaries (sorted, [0] = 0)
     uint4 *d_ipc[2] = {};       // per /16 block: first boundary index | count << 24, 6 boundary low halves
     uint16_t *d_port[2] = {};   // sport / dport -> interval (65536 entries each)
+    uint32_t *d_pbk[2] = {};    // the same as 2048 buckets of 32 ports (12 KB: boundary bits, then u16 bases)
     uint8_t *d_cls = nullptr;   // protocol -> class (256 entries)
     int64_t sp_rows = 0;        // sport intervals = rows per protocol class
     size_t bytes = 0;           // device bytes of all of the above
