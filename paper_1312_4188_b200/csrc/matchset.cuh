@@ -19,7 +19,7 @@
 // Layout in HBM (struct MatchSet): the four dimensions' rows in one
 // allocation, rows x wp words each (wp = rules/32 rounded up to a whole step
 // of 128 words, 512 bytes); optional block summaries (one bit per 1024-rule
-// block per row); compressed rows above ~24K rules (each (dimension, 1024-rule
+// block per row); compressed rows above 16K rules (each (dimension, 1024-rule
 // block) stores its distinct lines once, rows hold u16 line indices, a dense
 // head array the first 8 blocks'); IP value -> interval through a 65536-entry
 // table of 16-byte /16-block entries (boundary range + the first 6 boundaries'
@@ -57,10 +57,10 @@ int g_ms_group = 0;            // lanes per packet (8, 16, 32; 0 = by ruleset si
 int g_ms_words = 4;            // words per lane per step: 32 * group * words rules per step
 int g_ms_summary = 2;          // block summaries: 0 off, 1 on, 2 auto (built and used when they skip enough)
 int g_ms_compress = 2;         // compressed rows: 0 off, 1 on, 2 auto (see ms_create)
-// auto: compressed rows above this many rules.  The plain rows' leading lines
-// outgrow L2 there; the compressed rows stay L2-resident and scan at ~8 Gpps
-// flat from 20K to 100K rules (plain: 9.2 Gpps at 20K, 6.4 at 30K, 5.2 at 100K)
-constexpr int64_t MS_CMP_MIN_RULES = 24576;
+// auto: compressed rows above this many rules.  Above it the plain rows'
+// leading lines no longer stay in L2 (r2 sweep, 16Mi packets: plain 12.9 Gpps
+// at 16K rules, 10.1 at 18K, 9.3 at 20K; compressed ~10.6 flat from 10K up)
+constexpr int64_t MS_CMP_MIN_RULES = 16384;
 constexpr double MS_SUM_KEEP_MAX = 0.75;  // auto: use summaries if a packet keeps < 75% of blocks
 int g_ms_lean = 3;             // whole-table plain-row scans: 0 general kernel, 1 lean 8-lane groups, 2 lean 4-lane groups (256-bit loads), 3 auto
 int g_count_blocks = 0;        // count the summary scan's block reads (pfw_read_counter "blocks_read")
@@ -1725,7 +1725,7 @@ int ms_create(pfw_ruleset *h, const uint8_t *proto, const uint32_t *src_base, co
     fits = fits && all_words < (1ull << 32);
     // compressed rows: forced, or (auto) for large rulesets or when the plain
     // rows do not fit -- ~20x smaller; slower than plain rows only while
-    // those stay L2-friendly (<= ~24K rules)
+    // those stay L2-friendly (<= 16K rules)
     const bool use_cmp = g_ms_compress == 1 || (g_ms_compress == 2 && (!fits || n > MS_CMP_MIN_RULES));
     // (boundary indices are packed in 24 bits: beyond ~8M rules the ruleset scans rule by rule)
     if ((!fits && !use_cmp) || bs.size() >= (1u << 24) || bd.size() >= (1u << 24)) {

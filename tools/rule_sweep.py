@@ -26,11 +26,15 @@ def main():
     ap.add_argument("--rule-scan-max", type=int, default=1000000)
     ap.add_argument("--compare-rows", action="store_true",
                     help="also time the match-set scan with plain rows and with compressed rows forced")
+    ap.add_argument("--tune", action="append", default=[], metavar="KEY=VALUE", help="pfw_set_tuning before the sweep")
     args = ap.parse_args()
     import numpy as np
     import torch
     import paper_1312_4188_b200 as pfw
     from paper_1312_4188_b200 import _native
+    for kv in args.tune:
+        k, _, v = kv.partition("=")
+        _native.set_tuning(k, int(v))
     from paper_1312_4188_b200.classifier import NO_MATCH
     from oracle import oracle
     n = args.packets
