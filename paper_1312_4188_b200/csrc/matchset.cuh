@@ -1986,10 +1986,12 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
         return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
     // whole-table scans over plain rows in the default shape: the lean kernel
     void (*kern_l)(ScanParams, MsView, uint32_t) = nullptr;
-    // (auto, measured on B200: 4-lane groups with 256-bit loads up to 2K rules
-    // (oracle config 5.7 vs 5.3 Gpps), above that 8-lane groups with 64-packet
-    // batches (data 13.65 Gpps vs 12.55 on the general kernel, grid 16.15)
-    const int lean = g_ms_lean == 3 ? (h->n <= 2048 ? 2 : 6) : g_ms_lean;
+    // (auto, measured on B200: 4-lane groups with 256-bit loads for rulesets up
+    // to 2K rules in batches under 4Mi packets -- one latency-bound wave: the
+    // oracle config 6.4 vs 5.5 Gpps --, otherwise 8-lane groups with 64-packet
+    // batches: data 13.65 Gpps vs 12.55 on the general kernel, grid 16.15, and
+    // 1K rules x 16Mi packets 27.9 vs 25.7)
+    const int lean = g_ms_lean == 3 ? ((h->n <= 2048 && p.n < (int64_t(1) << 22)) ? 2 : 6) : g_ms_lean;
     // compressed rows, whole table, no summaries: the lean compressed kernel
     // (tuning ms_lean_cmp: 0 off, 1 8-lane groups, 2 4-lane groups / 256-bit loads)
     void (*kern_lc)(ScanParams, MsView, MsCmp, uint32_t) = nullptr;
