@@ -1072,3 +1072,25 @@ def test_lean_compressed_repark_windows(lc, R):
     want = oracle.scan_range(rules, pk, 0, R)
     assert (want < 0).mean() > 0.05  # default deny walks every block
     np.testing.assert_array_equal(c.scan_range(p, 0, R), want)
+
+
+def test_c_abi_argument_errors_new_entry_points():
+    """pfw_scan_partitions / pfw_probe_l2_lines reject bad arguments with
+    PFW_ERR_INVALID (ValueError) before any launch; a valid probe call runs."""
+    c = compiled(oracle.gen_ruleset(100, 3))
+    p = dev_pkts(oracle.gen_traffic_uniform(50, 4))
+    f = torch.empty(50, dtype=torch.int32, device="cuda:0")
+    cm = torch.empty(50, dtype=torch.int32, device="cuda:0")
+    with pytest.raises(ValueError):
+        c.scan_partitions(p, 0, f, cm)
+    lib = _native.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    with pytest.raises(ValueError):
+        _native.check(lib.pfw_scan_partitions(c.handle, 2, p.data.data_ptr(), 50, None, cm.data_ptr(), None, st),
+                      "pfw_scan_partitions")
+    buf = torch.empty(2 << 20, dtype=torch.uint8, device="cuda:0")
+    for k, occ, iters, ok in ((8, 4, 4, True), (3, 4, 4, False), (8, 0, 4, False), (8, 4, 0, False)):
+        rc = lib.pfw_probe_l2_lines(buf.data_ptr(), buf.numel(), k, occ, iters, st)
+        assert (rc == 0) == ok, (k, occ, iters, rc)
+    assert lib.pfw_probe_l2_lines(buf.data_ptr(), 1000, 8, 4, 4, st) != 0   # buffer under 1 MiB
+    torch.cuda.synchronize()
