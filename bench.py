@@ -859,10 +859,12 @@ def run_ours(args, w, world, rank, local) -> int:
         link = host_link_peaks(dev)
         e2e_s = e_s / args.steps
         e2e = {"value": pk_per_step * args.steps / e_s / 1e6, "unit": "Mpps",
-               "h2d_bytes_per_step": n * 13, "d2h_bytes_per_step": n * (9 if fn_e2e else 5),
+               # (one node: the whole-table pipeline, comparisons derived on the host as first + 1
+               # or R; several nodes: pfw_classify_host_partitions copies them out too)
+               "h2d_bytes_per_step": n * 13, "d2h_bytes_per_step": n * (9 if fn_e2e and world > 1 else 5),
                "api": (f"Engine(EngineConfig(FUNCTION_PARALLEL, nodes={world})).run_arrays(compiled, host_columns) "
-                       "-> EngineResult (pfw_classify_host_partitions: the same pipeline, per-packet comparisons "
-                       "copied out too)" if fn_e2e else
+                       "-> EngineResult (one node = the sequential scan exactly: the same chunked H2D / scan / "
+                       "D2H pipeline, first + verdict copied out, per-packet comparisons derived)" if fn_e2e else
                        "Engine(EngineConfig(DATA_PARALLEL)).run_arrays(compiled, host_columns) -> EngineResult "
                        "(the reference's five PacketArrays columns as numpy arrays in pinned host memory; "
                        "pfw_classify_host_ex: chunked H2D / scan / D2H pipeline, copy-in + 2 compute + copy-out "

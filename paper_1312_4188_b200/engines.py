@@ -368,6 +368,13 @@ class Engine:
         self._copies[key] = (weakref.ref(compiled), c)
         return c
 
+    def _whole_table(self, model: ExecutionModel) -> bool:
+        """One scan of [0, R) gives the model's exact results: sequential /
+        data-parallel, and function-parallel / hybrid with one node (a single
+        partition holding every rule: the same first match, per-task
+        comparisons first + 1 or R, and per-task maximum, engines.py:349-369)."""
+        return model in (ExecutionModel.SEQUENTIAL, ExecutionModel.DATA_PARALLEL) or self.config.nodes == 1
+
     # ------------------------------------------------------------- device
     def run_device(self, compiled: CompiledRuleset, pkts: PacketArrays, stream: int | None = None):
         """Launch the configured model on one device; returns device tensors
@@ -379,7 +386,7 @@ class Engine:
         stats = torch.zeros(2, dtype=torch.int64, device=dev)
         model = self.config.model
         R = compiled.num_rules
-        if model in (ExecutionModel.SEQUENTIAL, ExecutionModel.DATA_PARALLEL):
+        if self._whole_table(model):
             first = compiled.scan_range_device(pkts, 0, R, comps=comps, stats=stats, stream=stream)
             return first, comps, stats
         if model not in (ExecutionModel.FUNCTION_PARALLEL, ExecutionModel.HYBRID):
@@ -409,7 +416,7 @@ class Engine:
             z = np.zeros(0, np.int64)
             return EngineResult(z, z, np.zeros(0, np.bool_), ClassifyStats(0, 0, time.perf_counter_ns() - start, 0))
         model = self.config.model
-        seq = model in (ExecutionModel.SEQUENTIAL, ExecutionModel.DATA_PARALLEL)
+        seq = self._whole_table(model)
         if seq and host:
             with _nvtx("Engine.run_arrays: e2e (host batch)"):
                 first, verdict, st = self._data_host(compiled, packets, n)
