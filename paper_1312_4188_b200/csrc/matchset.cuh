@@ -1986,12 +1986,15 @@ int launch_ms_k(pfw_ruleset *h, const ScanParams &p, cudaStream_t st) {
         return set_err(PFW_ERR_INVALID, "ms_group %d x ms_words %d not built", grp, g_ms_words);
     // whole-table scans over plain rows in the default shape: the lean kernel
     void (*kern_l)(ScanParams, MsView, uint32_t) = nullptr;
-    // (auto, measured on B200: 4-lane groups with 256-bit loads for rulesets up
-    // to 2K rules in batches under 4Mi packets -- one latency-bound wave: the
-    // oracle config 6.4 vs 5.5 Gpps --, otherwise 8-lane groups with 64-packet
-    // batches: data 13.65 Gpps vs 12.55 on the general kernel, grid 16.15, and
-    // 1K rules x 16Mi packets 27.9 vs 25.7)
-    const int lean = g_ms_lean == 3 ? ((h->n <= 2048 && p.n < (int64_t(1) << 22)) ? 2 : 6) : g_ms_lean;
+    // (auto, measured on B200: 4-lane groups with 256-bit loads -- twice the
+    // packets in flight per warp -- for batches that fill the GPU only a few
+    // times over: under 768K packets (10K rules x 100K packets 3.7 vs 2.1 Gpps,
+    // x 512K 7.6 vs 7.3), under 4Mi for rulesets up to 2K rules (the oracle
+    // config 6.4 vs 5.5); otherwise 8-lane groups with 64-packet batches: data
+    // 13.65 Gpps vs 12.55 on the general kernel, grid 16.15, 1K rules x 16Mi
+    // packets 27.9 vs 25.7, 10K rules x 1Mi packets 10.3 vs 9.4)
+    const bool small_batch = p.n < (int64_t(3) << 18) || (h->n <= 2048 && p.n < (int64_t(1) << 22));
+    const int lean = g_ms_lean == 3 ? (small_batch ? 2 : 6) : g_ms_lean;
     // compressed rows, whole table, no summaries: the lean compressed kernel
     // (tuning ms_lean_cmp: 0 off, 1 8-lane groups, 2 4-lane groups / 256-bit loads)
     void (*kern_lc)(ScanParams, MsView, MsCmp, uint32_t) = nullptr;
